@@ -1,0 +1,707 @@
+"""CPU oracle for the block-Jacobi / Krylov 7-point stencil path.
+
+TEST INFRASTRUCTURE ONLY.  This module is the *checker*: it restates, in
+plain numpy, the algorithm of the reference package ``blocksolve``
+(``/root/reference/pkg/src/blocksolve``) for the hot path this repository
+accelerates.  Only ``tests/``, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import it.
+The product path (``paper_2009_12638_b200``) never imports or calls it.
+
+Pinning: ``tests/test_oracle_golden.py`` checks every function here against
+golden vectors produced by running the unmodified reference in the build
+container (``tests/golden/make_golden.py``) and against the reference's own
+known-answer tests (restated).  Citations are ``file:line`` into
+``/root/reference/pkg/src/blocksolve``.
+
+Arithmetic notes (the parity contract):
+
+* CSR SpMV (``linalg.py:178-194``) is ``np.add.reduceat`` over the per-row
+  products.  numpy 2.x evaluates a segment as ``t_first + seq(t_rest)``
+  (pairwise summation degenerates to a left-to-right loop below 8 terms);
+  ``stencil_apply`` reproduces that association matrix-free.
+* Dot products go through ``@`` (BLAS) exactly as the reference does, so the
+  oracle's CG/GMRES iterates are bit-identical to the reference's on the same
+  machine; the GPU uses fixed-order tree reductions and is compared within
+  tolerance (iteration counts must match).
+* The block-residual combiner uses Python's built-in ``sum`` (Neumaier
+  compensated on CPython >= 3.12), as ``comm.py:442-445`` does.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Callable
+
+import numpy as np
+
+# --------------------------------------------------------------------------
+# problem definition  (problems.py:37-175)
+# --------------------------------------------------------------------------
+
+FACES = ("x_lo", "x_hi", "y_lo", "y_hi", "z_lo", "z_hi")
+# order in which Dirichlet face values are accumulated into the rhs
+# (problems.py:143-167: z_lo, y_lo, x_lo, [diag], x_hi, y_hi, z_hi)
+RHS_FACE_ORDER = ("z_lo", "y_lo", "x_lo", "x_hi", "y_hi", "z_hi")
+
+
+def _face_values(spec, a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """Evaluate a face spec (constant or callable (u, v)) on index grids."""
+    if callable(spec):
+        out = np.empty(a.shape)
+        for idx in np.ndindex(a.shape):
+            out[idx] = float(spec(int(a[idx]), int(b[idx])))
+        return out
+    return np.full(a.shape, float(spec))
+
+
+def dirichlet_rhs(nx: int, ny: int, nz: int, faces: dict | None = None) -> np.ndarray:
+    """Boundary-folded rhs of ``build_laplace_3d`` (problems.py:136-167).
+
+    Each point starts at 0.0 and receives ``+= value`` for every global face
+    it touches, in the order z_lo, y_lo, x_lo, x_hi, y_hi, z_hi.  Returned
+    flat in x-fastest order (problems.py:110-111).
+    """
+    faces = dict(faces or {})
+    rhs = np.zeros((nz, ny, nx))
+    for face in RHS_FACE_ORDER:
+        spec = faces.get(face, 0.0)
+        if face == "z_lo":
+            jj, ii = np.meshgrid(np.arange(ny), np.arange(nx), indexing="ij")
+            rhs[0, :, :] += _face_values(spec, ii, jj)
+        elif face == "z_hi":
+            jj, ii = np.meshgrid(np.arange(ny), np.arange(nx), indexing="ij")
+            rhs[nz - 1, :, :] += _face_values(spec, ii, jj)
+        elif face == "y_lo":
+            kk, ii = np.meshgrid(np.arange(nz), np.arange(nx), indexing="ij")
+            rhs[:, 0, :] += _face_values(spec, ii, kk)
+        elif face == "y_hi":
+            kk, ii = np.meshgrid(np.arange(nz), np.arange(nx), indexing="ij")
+            rhs[:, ny - 1, :] += _face_values(spec, ii, kk)
+        elif face == "x_lo":
+            kk, jj = np.meshgrid(np.arange(nz), np.arange(ny), indexing="ij")
+            rhs[:, :, 0] += _face_values(spec, jj, kk)
+        elif face == "x_hi":
+            kk, jj = np.meshgrid(np.arange(nz), np.arange(ny), indexing="ij")
+            rhs[:, :, nx - 1] += _face_values(spec, jj, kk)
+    return rhs.ravel()
+
+
+@dataclass
+class CSR:
+    """CSR matrix with strictly increasing columns per row (linalg.py:56-69)."""
+
+    num_rows: int
+    num_cols: int
+    row_offsets: np.ndarray
+    col_indices: np.ndarray
+    values: np.ndarray
+
+    def to_dense(self) -> np.ndarray:
+        a = np.zeros((self.num_rows, self.num_cols))
+        rows = np.repeat(np.arange(self.num_rows), np.diff(self.row_offsets))
+        a[rows, self.col_indices] = self.values
+        return a
+
+
+def laplace_csr(nx: int, ny: int, nz: int) -> CSR:
+    """The 7-point operator of ``build_laplace_3d`` (problems.py:123-175).
+
+    Diagonal 6, -1 for every interior neighbor, entries per row in ascending
+    column order z-1, y-1, x-1, diag, x+1, y+1, z+1.  Vectorised restatement
+    of the reference's Python triple loop.
+    """
+    n = nx * ny * nz
+    p = np.arange(n, dtype=np.int64)
+    i = p % nx
+    j = (p // nx) % ny
+    k = p // (nx * ny)
+    offs = (-nx * ny, -nx, -1, 0, 1, nx, nx * ny)
+    valid = (k > 0, j > 0, i > 0, np.ones(n, bool), i < nx - 1, j < ny - 1, k < nz - 1)
+    vals = (-1.0, -1.0, -1.0, 6.0, -1.0, -1.0, -1.0)
+    cols = np.stack([p + o for o in offs], axis=1)
+    ok = np.stack(valid, axis=1)
+    v = np.broadcast_to(np.asarray(vals), (n, 7))
+    counts = ok.sum(axis=1)
+    offsets = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(counts, out=offsets[1:])
+    return CSR(n, n, offsets, cols[ok].astype(np.int64), np.ascontiguousarray(v[ok]))
+
+
+def csr_spmv(a: CSR, x: np.ndarray) -> np.ndarray:
+    """y = A x exactly as ``linalg.spmv`` evaluates it (linalg.py:178-194)."""
+    x = np.asarray(x, dtype=np.float64)
+    if x.ndim != 1 or x.shape[0] != a.num_cols:
+        raise ValueError("dimension mismatch")
+    out = np.zeros(a.num_rows)
+    if a.values.shape[0] == 0:
+        return out
+    prod = a.values * x[a.col_indices]
+    starts = a.row_offsets[:-1]
+    nonempty = a.row_offsets[1:] > starts
+    out[nonempty] = np.add.reduceat(prod, starts[nonempty])
+    return out
+
+
+# --------------------------------------------------------------------------
+# matrix-free restatement of the same SpMV on a (possibly non-box) region
+# --------------------------------------------------------------------------
+
+
+def _shift(a: np.ndarray, axis: int, step: int, fill) -> np.ndarray:
+    """out[idx] = a[idx + step along axis] (fill outside)."""
+    out = np.full_like(a, fill)
+    src = [slice(None)] * 3
+    dst = [slice(None)] * 3
+    if step < 0:
+        dst[axis] = slice(-step, None)
+        src[axis] = slice(None, step)
+    else:
+        dst[axis] = slice(None, -step)
+        src[axis] = slice(step, None)
+    out[tuple(dst)] = a[tuple(src)]
+    return out
+
+
+def stencil_apply(u3: np.ndarray, region: np.ndarray | None = None) -> np.ndarray:
+    """Principal-submatrix SpMV of the 7-point operator on ``region``.
+
+    ``u3`` has shape (nz, ny, nx); ``region`` is a boolean mask of the rows
+    and columns kept (default: the whole box, i.e. the global operator with
+    zero Dirichlet data).  Reproduces ``csr_spmv`` bit for bit: the present
+    terms t = [-u(z-1), -u(y-1), -u(x-1), 6u, -u(x+1), -u(y+1), -u(z+1)] are
+    combined as ``t_first + (((t_a + t_b) + ...) + t_last)`` (numpy
+    ``reduceat`` semantics); absent terms are exact zeros
+    inside the left-to-right chain, which leaves every partial sum unchanged.
+    Rows outside the region are returned as 0.
+    """
+    if region is None:
+        region = np.ones(u3.shape, dtype=bool)
+    u = np.where(region, u3, 0.0)
+    zm = _shift(u, 0, -1, 0.0)
+    ym = _shift(u, 1, -1, 0.0)
+    xm = _shift(u, 2, -1, 0.0)
+    xp = _shift(u, 2, 1, 0.0)
+    yp = _shift(u, 1, 1, 0.0)
+    zp = _shift(u, 0, 1, 0.0)
+    pz = _shift(region, 0, -1, False)
+    py = _shift(region, 1, -1, False)
+    px = _shift(region, 2, -1, False)
+    t = [-zm, -ym, -xm, 6.0 * u, -xp, -yp, -zp]
+
+    def chain(first: int) -> np.ndarray:
+        s = t[first]
+        for q in range(first + 1, 7):
+            s = s + t[q]
+        return s
+
+    y = np.where(
+        pz,
+        t[0] + chain(1),
+        np.where(py, t[1] + chain(2), np.where(px, t[2] + chain(3), t[3] + chain(4))),
+    )
+    return np.where(region, y, 0.0)
+
+
+# --------------------------------------------------------------------------
+# inner solvers  (inner_solvers.py)
+# --------------------------------------------------------------------------
+
+STAGNATION_RTOL = 1e-14  # inner_solvers.py:37
+
+
+@dataclass
+class Report:
+    """Mirror of ``InnerSolveReport`` (inner_solvers.py:60-67)."""
+
+    iterations_used: int
+    final_relative_residual: float
+    stop_reason: str
+    residual_history: list = field(default_factory=list)
+
+
+def _scale(b: np.ndarray) -> float:
+    """inner_solvers.py:70-72."""
+    bnorm = float(np.linalg.norm(b))
+    return bnorm if bnorm > 0.0 else 1.0
+
+
+def cg(apply: Callable, b, x0, max_iterations: int, tolerance: float = 0.0,
+       basis: str = "rhs"):
+    """Conjugate gradients, restating ``cg_solve`` (inner_solvers.py:102-146).
+
+    ``basis="rhs"`` is the reference semantics (stop when ||r||/||b|| <= tol).
+    ``basis="initial"`` is the r0-relative wrapper of SURVEY §8(c): the
+    reference CG called with ``tol' = tol * ||b - A x0|| / ||b||``.
+    """
+    b = np.asarray(b, dtype=np.float64)
+    x = np.array(x0, dtype=np.float64, copy=True)
+    scale = _scale(b)
+    r = b - apply(x)
+    rel = float(np.linalg.norm(r)) / scale
+    tol = tolerance if basis == "rhs" else tolerance * rel
+    if rel <= tol:
+        return x, Report(0, rel, "tolerance_met")
+    p = r.copy()
+    rr = float(r @ r)
+    history = []
+    it = 0
+    while it < max_iterations:
+        ap = apply(p)
+        pap = float(p @ ap)
+        if pap <= 0.0 or not np.isfinite(pap):
+            return x, Report(it, rel, "breakdown", history)
+        alpha = rr / pap
+        x += alpha * p
+        r -= alpha * ap
+        it += 1
+        rr_new = float(r @ r)
+        rel = np.sqrt(rr_new) / scale
+        history.append(rel)
+        if not np.isfinite(rel):
+            return x, Report(it, rel, "breakdown", history)
+        if rel <= tol:
+            r_true = b - apply(x)
+            rel_true = float(np.linalg.norm(r_true)) / scale
+            if rel_true <= tol:
+                history[-1] = rel_true
+                return x, Report(it, rel_true, "tolerance_met", history)
+            r = r_true
+            rr_new = float(r @ r)
+            rel = np.sqrt(rr_new) / scale
+            history[-1] = rel
+        beta = rr_new / rr
+        p = r + beta * p
+        rr = rr_new
+    return x, Report(it, rel, "max_iterations", history)
+
+
+def _back_substitute(u: np.ndarray, rhs: np.ndarray) -> np.ndarray:
+    """inner_solvers.py:246-251."""
+    y = np.zeros_like(rhs)
+    for i in range(rhs.shape[0] - 1, -1, -1):
+        y[i] = (rhs[i] - u[i, i + 1:] @ y[i + 1:]) / u[i, i]
+    return y
+
+
+def gmres(apply: Callable, b, x0, max_iterations: int, tolerance: float = 0.0,
+          restart: int | None = None, basis: str = "rhs"):
+    """Restarted GMRES(m) with MGS Arnoldi + Givens, restating
+    ``gmres_solve`` (inner_solvers.py:149-243)."""
+    b = np.asarray(b, dtype=np.float64)
+    x = np.array(x0, dtype=np.float64, copy=True)
+    n = b.shape[0]
+    m = min(restart if restart is not None else 30, n)
+    scale = _scale(b)
+    tol = tolerance
+    if basis == "initial":
+        tol = tolerance * (float(np.linalg.norm(b - apply(x))) / scale)
+    history: list = []
+    total = 0
+    v = np.zeros((m + 1, n))
+    h = np.zeros((m + 1, m))
+    cs = np.zeros(m)
+    sn = np.zeros(m)
+    g = np.zeros(m + 1)
+
+    def form(j: int) -> np.ndarray:
+        y = _back_substitute(h[: j + 1, : j + 1], g[: j + 1])
+        return x + v[: j + 1].T @ y
+
+    while True:
+        r = b - apply(x)
+        beta = float(np.linalg.norm(r))
+        rel = beta / scale
+        if total == 0 and rel <= tol:
+            return x, Report(0, rel, "tolerance_met")
+        cycle_start = rel
+        h[:] = 0.0
+        g[:] = 0.0
+        g[0] = beta
+        v[0] = r / beta
+        for j in range(m):
+            w = apply(v[j])
+            for i in range(j + 1):
+                h[i, j] = float(v[i] @ w)
+                w -= h[i, j] * v[i]
+            wnorm = float(np.linalg.norm(w))
+            h[j + 1, j] = wnorm
+            happy = wnorm <= 1e-14 * max(float(np.linalg.norm(h[: j + 2, j])), 1e-300)
+            for i in range(j):
+                hij = cs[i] * h[i, j] + sn[i] * h[i + 1, j]
+                h[i + 1, j] = -sn[i] * h[i, j] + cs[i] * h[i + 1, j]
+                h[i, j] = hij
+            denom = float(np.hypot(h[j, j], h[j + 1, j]))
+            cs[j] = h[j, j] / denom
+            sn[j] = h[j + 1, j] / denom
+            h[j, j] = denom
+            h[j + 1, j] = 0.0
+            g[j + 1] = -sn[j] * g[j]
+            g[j] = cs[j] * g[j]
+            total += 1
+            rel = abs(g[j + 1]) / scale
+            history.append(rel)
+            if happy:
+                x = form(j)
+                rel = float(np.linalg.norm(b - apply(x))) / scale
+                history[-1] = rel
+                return x, Report(total, rel, "tolerance_met", history)
+            if rel <= tol or total >= max_iterations:
+                x = form(j)
+                rel_true = float(np.linalg.norm(b - apply(x))) / scale
+                if rel_true <= tol:
+                    history[-1] = rel_true
+                    return x, Report(total, rel_true, "tolerance_met", history)
+                if total >= max_iterations:
+                    return x, Report(total, rel_true, "max_iterations", history)
+                break
+            if j == m - 1:
+                x = form(j)
+                break
+            v[j + 1] = w / wnorm
+        rel_true = float(np.linalg.norm(b - apply(x))) / scale
+        if not np.isfinite(rel_true):
+            return x, Report(total, rel_true, "breakdown", history)
+        if cycle_start - rel_true < STAGNATION_RTOL * cycle_start:
+            return x, Report(total, rel_true, "breakdown", history)
+
+
+# --------------------------------------------------------------------------
+# decomposition  (problems.py:178-359)
+# --------------------------------------------------------------------------
+
+
+def split_ranges(n: int, g: int) -> list:
+    """problems.py:216-225: near-equal ranges, remainder to the low blocks."""
+    base, rem = divmod(n, g)
+    out, start = [], 0
+    for b in range(g):
+        w = base + (1 if b < rem else 0)
+        out.append((start, start + w))
+        start += w
+    return out
+
+
+def owned_boxes(shape, block_grid) -> list:
+    """Owned boxes in block-id order bx fastest (problems.py:322-328).
+
+    Each box is ((x0, y0, z0), (x1, y1, z1)), half open.
+    """
+    nx, ny, nz = shape
+    gx, gy, gz = block_grid
+    rx, ry, rz = split_ranges(nx, gx), split_ranges(ny, gy), split_ranges(nz, gz)
+    boxes = []
+    for bz in range(gz):
+        for by in range(gy):
+            for bx in range(gx):
+                boxes.append(((rx[bx][0], ry[by][0], rz[bz][0]),
+                              (rx[bx][1], ry[by][1], rz[bz][1])))
+    return boxes
+
+
+def dilate(mask: np.ndarray, steps: int) -> np.ndarray:
+    """7-point dilation of a (nz, ny, nx) mask (problems.py:178-190)."""
+    out = mask.copy()
+    for _ in range(steps):
+        grown = out.copy()
+        for axis in range(3):
+            grown |= _shift(out, axis, -1, False)
+            grown |= _shift(out, axis, 1, False)
+        out = grown
+    return out
+
+
+def region_mask(shape, box, overlap: int) -> np.ndarray:
+    """Extended region = owned box dilated ``overlap`` times, computed
+    analytically as the L1 ball {p : dist_1(p, box) <= overlap} (equal to
+    ``_dilate`` of the box mask, problems.py:330-340)."""
+    nx, ny, nz = shape
+    (x0, y0, z0), (x1, y1, z1) = box
+    k, j, i = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    d = (np.maximum(0, np.maximum(x0 - i, i - (x1 - 1)))
+         + np.maximum(0, np.maximum(y0 - j, j - (y1 - 1)))
+         + np.maximum(0, np.maximum(z0 - k, k - (z1 - 1))))
+    return d <= overlap
+
+
+@dataclass
+class Workspace:
+    """Per-block geometry and payload maps (multisplit.py:122-163, 198-330)."""
+
+    block_id: int
+    ext: np.ndarray
+    a_ii: CSR
+    coupling: CSR
+    halo_cols: np.ndarray
+    b_ext: np.ndarray
+    b_owned_norm: float
+    b_global_norm: float
+    owned_global: np.ndarray
+    owned_local: np.ndarray
+    shared_local: np.ndarray
+    m_halo: np.ndarray
+    m_shared: np.ndarray
+    neighbors: list
+    send_idx: dict = field(default_factory=dict)
+    recv_halo: dict = field(default_factory=dict)
+    recv_shared: dict = field(default_factory=dict)
+    owner_halo_map: dict = field(default_factory=dict)
+    owner_shared_map: dict = field(default_factory=dict)
+    payload_len: dict = field(default_factory=dict)
+
+
+def _sub_csr(a: CSR, rows: np.ndarray, col_map: np.ndarray, keep_cols) -> tuple:
+    """Rows ``rows`` of ``a`` split into (kept, dropped) column sets."""
+    counts = a.row_offsets[rows + 1] - a.row_offsets[rows]
+    total = int(counts.sum())
+    pos = np.repeat(a.row_offsets[rows], counts) + (
+        np.arange(total) - np.repeat(np.cumsum(counts) - counts, counts))
+    local_rows = np.repeat(np.arange(rows.shape[0]), counts)
+    cols = a.col_indices[pos]
+    vals = a.values[pos]
+    inside = keep_cols[cols]
+    return local_rows, cols, vals, inside
+
+
+def _csr_from_rows(m: int, ncols: int, rows, cols, vals) -> CSR:
+    order = np.lexsort((cols, rows))
+    rows, cols, vals = rows[order], cols[order], vals[order]
+    off = np.zeros(m + 1, dtype=np.int64)
+    np.add.at(off, rows + 1, 1)
+    np.cumsum(off, out=off)
+    return CSR(m, ncols, off, cols.astype(np.int64), vals.astype(np.float64))
+
+
+def build_workspaces(shape, b: np.ndarray, block_grid, overlap: int,
+                     a: CSR | None = None) -> tuple:
+    """Restates ``decompose`` + ``build_workspaces``
+    (problems.py:287-406, multisplit.py:198-330) for small grids."""
+    nx, ny, nz = shape
+    n = nx * ny * nz
+    if a is None:
+        a = laplace_csr(nx, ny, nz)
+    boxes = owned_boxes(shape, block_grid)
+    masks = [region_mask(shape, box, overlap) for box in boxes]
+    exts = [np.nonzero(mk.ravel())[0] for mk in masks]
+    cover = np.zeros(n, dtype=np.int64)
+    for mk in masks:
+        cover += mk.ravel()
+    reach = [dilate(mk, 1) for mk in masks]
+    nb = len(boxes)
+    neighbors = [[] for _ in range(nb)]
+    for p in range(nb):
+        for q in range(p + 1, nb):
+            if np.any(reach[p] & masks[q]):
+                neighbors[p].append(q)
+                neighbors[q].append(p)
+    b_global_norm = float(np.linalg.norm(b))
+    wss = []
+    for blk in range(nb):
+        ext = exts[blk]
+        in_ext = np.zeros(n, dtype=bool)
+        in_ext[ext] = True
+        local_of = np.full(n, -1, dtype=np.int64)
+        local_of[ext] = np.arange(ext.shape[0])
+        rows, cols, vals, inside = _sub_csr(a, ext, local_of, in_ext)
+        a_ii = _csr_from_rows(ext.shape[0], ext.shape[0], rows[inside],
+                              local_of[cols[inside]], vals[inside])
+        halo_cols = np.unique(cols[~inside])
+        coupling = _csr_from_rows(ext.shape[0], halo_cols.shape[0], rows[~inside],
+                                  np.searchsorted(halo_cols, cols[~inside]), vals[~inside])
+        (x0, y0, z0), (x1, y1, z1) = boxes[blk]
+        owned = (np.arange(x0, x1)[None, None, :]
+                 + nx * (np.arange(y0, y1)[None, :, None]
+                         + ny * np.arange(z0, z1)[:, None, None])).ravel()
+        owned_local = np.searchsorted(ext, owned)
+        mask = np.zeros(ext.shape[0], bool)
+        mask[owned_local] = True
+        shared_local = np.nonzero(~mask)[0]
+        wss.append(Workspace(
+            block_id=blk, ext=ext, a_ii=a_ii, coupling=coupling, halo_cols=halo_cols,
+            b_ext=b[ext].copy(), b_owned_norm=float(np.linalg.norm(b[owned])),
+            b_global_norm=b_global_norm, owned_global=owned, owned_local=owned_local,
+            shared_local=shared_local, m_halo=cover[halo_cols].astype(float),
+            m_shared=cover[ext[shared_local]].astype(float),
+            neighbors=list(neighbors[blk])))
+
+    def owned_by(q, pts):
+        (qx0, qy0, qz0), (qx1, qy1, qz1) = boxes[q]
+        i, j, k = pts % nx, (pts // nx) % ny, pts // (nx * ny)
+        return (qx0 <= i) & (i < qx1) & (qy0 <= j) & (j < qy1) & (qz0 <= k) & (k < qz1)
+
+    for blk, ws in enumerate(wss):
+        shared_global = ws.ext[ws.shared_local]
+        need = np.union1d(shared_global, ws.halo_cols)
+        for q in ws.neighbors:
+            shipped = np.intersect1d(exts[q], need, assume_unique=True)
+            wss[q].send_idx[blk] = np.searchsorted(exts[q], shipped)
+            ws.payload_len[q] = int(shipped.shape[0])
+            own_q = owned_by(q, shipped)
+            in_halo = np.isin(shipped, ws.halo_cols)
+            ws.recv_halo[q] = (np.nonzero(in_halo)[0],
+                               np.searchsorted(ws.halo_cols, shipped[in_halo]))
+            sel = in_halo & own_q
+            ws.owner_halo_map[q] = (np.nonzero(sel)[0],
+                                    np.searchsorted(ws.halo_cols, shipped[sel]))
+            in_sh = np.isin(shipped, shared_global)
+            ws.recv_shared[q] = (np.nonzero(in_sh)[0],
+                                 np.searchsorted(shared_global, shipped[in_sh]))
+            sel = in_sh & own_q
+            ws.owner_shared_map[q] = (np.nonzero(sel)[0],
+                                      np.searchsorted(shared_global, shipped[sel]))
+    return boxes, wss, neighbors, cover
+
+
+# --------------------------------------------------------------------------
+# outer sweep  (multisplit.py:333-426, 544-797) — synchronous replay
+# --------------------------------------------------------------------------
+
+
+@dataclass
+class OracleTraceRow:
+    outer_iteration: int
+    estimated_residual: float
+    true_residual: float | None
+    inner_iterations: int
+
+
+@dataclass
+class OracleResult:
+    solution: np.ndarray
+    rows: list
+    converged: bool
+    outer_iterations: int
+    final_true_residual: float
+    per_block_inner: list  # [k][block] inner iterations
+    snapshots: list = field(default_factory=list)
+
+
+def true_relative_residual(a: CSR, b: np.ndarray, x: np.ndarray) -> float:
+    """multisplit.py:404-406 -> linalg.residual_norms (linalg.py:197-205)."""
+    r = b - csr_spmv(a, x)
+    bnorm = float(np.linalg.norm(b))
+    if bnorm == 0.0:
+        raise ZeroDivisionError("relative residual undefined for a zero rhs")
+    return float(np.linalg.norm(r)) / bnorm
+
+
+def outer_solve_sync(shape, b: np.ndarray, block_grid, overlap: int, inner: dict,
+                     tol: float = 1e-6, max_outer: int = 5000,
+                     residual_check_mode: str = "paper",
+                     true_residual_interval: int = 10,
+                     capture_iterates: bool = False) -> OracleResult:
+    """Synchronous two-stage solve (multisplit.py:544-797, replay execution).
+
+    ``inner`` = dict(kind="cg"|"gmres", max_iterations, tolerance, restart,
+    basis="rhs"|"initial").  Sync exchanges deliver every neighbor's
+    iteration-k payload, so the schedule is plain block Jacobi and the
+    result does not depend on worker order.
+    """
+    nx, ny, nz = shape
+    a = laplace_csr(nx, ny, nz)
+    boxes, wss, neighbors, cover = build_workspaces(shape, b, block_grid, overlap, a)
+    kind = inner["kind"]
+    max_its = inner["max_iterations"]
+    itol = inner.get("tolerance", 0.0)
+    basis = inner.get("basis", "rhs")
+    restart = inner.get("restart")
+    if kind == "gmres" and restart is None:
+        restart = max_its  # multisplit.py:532-536
+    nb = len(wss)
+    # per-block state (multisplit.py:151-163)
+    xs = [np.zeros(ws.ext.shape[0]) for ws in wss]
+    halo = [np.zeros(ws.halo_cols.shape[0]) for ws in wss]
+    own_shared = [np.zeros(ws.shared_local.shape[0]) for ws in wss]
+    owner_halo = [np.zeros(ws.halo_cols.shape[0]) for ws in wss]
+    owner_shared = [np.zeros(ws.shared_local.shape[0]) for ws in wss]
+    rows, per_block_inner, snapshots = [], [], []
+    converged = False
+    k = 0
+    solution = np.zeros(a.num_rows)
+    last_true = {}
+    while True:
+        its_k = []
+        for blk, ws in enumerate(wss):
+            rhs = ws.b_ext.copy()
+            if ws.halo_cols.size:
+                rhs -= csr_spmv(ws.coupling, halo[blk])
+            ap = (lambda v, m=ws.a_ii: csr_spmv(m, v))
+            if kind == "cg":
+                x_new, rep = cg(ap, rhs, xs[blk], max_its, itol, basis)
+            else:
+                x_new, rep = gmres(ap, rhs, xs[blk], max_its, itol, restart, basis)
+            if rep.stop_reason == "breakdown":
+                raise RuntimeError(f"breakdown in block {blk} at outer iteration {k}")
+            xs[blk] = x_new
+            own_shared[blk] = x_new[ws.shared_local].copy()
+            its_k.append(rep.iterations_used)
+        payloads = [{q: xs[blk][wss[blk].send_idx[q]] for q in wss[blk].neighbors}
+                    for blk in range(nb)]
+        locals_ = []
+        for blk, ws in enumerate(wss):
+            # merge_overlap (multisplit.py:341-369)
+            if ws.halo_cols.size:
+                acc = np.zeros(ws.halo_cols.shape[0])
+                for q in ws.neighbors:
+                    pl = payloads[q][blk]
+                    sel, slots = ws.recv_halo[q]
+                    if sel.size:
+                        acc[slots] += pl[sel]
+                    sel, slots = ws.owner_halo_map[q]
+                    if sel.size:
+                        owner_halo[blk][slots] = pl[sel]
+                halo[blk] = acc / ws.m_halo
+            if ws.shared_local.size:
+                acc = own_shared[blk].copy()
+                for q in ws.neighbors:
+                    pl = payloads[q][blk]
+                    sel, slots = ws.recv_shared[q]
+                    if sel.size:
+                        acc[slots] += pl[sel]
+                    sel, slots = ws.owner_shared_map[q]
+                    if sel.size:
+                        owner_shared[blk][slots] = pl[sel]
+                xs[blk][ws.shared_local] = acc / ws.m_shared
+            # local_relative_residual (multisplit.py:372-396)
+            if ws.shared_local.size:
+                xv = xs[blk].copy()
+                xv[ws.shared_local] = owner_shared[blk]
+            else:
+                xv = xs[blk]
+            r = ws.b_ext - csr_spmv(ws.a_ii, xv)
+            if ws.halo_cols.size:
+                r -= csr_spmv(ws.coupling, owner_halo[blk])
+            num = float(np.linalg.norm(r[ws.owned_local]))
+            den = ws.b_owned_norm or ws.b_global_norm or 1.0
+            locals_.append(num / den)
+        total = float(sum(locals_[w] ** 2 for w in range(nb)))  # comm.py:442-445
+        estimate = math.sqrt(total)
+        for ws in wss:
+            solution[ws.owned_global] = xs[ws.block_id][ws.owned_local]
+        want_true = residual_check_mode == "true" or k % true_residual_interval == 0
+        sample = true_relative_residual(a, b, solution) if want_true else None
+        if capture_iterates:
+            snapshots.append((k, solution.copy()))
+        rows.append(OracleTraceRow(k, estimate, sample, int(sum(its_k))))
+        per_block_inner.append(its_k)
+        if sample is not None:
+            last_true[k] = sample
+        # check_termination (multisplit.py:409-426) then the driver's
+        # true-mode stop request (multisplit.py:685-686)
+        if estimate < tol or k + 1 >= max_outer:
+            converged = estimate < tol
+            break
+        if residual_check_mode == "true" and sample is not None and sample < tol:
+            converged = True
+            break
+        k += 1
+    final_true = true_relative_residual(a, b, solution)
+    if rows and rows[-1].true_residual is None:
+        rows[-1].true_residual = final_true
+    return OracleResult(solution, rows, converged, len(rows), final_true,
+                        per_block_inner, snapshots)
+
+
+def seeded_rhs(n: int, seed: int = 0) -> np.ndarray:
+    """SURVEY §8(d) convention: default_rng(seed).uniform(-1, 1, n), x-fastest."""
+    return np.random.default_rng(seed).uniform(-1.0, 1.0, n)

@@ -1,0 +1,198 @@
+"""Pin the CPU oracle against the reference's golden vectors and its own
+known-answer tests (restated).  CPU only."""
+
+import numpy as np
+import pytest
+
+from golden_io import arrays, meta
+from oracle import blocksolve_oracle as O
+
+
+def lap(shape):
+    return O.laplace_csr(*shape)
+
+
+# ---------------------------------------------------------------- assembly
+
+
+def test_assembly_bit_equal_to_reference():
+    A, M = arrays(), meta()["assembly"]
+    a = lap(M["shape"])
+    assert np.array_equal(a.row_offsets, A["assembly/offsets"])
+    assert np.array_equal(a.col_indices, A["assembly/cols"])
+    assert np.array_equal(a.values, A["assembly/vals"])
+    rhs = O.dirichlet_rhs(*M["shape"], M["faces"])
+    assert np.array_equal(rhs, A["assembly/rhs"])
+
+
+def test_callable_face_rhs():
+    rhs = O.dirichlet_rhs(3, 4, 2, {"y_lo": lambda i, k: 0.5 * i + k, "z_hi": 1.5})
+    assert np.array_equal(rhs, arrays()["assembly_callable/rhs"])
+
+
+def test_known_answers_assembly():
+    # test_problems.py:41-76 restated: [[6]]/[6]; 3x1x1 chain; mixed faces
+    a = lap((1, 1, 1))
+    assert np.array_equal(a.to_dense(), [[6.0]])
+    assert np.array_equal(O.dirichlet_rhs(1, 1, 1, {f: 1.0 for f in O.FACES}), [6.0])
+    chain = lap((3, 1, 1)).to_dense()
+    assert np.array_equal(chain[1], [-1.0, 6.0, -1.0])
+    rhs = O.dirichlet_rhs(2, 1, 1, {"x_lo": 2.0, "x_hi": 0.0, "y_lo": 0.25, "y_hi": 0.25})
+    assert np.array_equal(rhs, [2.5, 0.5])
+
+
+# ---------------------------------------------------------------- spmv
+
+
+@pytest.mark.parametrize("shape", [(6, 5, 4), (16, 16, 16), (7, 1, 3)])
+def test_csr_spmv_bit_equal(shape):
+    A = arrays()
+    key = "spmv/%dx%dx%d" % shape
+    y = O.csr_spmv(lap(shape), A[key + "/x"])
+    assert np.array_equal(y, A[key + "/y"])
+
+
+@pytest.mark.parametrize("shape", [(6, 5, 4), (16, 16, 16), (7, 1, 3)])
+def test_matrix_free_stencil_bit_equal(shape):
+    A = arrays()
+    key = "spmv/%dx%dx%d" % shape
+    nx, ny, nz = shape
+    y = O.stencil_apply(A[key + "/x"].reshape(nz, ny, nx)).ravel()
+    assert np.array_equal(y, A[key + "/y"])
+
+
+def _blocksys_keys():
+    return [k for k in meta() if k.startswith("blocksys/")]
+
+
+@pytest.mark.parametrize("key", _blocksys_keys())
+def test_block_regions_and_block_spmv(key):
+    """decompose (extended = L1 ball) + principal-submatrix SpMV, bitwise."""
+    A, M = arrays(), meta()[key]
+    shape, bg, ov = tuple(M["shape"]), tuple(M["block_grid"]), M["overlap"]
+    nx, ny, nz = shape
+    boxes = O.owned_boxes(shape, bg)
+    cover = np.zeros(nx * ny * nz, dtype=np.int64)
+    for b, box in enumerate(boxes):
+        mask = O.region_mask(shape, box, ov)
+        # analytic L1 ball == the reference's repeated 7-point dilation
+        seed = np.zeros((nz, ny, nx), bool)
+        (x0, y0, z0), (x1, y1, z1) = box
+        seed[z0:z1, y0:y1, x0:x1] = True
+        assert np.array_equal(mask, O.dilate(seed, ov))
+        ext = np.nonzero(mask.ravel())[0]
+        assert np.array_equal(ext, A[f"{key}/{b}/ext"])
+        cover += mask.ravel()
+        x = A[f"{key}/{b}/x"]
+        u = np.zeros(nx * ny * nz)
+        u[ext] = x
+        y = O.stencil_apply(u.reshape(nz, ny, nx), mask).ravel()[ext]
+        assert np.array_equal(y, A[f"{key}/{b}/y"])
+    assert np.array_equal(cover, A[key + "/cover"])
+    _, wss, nbrs, _ = O.build_workspaces(shape, np.zeros(nx * ny * nz), bg, ov)
+    assert nbrs == M["neighbors"]
+
+
+def test_spmv_known_answers():
+    # test_linalg.py:62-93 restated on the stencil
+    y = O.csr_spmv(lap((4, 4, 4)), np.ones(64))
+    assert y[1 + 4 * (1 + 4 * 1)] == 0.0
+    assert np.array_equal(O.csr_spmv(lap((3, 1, 1)), np.ones(3)), [5.0, 4.0, 5.0])
+
+
+# ---------------------------------------------------------------- CG / GMRES
+
+
+def _cg_case(key):
+    n = int(key.split("/")[1].split("_")[0])
+    seed = int(key.split("seed")[1])
+    b = O.seeded_rhs(n ** 3, seed)
+    a = lap((n, n, n))
+    return a, b, n
+
+
+@pytest.mark.parametrize("key", ["cg/12_seed0", "cg/20_seed1", "cg/32_seed0"])
+def test_cg_matches_reference(key):
+    A, M = arrays(), meta()[key]
+    a, b, n = _cg_case(key)
+    tol = {"cg/12_seed0": 1e-8, "cg/20_seed1": 1e-10, "cg/32_seed0": 1e-8}[key]
+    x, rep = O.cg(lambda v: O.csr_spmv(a, v), b, np.zeros(n ** 3), 10 * n, tol)
+    assert rep.iterations_used == M["iterations_used"]
+    assert rep.stop_reason == M["stop_reason"]
+    assert np.allclose(rep.residual_history, M["residual_history"], rtol=1e-12, atol=0)
+    assert np.abs(x - A[key + "/x"]).max() <= 1e-13 * np.abs(A[key + "/x"]).max()
+
+
+def test_cg_warm_start_and_initial_basis():
+    A, M = arrays(), meta()
+    n = 10
+    a = lap((n, n, n))
+    b = O.dirichlet_rhs(n, n, n, {"z_lo": 1.0})
+    x0 = A["cg/warm/x0"]
+    ap = lambda v: O.csr_spmv(a, v)
+    x, rep = O.cg(ap, b, x0, 17, 1e-3)
+    assert rep.iterations_used == M["cg/warm"]["iterations_used"] == 17
+    assert rep.stop_reason == "max_iterations"
+    assert np.allclose(x, A["cg/warm/x"], rtol=0, atol=1e-13)
+    x, rep = O.cg(ap, b, x0, 200, 1e-3, basis="initial")
+    assert rep.iterations_used == M["cg/warm_initial"]["iterations_used"]
+    assert np.allclose(x, A["cg/warm_initial/x"], rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("key", ["gmres/8_200_10", "gmres/10_30_30", "gmres/6_40_7"])
+def test_gmres_matches_reference(key):
+    A, M = arrays(), meta()[key]
+    _, n, its, restart = key.replace("/", "_").split("_")
+    n, its, restart = int(n), int(its), int(restart)
+    tol = {"gmres/8_200_10": 1e-10, "gmres/10_30_30": 1e-3, "gmres/6_40_7": 0.0}[key]
+    a = lap((n, n, n))
+    b = O.dirichlet_rhs(n, n, n, {"x_lo": 1.0, "y_hi": 0.5})
+    x, rep = O.gmres(lambda v: O.csr_spmv(a, v), b, np.zeros(n ** 3), its, tol, restart)
+    assert rep.iterations_used == M["iterations_used"]
+    assert rep.stop_reason == M["stop_reason"]
+    assert np.allclose(rep.residual_history, M["residual_history"], rtol=1e-10, atol=1e-300)
+    assert np.abs(x - A[key + "/x"]).max() <= 1e-12 * max(1.0, np.abs(x).max())
+
+
+def test_cg_known_answers():
+    # test_inner_solvers.py:91-130 restated
+    ident = lambda v: v.copy()
+    b = np.array([2.0, -1.0, 0.5])
+    x, rep = O.cg(ident, b, np.zeros(3), 5, 1e-12)
+    assert rep.iterations_used == 1 and np.allclose(x, b, atol=1e-15)
+    x, rep = O.cg(lambda v: np.array([1.0, -1.0]) * v, np.ones(2), np.zeros(2), 10, 1e-10)
+    assert rep.stop_reason == "breakdown"
+
+
+# ---------------------------------------------------------------- outer sync
+
+
+OUTER = ["outer/cfg1_16_fixed", "outer/cfg1_16_literal", "outer/cfg3_16_paper",
+         "outer/cfg3_16_true", "outer/box_12_222", "outer/cfg5_12_o2", "outer/o1_10_211"]
+
+
+@pytest.mark.parametrize("key", OUTER)
+def test_outer_sync_matches_reference_trace(key):
+    A, M = arrays(), meta()[key]
+    c = M["case"]
+    n = c["n"]
+    kind, its, itol = c["inner"]
+    res = O.outer_solve_sync((n, n, n), A[key + "/rhs"], tuple(c["bg"]), c["ov"],
+                             dict(kind=kind, max_iterations=its, tolerance=itol),
+                             tol=c["tol"], max_outer=c.get("max_outer", 5000),
+                             residual_check_mode=c["mode"])
+    assert res.converged == M["converged"]
+    assert res.outer_iterations == M["outer_iterations"]
+    ref_rows = M["trace"]
+    assert len(res.rows) == len(ref_rows)
+    for row, ref in zip(res.rows, ref_rows):
+        assert row.outer_iteration == ref[0]
+        assert row.inner_iterations == ref[4]
+        assert row.estimated_residual == pytest.approx(ref[2], rel=1e-10)
+        if ref[3] is None:
+            assert row.true_residual is None
+        else:
+            assert row.true_residual == pytest.approx(ref[3], rel=1e-10)
+    assert res.final_true_residual == pytest.approx(M["final_true_residual"], rel=1e-10)
+    sol = A[key + "/solution"]
+    assert np.linalg.norm(res.solution - sol) <= 1e-12 * np.linalg.norm(sol)
