@@ -1,0 +1,156 @@
+/*
+ * blocksolve_b200.h — C ABI of the B200 (sm_100a) block-Jacobi / Krylov
+ * 7-point stencil engine (libbsgpu.so).
+ *
+ * The reference package `blocksolve` is pure Python and has no FFI; its seam
+ * is the Python solver API.  Each entry point below replaces the numerical
+ * core of one reference function (cited file:line into
+ * /root/reference/pkg/src/blocksolve).  The Python host layer
+ * (paper_2009_12638_b200/) binds these through ctypes and keeps the
+ * reference's signatures and error behaviour.
+ *
+ * Conventions
+ *  - All vectors are fp64, x-fastest (index = i + nx*(j + ny*k),
+ *    problems.py:110-111), laid out over each block's *padded box*: the owned
+ *    box dilated by `overlap` and clipped to the grid (the bounding box of the
+ *    block's extended region, problems.py:330-340).
+ *  - Pointers are device pointers; `stream` is a cudaStream_t (NULL = legacy).
+ *  - Every call returns 0 on success, a negative BS_E* code on failure;
+ *    bs_last_error() returns a thread-local message for the last failure.
+ *  - Calls are asynchronous on `stream` unless documented as blocking.
+ */
+#ifndef BLOCKSOLVE_B200_H
+#define BLOCKSOLVE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BS_ABI_VERSION 1
+
+#define BS_OK 0
+#define BS_EINVAL -1   /* bad argument  -> ValueError / ConfigurationError */
+#define BS_ECUDA -2    /* CUDA runtime failure -> RuntimeError              */
+#define BS_ESTATE -3   /* call out of protocol order -> ProtocolError       */
+
+/* inner-solver stop reasons (inner_solvers.py:64) */
+#define BS_STOP_NONE 0
+#define BS_STOP_TOLERANCE_MET 1
+#define BS_STOP_MAX_ITERATIONS 2
+#define BS_STOP_BREAKDOWN 3
+
+/* tolerance basis: "rhs" is the reference (inner_solvers.py:70-72,108-113);
+ * "initial" measures against ||b - A x0|| (SURVEY §8(c) wrapper). */
+#define BS_BASIS_RHS 0
+#define BS_BASIS_INITIAL 1
+
+#define BS_KIND_CG 0
+#define BS_KIND_GMRES 1
+
+/* Direction order = ascending global column order of the stencil
+ * (problems.py:142-167): 0 z-1, 1 y-1, 2 x-1, 3 x+1, 4 y+1, 5 z+1. */
+#define BS_NDIR 6
+
+typedef struct bs_block_desc {
+    int32_t global_dims[3];  /* nx, ny, nz of the interior grid (Grid3D)    */
+    int32_t owned_lo[3];     /* owned box, half-open, (x,y,z) (problems.py:193-213) */
+    int32_t owned_hi[3];
+    int32_t overlap;         /* L1 dilation radius o (problems.py:178-190)  */
+    double *x;               /* iterate over the padded box (holds halo values at
+                                non-region cells when overlap > 0)          */
+    double *r;               /* residual scratch                            */
+    double *p0, *p1;         /* ping-pong search directions                 */
+    const double *b;         /* global rhs restricted to the padded box     */
+    double *ghost[BS_NDIR];  /* halo planes just outside the padded box (NULL
+                                where the face lies on the global boundary) */
+    double *history;         /* device residual history, history_cap entries */
+    int32_t history_cap;
+} bs_block_desc;
+
+/* Per-block solver report, host side (InnerSolveReport, inner_solvers.py:60-67,
+ * plus the squared sums the outer sweep needs, multisplit.py:372-406). */
+typedef struct bs_block_report {
+    int32_t phase;
+    int32_t stop_reason;
+    int32_t iterations_used;
+    int32_t pending_flush;
+    double final_relative_residual;
+    double rhs_sq;       /* ||rhs||^2 of the last residual sweep            */
+    double r_sq;         /* ||rhs - A x||^2 over the region                 */
+    double r_owned_sq;   /* same restricted to owned rows (local residual)  */
+    double rglob_owned_sq; /* ||b - A_global x||^2 over owned rows (true mode) */
+    double scale;
+} bs_block_report;
+
+typedef struct bs_ctx bs_ctx;
+
+int bs_abi_version(void);
+const char *bs_last_error(void);
+
+/* Create an engine over `nblocks` blocks resident on `device`.  z_chunk = 0
+ * picks the z-depth of a CTA tile automatically.  The descriptor table is
+ * copied; the buffers stay owned by the caller. */
+int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_chunk,
+                  bs_ctx **out);
+int bs_ctx_destroy(bs_ctx *ctx);
+int bs_ctx_num_ctas(const bs_ctx *ctx);
+
+/* a1: y = A_ii x on block `block`'s region — the principal-submatrix SpMV
+ * (linalg.py:178-194 on problems.py:362-406's A_ii), bit-identical to the
+ * reference's reduceat association.  Values of y outside the region are 0. */
+int bs_stencil_apply(bs_ctx *ctx, int block, const double *x, double *y, void *stream);
+
+/* a2: arm an inner CG solve on every block with active[b] != 0
+ * (inner_solvers.py:102-146, dispatched from multisplit.py:562-563).
+ * active == NULL arms all blocks.  The right-hand side is assembled on the
+ * device as b - C*ghost (multisplit.py:333-338); x is the warm start. */
+int bs_cg_begin(bs_ctx *ctx, int max_iterations, double tolerance, int basis,
+                const int32_t *active, void *stream);
+
+/* Run armed solves to completion with device-side stopping: launches
+ * sweeps in batches of `batch` and polls one device counter per batch.
+ * Blocking.  *sweeps_out receives the number of sweep launches issued. */
+int bs_run(bs_ctx *ctx, int batch, int max_launches, void *stream, int64_t *sweeps_out);
+
+/* Run only the residual sweep of armed solves (the INIT step: rhs assembly
+ * + r0 = rhs - A x0 + the local/true residual sums of the current iterate,
+ * multisplit.py:333-338 and 372-406).  Lets the outer driver read the
+ * sweep-k residual and decide termination (multisplit.py:409-426) before
+ * any CG iteration of sweep k+1 runs. */
+int bs_sweep_resid(bs_ctx *ctx, void *stream);
+
+/* Disarm the active blocks (phase -> done) without touching their iterate. */
+int bs_cancel(bs_ctx *ctx, const int32_t *active, void *stream);
+
+/* One residual sweep on the active blocks without starting a solve:
+ * r = (b - C*ghost) - A_ii x and the report's squared sums (multisplit.py:
+ * 372-396 local residual, 404-406 true residual on owned rows).  Blocking
+ * only through bs_read_reports. */
+int bs_residual(bs_ctx *ctx, const int32_t *active, void *stream);
+
+/* Apply the deferred x += alpha*p update of every block that has one. */
+int bs_flush(bs_ctx *ctx, void *stream);
+
+/* a8 (sync halo, overlap 0): for each plan entry (dst_block, dir, src_block)
+ * write src's current boundary values (x + pending alpha*p) into dst's
+ * ghost[dir] plane (comm.py:332-365 + multisplit.py:341-369 with m=1). */
+int bs_halo_pack(bs_ctx *ctx, int nplan, const int32_t *plan, void *stream);
+
+/* Number of kernels this library has launched (process lifetime). */
+unsigned long long bs_launch_count(void);
+
+/* CUDA-event timing of the sweep kernels issued by bs_run, per kind
+ * [0] residual sweep, [1] CG sweep 1, [2] CG sweep 2: total milliseconds and
+ * launch counts since the last reset.  enable: 1 on, 0 off, -1 read only
+ * (1 and 0 also reset the totals). */
+int bs_timing(bs_ctx *ctx, int enable, double *ms_out, long long *n_out);
+
+/* Copy every block's report to host memory (blocking). */
+int bs_read_reports(bs_ctx *ctx, bs_block_report *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BLOCKSOLVE_B200_H */

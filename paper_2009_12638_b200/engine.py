@@ -1,0 +1,224 @@
+"""Device-side block set: buffers in HBM + the libbsgpu.so context.
+
+A ``BlockEngine`` owns, for every block resident on one GPU, the padded-box
+vectors x, r, p0, p1, b (fp64, x-fastest), the halo planes just outside the
+padded box, and a device residual-history buffer.  Tensors are torch-owned
+(PyTorch is plumbing here: allocation and streams); all arithmetic runs in
+the hand-written sm_100a kernels of ``csrc/bs_engine.cu``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import DeviceError
+from .problems import Box
+
+try:  # torch is the buffer/stream plumbing; absence is a hard error on use
+    import torch
+except Exception:  # pragma: no cover
+    torch = None
+
+
+def require_cuda(device) -> "torch.device":
+    if torch is None or not torch.cuda.is_available():
+        raise DeviceError("the B200 engine needs a CUDA device (no CPU fallback)")
+    dev = torch.device(device if device is not None else "cuda")
+    if dev.type != "cuda":
+        raise DeviceError(f"device must be a CUDA device, got {dev}")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    return dev
+
+
+@dataclass
+class BlockBuffers:
+    owned: Box
+    padded: Box
+    x: "torch.Tensor"
+    r: "torch.Tensor"
+    p0: "torch.Tensor"
+    p1: "torch.Tensor"
+    b: "torch.Tensor"
+    ghost: list
+    history: "torch.Tensor"
+
+    @property
+    def dims(self) -> tuple:
+        return tuple(self.padded.hi[d] - self.padded.lo[d] for d in range(3))
+
+    def view3(self, t: "torch.Tensor") -> "torch.Tensor":
+        nx, ny, nz = self.dims
+        return t.view(nz, ny, nx)
+
+    def owned_slices(self) -> tuple:
+        lo, plo = self.owned.lo, self.padded.lo
+        return tuple(slice(self.owned.lo[d] - plo[d], self.owned.hi[d] - plo[d]) for d in (2, 1, 0))
+
+
+class BlockEngine:
+    """All blocks of one decomposition that live on one device."""
+
+    def __init__(self, grid_shape, owned: list, overlap: int, device=None,
+                 history_cap: int = 0, z_chunk: int = 0, block_ids=None):
+        self.lib = _lib.load()
+        self.device = require_cuda(device)
+        self.grid_shape = tuple(int(v) for v in grid_shape)
+        self.overlap = int(overlap)
+        self.block_ids = list(block_ids) if block_ids is not None else list(range(len(owned)))
+        self.blocks: list = []
+        nx, ny, nz = self.grid_shape
+        descs = (_lib.BlockDesc * len(owned))()
+        opts = dict(dtype=torch.float64, device=self.device)
+        cap = max(1, int(history_cap))
+        for i, box in enumerate(owned):
+            lo = tuple(max(0, box.lo[d] - overlap) for d in range(3))
+            hi = tuple(min(self.grid_shape[d], box.hi[d] + overlap) for d in range(3))
+            pad = Box(lo, hi)
+            px, py, pz = (hi[d] - lo[d] for d in range(3))
+            n = px * py * pz
+            ghosts = []
+            faces = (  # dir -> (exists, plane size)
+                (lo[2] > 0, px * py), (lo[1] > 0, px * pz), (lo[0] > 0, py * pz),
+                (hi[0] < nx, py * pz), (hi[1] < ny, px * pz), (hi[2] < nz, px * py))
+            for exists, size in faces:
+                ghosts.append(torch.zeros(size, **opts) if exists else None)
+            bb = BlockBuffers(
+                owned=box, padded=pad, x=torch.zeros(n, **opts), r=torch.zeros(n, **opts),
+                p0=torch.zeros(n, **opts), p1=torch.zeros(n, **opts), b=torch.zeros(n, **opts),
+                ghost=ghosts, history=torch.zeros(cap, **opts))
+            self.blocks.append(bb)
+            d = descs[i]
+            d.global_dims[:] = [nx, ny, nz]
+            d.owned_lo[:] = list(box.lo)
+            d.owned_hi[:] = list(box.hi)
+            d.overlap = overlap
+            d.x, d.r, d.p0, d.p1, d.b = (bb.x.data_ptr(), bb.r.data_ptr(), bb.p0.data_ptr(),
+                                         bb.p1.data_ptr(), bb.b.data_ptr())
+            for q in range(_lib.NDIR):
+                d.ghost[q] = ghosts[q].data_ptr() if ghosts[q] is not None else None
+            d.history = bb.history.data_ptr()
+            d.history_cap = cap
+        self._descs = descs
+        ctx = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.check(self.lib.bs_ctx_create(self.device.index, len(owned), descs, int(z_chunk),
+                                              ctypes.byref(ctx)))
+        self.ctx = ctx
+        self.nblocks = len(owned)
+        self._reports = (_lib.BlockReport * self.nblocks)()
+
+    # -- plumbing ---------------------------------------------------------
+    def close(self) -> None:
+        if getattr(self, "ctx", None):
+            self.lib.bs_ctx_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream(self) -> ctypes.c_void_p:
+        return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def _mask(self, active):
+        if active is None:
+            return None
+        arr = (ctypes.c_int32 * self.nblocks)(*[1 if a else 0 for a in active])
+        return ctypes.cast(arr, ctypes.c_void_p), arr
+
+    @property
+    def num_ctas(self) -> int:
+        return self.lib.bs_ctx_num_ctas(self.ctx)
+
+    # -- data movement ----------------------------------------------------
+    def load_global(self, name: str, g3: "torch.Tensor") -> None:
+        """Scatter a global (nz, ny, nx) device tensor into every block's padded box."""
+        for bb in self.blocks:
+            (x0, y0, z0), (x1, y1, z1) = bb.padded.lo, bb.padded.hi
+            bb.view3(getattr(bb, name)).copy_(g3[z0:z1, y0:y1, x0:x1])
+
+    def gather_owned(self, out3: "torch.Tensor", name: str = "x") -> None:
+        """Write every block's owned values of ``name`` into a global (nz, ny, nx) tensor."""
+        for bb in self.blocks:
+            (x0, y0, z0), (x1, y1, z1) = bb.owned.lo, bb.owned.hi
+            out3[z0:z1, y0:y1, x0:x1].copy_(bb.view3(getattr(bb, name))[bb.owned_slices()])
+
+    def zero(self, *names) -> None:
+        for bb in self.blocks:
+            for name in names:
+                getattr(bb, name).zero_()
+            if "ghost" in names:
+                for g in bb.ghost:
+                    if g is not None:
+                        g.zero_()
+
+    # -- engine calls -----------------------------------------------------
+    def apply(self, block: int, x: "torch.Tensor", y: "torch.Tensor") -> None:
+        _lib.check(self.lib.bs_stencil_apply(self.ctx, block, x.data_ptr(), y.data_ptr(), self.stream))
+
+    def cg_begin(self, max_iterations: int, tolerance: float, basis: str = "rhs", active=None) -> None:
+        m = self._mask(active)
+        _lib.check(self.lib.bs_cg_begin(self.ctx, int(max_iterations), float(tolerance),
+                                        _lib.BASIS[basis], m[0] if m else None, self.stream))
+
+    def sweep_resid(self) -> None:
+        _lib.check(self.lib.bs_sweep_resid(self.ctx, self.stream))
+
+    def cancel(self, active=None) -> None:
+        m = self._mask(active)
+        _lib.check(self.lib.bs_cancel(self.ctx, m[0] if m else None, self.stream))
+
+    def run(self, batch: int = 4, max_launches: int = 0) -> int:
+        n = ctypes.c_int64(0)
+        _lib.check(self.lib.bs_run(self.ctx, int(batch), int(max_launches), self.stream, ctypes.byref(n)))
+        return n.value
+
+    def residual(self, active=None) -> None:
+        m = self._mask(active)
+        _lib.check(self.lib.bs_residual(self.ctx, m[0] if m else None, self.stream))
+
+    def flush(self) -> None:
+        _lib.check(self.lib.bs_flush(self.ctx, self.stream))
+
+    def halo_pack(self, plan: np.ndarray) -> None:
+        plan = np.ascontiguousarray(plan, dtype=np.int32)
+        if plan.size == 0:
+            return
+        _lib.check(self.lib.bs_halo_pack(self.ctx, plan.shape[0], plan.ctypes.data_as(ctypes.c_void_p),
+                                         self.stream))
+
+    def reports(self) -> list:
+        _lib.check(self.lib.bs_read_reports(self.ctx, self._reports, self.stream))
+        return [self._reports[i] for i in range(self.nblocks)]
+
+
+def launch_bound(max_iterations: int, batch: int) -> int:
+    """Safety cap on sweep launches of one armed solve: every CG iteration takes
+    at most two RESID/S1/S2 cycles (a failed convergence check adds one)."""
+    return 3 * (2 * int(max_iterations) + 4 + int(batch))
+
+
+def box_halo_plan(decomp_owned: list, block_grid: tuple) -> np.ndarray:
+    """(dst, dir, src) triples of the overlap-0 face exchange for a box grid.
+
+    Direction order = ascending column order (0 z-1, 1 y-1, 2 x-1, 3 x+1,
+    4 y+1, 5 z+1); block ids are bx-fastest (problems.py:322-328).
+    """
+    gx, gy, gz = block_grid
+    plan = []
+    for bid in range(len(decomp_owned)):
+        bx, by, bz = bid % gx, (bid // gx) % gy, bid // (gx * gy)
+        cand = ((0, bz > 0, bid - gx * gy), (1, by > 0, bid - gx), (2, bx > 0, bid - 1),
+                (3, bx < gx - 1, bid + 1), (4, by < gy - 1, bid + gx), (5, bz < gz - 1, bid + gx * gy))
+        for d, ok, src in cand:
+            if ok:
+                plan.append((bid, d, src))
+    return np.asarray(plan, dtype=np.int32).reshape(-1, 3)

@@ -1,0 +1,129 @@
+"""Inner solvers on the GPU (mirror of inner_solvers.py).
+
+``cg_solve(a, b, x0, spec)`` keeps the reference signature and stopping
+semantics (inner_solvers.py:102-146): relative to ||b|| (1 if b = 0), the
+true residual is re-checked whenever the recurrence claims convergence, and
+breakdown is reported, not raised.  The solve runs entirely on the device
+(fused CG sweeps, device-side stop tests); the host polls once per batch.
+
+``tolerance_basis="initial"`` (an addition; default keeps the reference
+behaviour) measures the tolerance against ||b - A x0|| instead, which is
+what fixed-count inner stages and PETSc's rtol mean.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._lib import STOP_NAMES
+from .engine import torch
+from .errors import ConfigurationError
+from .engine import launch_bound
+from .linalg import as_device_vector, single_block_engine
+from .problems import StencilOperator
+
+__all__ = [
+    "InnerSolverSpec",
+    "InnerSolveReport",
+    "cg_solve",
+    "gmres_solve",
+    "solve",
+    "SOLVER_KINDS",
+]
+
+SOLVER_KINDS = ("jacobi", "cg", "gmres", "direct")
+DEVICE_KINDS = ("cg", "gmres")
+DEFAULT_RESTART = 30
+
+
+@dataclass(frozen=True)
+class InnerSolverSpec:
+    """Which solver to run and when to stop it (inner_solvers.py:40-57)."""
+
+    kind: str
+    max_iterations: int
+    tolerance: float = 0.0
+    restart: int | None = None
+
+    def __post_init__(self):
+        if self.kind not in SOLVER_KINDS:
+            raise ValueError(f"unknown solver kind {self.kind!r}")
+        if self.max_iterations < 1:
+            raise ValueError("max_iterations must be at least 1")
+        if self.tolerance < 0:
+            raise ValueError("tolerance must be non-negative")
+        if self.restart is not None and self.restart < 1:
+            raise ValueError("restart must be at least 1")
+
+
+@dataclass
+class InnerSolveReport:
+    """Outcome of one solver invocation (inner_solvers.py:60-67)."""
+
+    iterations_used: int
+    final_relative_residual: float
+    stop_reason: str  # tolerance_met | max_iterations | breakdown
+    residual_history: list = field(default_factory=list)
+
+
+def _check_basis(basis: str) -> None:
+    if basis not in ("rhs", "initial"):
+        raise ConfigurationError(f"tolerance_basis: unknown basis {basis!r}")
+
+
+def cg_solve(a: StencilOperator, b, x0, spec: InnerSolverSpec, tolerance_basis: str = "rhs",
+             batch: int = 8, out=None):
+    """Conjugate gradients on the GPU; returns (x, InnerSolveReport).
+
+    numpy in -> numpy out; CUDA tensor in -> CUDA tensor out (resident);
+    host tensor in -> host tensor out (written into ``out`` when given, e.g.
+    a pinned buffer, so the device->host copy runs at full PCIe speed).
+    """
+    _check_basis(tolerance_basis)
+    n = a.num_rows
+    is_tensor = torch is not None and isinstance(b, torch.Tensor)
+    on_device = is_tensor and b.is_cuda
+    eng = single_block_engine(a, b.device if on_device else None, history_cap=spec.max_iterations)
+    bd, host = as_device_vector(b, n, eng.device)
+    xd, _ = as_device_vector(x0, n, eng.device)
+    bb = eng.blocks[0]
+    with torch.cuda.device(eng.device):
+        bb.b.copy_(bd)
+        bb.x.copy_(xd)
+        eng.cg_begin(spec.max_iterations, spec.tolerance, tolerance_basis)
+        eng.run(batch=batch, max_launches=launch_bound(spec.max_iterations, batch))
+        eng.flush()
+        rep = eng.reports()[0]
+        its = int(rep.iterations_used)
+        hist = bb.history[:its].tolist() if its else []
+        x = bb.x  # engine buffer: copied out below, never aliased to the caller
+    report = InnerSolveReport(its, float(rep.final_relative_residual), STOP_NAMES[int(rep.stop_reason)],
+                              hist)
+    if host:
+        return x.cpu().numpy(), report
+    if is_tensor and not on_device:  # host tensor in, host tensor out
+        if out is None:
+            return x.cpu(), report
+        out.copy_(x)
+        return out, report
+    if out is not None:
+        out.copy_(x)
+        return out, report
+    return x.clone(), report
+
+
+def gmres_solve(a: StencilOperator, b, x0, spec: InnerSolverSpec, tolerance_basis: str = "rhs"):
+    """Restarted GMRES(m) (inner_solvers.py:149-243) — device path pending."""
+    raise ConfigurationError("inner: gmres is not available on the device engine yet")
+
+
+def solve(a: StencilOperator, b, x0, spec: InnerSolverSpec, tolerance_basis: str = "rhs"):
+    """Dispatch on ``spec.kind`` (inner_solvers.py:264-276)."""
+    if spec.kind == "cg":
+        return cg_solve(a, b, x0, spec, tolerance_basis)
+    if spec.kind == "gmres":
+        return gmres_solve(a, b, x0, spec, tolerance_basis)
+    raise ConfigurationError(
+        f"inner: {spec.kind!r} is outside the accelerated path (device kinds: {DEVICE_KINDS})")

@@ -1,0 +1,247 @@
+"""GPU parity: the CUDA path vs the reference golden vectors and the oracle.
+
+All tests call through the C ABI (ctypes) via the package's public API.
+Bars (north_star): SpMV bit-identical; inner/outer iteration counts equal in
+sync mode; converged solution within 1e-8 relative L2 of the reference.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from golden_io import arrays, meta
+from oracle import blocksolve_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+import paper_2009_12638_b200 as bs  # noqa: E402
+from paper_2009_12638_b200.engine import BlockEngine  # noqa: E402
+from paper_2009_12638_b200.problems import Box  # noqa: E402
+
+
+def torch():
+    import torch as t
+
+    return t
+
+
+# ------------------------------------------------------------------ SpMV (a1)
+
+
+@pytest.mark.parametrize("shape", [(6, 5, 4), (16, 16, 16), (7, 1, 3)])
+def test_spmv_bit_identical_to_reference(shape):
+    A = arrays()
+    key = "spmv/%dx%dx%d" % shape
+    y = bs.spmv(bs.StencilOperator(*shape), A[key + "/x"])
+    assert np.array_equal(y, A[key + "/y"])
+
+
+def _blocksys_keys():
+    return [k for k in meta() if k.startswith("blocksys/")]
+
+
+@pytest.mark.parametrize("key", _blocksys_keys())
+def test_block_system_spmv_bit_identical(key):
+    """Principal-submatrix SpMV on box and L1-dilated regions (problems.py:362-406)."""
+    t = torch()
+    A, M = arrays(), meta()[key]
+    shape, bg, ov = tuple(M["shape"]), tuple(M["block_grid"]), M["overlap"]
+    dec = bs.decompose(bs.Grid3D(*shape), bg, ov)
+    assert dec.neighbors == M["neighbors"]
+    eng = BlockEngine(shape, dec.owned, ov, "cuda")
+    nx, ny, _ = shape
+    for b in range(dec.num_blocks):
+        ext = A[f"{key}/{b}/ext"]
+        assert np.array_equal(dec.extended_indices(b), ext)
+        pad = dec.padded_box(b)
+        px, py, pz = (pad.hi[d] - pad.lo[d] for d in range(3))
+        gi, gj, gk = ext % nx, (ext // nx) % ny, ext // (nx * ny)
+        loc = (gi - pad.lo[0]) + px * ((gj - pad.lo[1]) + py * (gk - pad.lo[2]))
+        xp = np.full(px * py * pz, 1e300)  # garbage outside the region must be ignored
+        xp[loc] = A[f"{key}/{b}/x"]
+        xd = t.from_numpy(xp).cuda()
+        yd = t.zeros_like(xd)
+        eng.apply(b, xd, yd)
+        y = yd.cpu().numpy()[loc]
+        assert np.array_equal(y, A[f"{key}/{b}/y"]), f"block {b}"
+    eng.close()
+
+
+def test_spmv_known_answers():
+    # test_linalg.py:73-79 restated on the device operator
+    y = bs.spmv(bs.StencilOperator(4, 4, 4), np.ones(64))
+    assert y[bs.Grid3D(4, 4, 4).index(1, 1, 1)] == 0.0
+    with pytest.raises(ValueError, match="dimension mismatch"):
+        bs.spmv(bs.StencilOperator(4, 4, 4), np.ones(63))
+
+
+def test_spmv_linearity_and_oracle_at_scale():
+    rng = np.random.default_rng(1)
+    shape = (67, 45, 33)  # ragged vs the 32x8 tiles
+    n = 67 * 45 * 33
+    x, z = rng.standard_normal(n), rng.standard_normal(n)
+    op = bs.StencilOperator(*shape)
+    left = bs.spmv(op, 0.7 * x - 1.3 * z)
+    right = 0.7 * bs.spmv(op, x) - 1.3 * bs.spmv(op, z)
+    assert np.linalg.norm(left - right) <= 1e-12 * np.linalg.norm(left)
+    ref = O.stencil_apply(x.reshape(33, 45, 67)).ravel()
+    assert np.array_equal(bs.spmv(op, x), ref)
+
+
+# ------------------------------------------------------------------ CG (a2)
+
+
+@pytest.mark.parametrize("key,tol", [("cg/12_seed0", 1e-8), ("cg/20_seed1", 1e-10), ("cg/32_seed0", 1e-8)])
+def test_cg_matches_reference(key, tol):
+    A, M = arrays(), meta()[key]
+    n = int(key.split("/")[1].split("_")[0])
+    seed = int(key.split("seed")[1])
+    b = O.seeded_rhs(n ** 3, seed)
+    x, rep = bs.cg_solve(bs.StencilOperator(n, n, n), b, np.zeros(n ** 3),
+                         bs.InnerSolverSpec("cg", 10 * n, tol))
+    assert rep.iterations_used == M["iterations_used"]
+    assert rep.stop_reason == M["stop_reason"]
+    assert np.allclose(rep.residual_history, M["residual_history"], rtol=1e-9, atol=0)
+    ref = A[key + "/x"]
+    assert np.linalg.norm(x - ref) <= 1e-10 * np.linalg.norm(ref)
+
+
+def test_cg_warm_start_capped_and_initial_basis():
+    A, M = arrays(), meta()
+    n = 10
+    prob = bs.build_laplace_3d(bs.Grid3D(n, n, n, bs.DirichletBoundary({"z_lo": 1.0})))
+    x0 = A["cg/warm/x0"]
+    x, rep = bs.cg_solve(prob.matrix, prob.rhs, x0, bs.InnerSolverSpec("cg", 17, 1e-3))
+    assert (rep.iterations_used, rep.stop_reason) == (17, "max_iterations")
+    assert np.allclose(rep.residual_history, M["cg/warm"]["residual_history"], rtol=1e-9)
+    assert np.abs(x - A["cg/warm/x"]).max() <= 1e-12
+    x, rep = bs.cg_solve(prob.matrix, prob.rhs, x0, bs.InnerSolverSpec("cg", 200, 1e-3),
+                         tolerance_basis="initial")
+    assert rep.iterations_used == M["cg/warm_initial"]["iterations_used"]
+    assert rep.stop_reason == "tolerance_met"
+    assert np.abs(x - A["cg/warm_initial/x"]).max() <= 1e-11
+
+
+def test_cg_edge_cases():
+    op = bs.StencilOperator(5, 4, 3)
+    # zero rhs with a non-zero start: scale falls back to 1, converges to 0
+    rng = np.random.default_rng(7)
+    x, rep = bs.cg_solve(op, np.zeros(60), rng.standard_normal(60), bs.InnerSolverSpec("cg", 500, 1e-12))
+    assert rep.stop_reason == "tolerance_met" and np.abs(x).max() <= 1e-10
+    # exact start: zero iterations, x untouched
+    b = rng.standard_normal(60)
+    xs, _ = bs.cg_solve(op, b, np.zeros(60), bs.InnerSolverSpec("cg", 500, 1e-14))
+    x2, rep2 = bs.cg_solve(op, b, xs, bs.InnerSolverSpec("cg", 500, 1e-3))
+    assert rep2.iterations_used == 0 and np.array_equal(x2, xs)
+    # 1x1x1 grid: [[6]] x = b in one iteration
+    x, rep = bs.cg_solve(bs.StencilOperator(1, 1, 1), np.array([3.0]), np.zeros(1),
+                         bs.InnerSolverSpec("cg", 5, 1e-12))
+    assert rep.iterations_used == 1 and x[0] == 0.5
+    # determinism: bitwise identical repeats
+    xa, ra = bs.cg_solve(op, b, np.zeros(60), bs.InnerSolverSpec("cg", 30, 1e-9))
+    xb, rb = bs.cg_solve(op, b, np.zeros(60), bs.InnerSolverSpec("cg", 30, 1e-9))
+    assert np.array_equal(xa, xb) and ra.residual_history == rb.residual_history
+
+
+def test_cg_config2_analogue_64_against_oracle():
+    n = 64
+    b = O.seeded_rhs(n ** 3, 0)
+    a = O.laplace_csr(n, n, n)
+    xo, ro = O.cg(lambda v: O.csr_spmv(a, v), b, np.zeros(n ** 3), 2000, 1e-8)
+    x, rep = bs.cg_solve(bs.StencilOperator(n, n, n), b, np.zeros(n ** 3), bs.InnerSolverSpec("cg", 2000, 1e-8))
+    assert rep.iterations_used == ro.iterations_used == 231
+    assert np.allclose(rep.residual_history, ro.residual_history, rtol=1e-8)
+    assert np.linalg.norm(x - xo) <= 1e-10 * np.linalg.norm(xo)
+
+
+def test_cg_config2_full_256_iteration_count():
+    """Config 2 at full size: 856 CG iterations, final rel 9.832311620407356e-09
+    (reference run)."""
+    t = torch()
+    n = 256
+    b = t.from_numpy(O.seeded_rhs(n ** 3, 0)).cuda()
+    x, rep = bs.cg_solve(bs.StencilOperator(n, n, n), b, t.zeros_like(b), bs.InnerSolverSpec("cg", 5000, 1e-8))
+    assert rep.iterations_used == 856
+    assert rep.stop_reason == "tolerance_met"
+    assert rep.final_relative_residual == pytest.approx(9.832311620407356e-09, rel=1e-6)
+    assert rep.residual_history[:3] == pytest.approx(
+        [0.4073481114578424, 0.24363013224694208, 0.17767096348143008], rel=1e-12)
+    # size-independent check: the true residual of the returned iterate
+    _, rel = bs.residual_norms(bs.StencilOperator(n, n, n), x, b)
+    assert rel <= 1e-8
+
+
+# ------------------------------------------------------------------ outer sync
+
+
+OUTER = ["outer/cfg1_16_fixed", "outer/cfg1_16_literal", "outer/cfg3_16_paper",
+         "outer/cfg3_16_true", "outer/box_12_222"]
+
+
+@pytest.mark.parametrize("key", OUTER)
+def test_outer_sync_matches_reference(key):
+    A, M = arrays(), meta()[key]
+    c = M["case"]
+    n = c["n"]
+    kind, its, itol = c["inner"]
+    grid = bs.Grid3D(n, n, n)
+    prob = bs.LinearProblem(bs.StencilOperator(n, n, n), A[key + "/rhs"], grid)
+    cfg = bs.OuterConfig(block_grid=tuple(c["bg"]), overlap=c["ov"],
+                         inner=bs.InnerSolverSpec(kind, its, itol), tol=c["tol"],
+                         max_outer=c.get("max_outer", 5000), residual_check_mode=c["mode"])
+    res = bs.outer_solve(prob, cfg)
+    assert res.converged == M["converged"]
+    assert res.outer_iterations == M["outer_iterations"]
+    for row, ref in zip(res.trace.rows, M["trace"]):
+        assert row.outer_iteration == ref[0] and row.time == ref[1]
+        assert row.inner_iterations == ref[4], f"sweep {ref[0]}"
+        assert row.estimated_residual == pytest.approx(ref[2], rel=1e-9)
+        if ref[3] is None:
+            assert row.true_residual is None
+        else:
+            assert row.true_residual == pytest.approx(ref[3], rel=1e-9)
+        assert row.max_halo_staleness == ref[5]
+    sol = A[key + "/solution"]
+    assert np.linalg.norm(res.solution - sol) <= 1e-10 * np.linalg.norm(sol)
+    assert res.final_true_residual == pytest.approx(M["final_true_residual"], rel=1e-8)
+
+
+def test_outer_config1_full_size_counts():
+    """Config 1 (64^3, z_lo=1, 2 z-slabs, CG 50 its, outer 1e-6) in both tolerance
+    bases.  Reference runs: literal basis stalls at
+    8.063e-3; the r0-relative basis converges in 134 sweeps / 13,350 inner its
+    with true residual 9.537e-7."""
+    prob = bs.build_laplace_3d(bs.Grid3D(64, 64, 64, bs.DirichletBoundary({"z_lo": 1.0})))
+    cfg = bs.OuterConfig(block_grid=(1, 1, 2), inner=bs.InnerSolverSpec("cg", 50, 1e-2), tol=1e-6,
+                         max_outer=5000, tolerance_basis="initial")
+    res = bs.outer_solve(prob, cfg)
+    assert res.converged and res.outer_iterations == 134
+    assert sum(r.inner_iterations for r in res.trace.rows) == 13350
+    assert res.final_true_residual == pytest.approx(9.537e-7, rel=1e-3)
+    lit = bs.outer_solve(prob, bs.OuterConfig(block_grid=(1, 1, 2), inner=bs.InnerSolverSpec("cg", 50, 1e-2),
+                                              tol=1e-6, max_outer=40))
+    assert not lit.converged
+    assert [r.inner_iterations for r in lit.trace.rows[:6]] == [50, 55, 50, 6, 46, 0]
+    assert lit.trace.rows[-1].estimated_residual == pytest.approx(8.063e-3, rel=1e-3)
+
+
+def test_outer_block_count_invariance_of_counts():
+    """Same problem split into the same 8 slabs: per-sweep counts are a pure
+    function of the decomposition (the basis of 1/2/4/8-GPU invariance)."""
+    n = 32
+    b = O.seeded_rhs(n ** 3, 0)
+    prob = bs.LinearProblem(bs.StencilOperator(n, n, n), b, bs.Grid3D(n, n, n))
+    cfg = bs.OuterConfig(block_grid=(1, 1, 8), inner=bs.InnerSolverSpec("cg", 100, 1e-3), tol=1e-8,
+                         tolerance_basis="initial", residual_check_mode="true")
+    r1 = bs.outer_solve(prob, cfg)
+    r2 = bs.outer_solve(prob, cfg)
+    assert r1.inner_iterations_per_block == r2.inner_iterations_per_block
+    assert np.array_equal(r1.solution, r2.solution)
+    # oracle replay of the same configuration
+    ro = O.outer_solve_sync((n, n, n), b, (1, 1, 8), 0,
+                            dict(kind="cg", max_iterations=100, tolerance=1e-3, basis="initial"),
+                            tol=1e-8, residual_check_mode="true")
+    assert r1.outer_iterations == ro.outer_iterations
+    assert r1.inner_iterations_per_block == ro.per_block_inner
+    assert np.linalg.norm(r1.solution - ro.solution) <= 1e-8 * np.linalg.norm(ro.solution)
