@@ -97,7 +97,12 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
 int bs_ctx_destroy(bs_ctx *ctx);
 int bs_ctx_num_ctas(const bs_ctx *ctx);
 
-/* a1: y = A_ii x on block `block`'s region — the principal-submatrix SpMV
+/* Row pitch (in doubles) of block `block`'s padded-box vectors: the x extent
+ * rounded up to 4 (TMA needs 16-byte row strides).  Index of padded-box cell
+ * (i, j, k) = i + pitch * (j + ny_pad * k).  Returns < 0 on error. */
+int bs_block_pitch(const bs_ctx *ctx, int block);
+
+/* a1: y = A_ii x on block `block`'s region (x, y in the block's pitched layout) — the principal-submatrix SpMV
  * (linalg.py:178-194 on problems.py:362-406's A_ii), bit-identical to the
  * reference's reduceat association.  Values of y outside the region are 0. */
 int bs_stencil_apply(bs_ctx *ctx, int block, const double *x, double *y, void *stream);
@@ -109,9 +114,14 @@ int bs_stencil_apply(bs_ctx *ctx, int block, const double *x, double *y, void *s
 int bs_cg_begin(bs_ctx *ctx, int max_iterations, double tolerance, int basis,
                 const int32_t *active, void *stream);
 
-/* Run armed solves to completion with device-side stopping: launches
- * sweeps in batches of `batch` and polls one device counter per batch.
- * Blocking.  *sweeps_out receives the number of sweep launches issued. */
+/* Run armed solves to completion with device-side stopping.  Default: one
+ * CUDA-graph launch whose WHILE node iterates {CG sweep 1, CG sweep 2,
+ * IF(any block verifying) residual sweep} until no block is active — no host
+ * round trip per iteration.  With timing enabled (bs_timing) the same kernels
+ * are launched from the host in batches of `batch` cycles with CUDA events
+ * around each.  max_launches > 0 bounds the sweeps (runaway guard; exceeding
+ * it stops the solves and returns BS_ESTATE).  Blocking.  *sweeps_out
+ * receives the number of sweep kernels that ran. */
 int bs_run(bs_ctx *ctx, int batch, int max_launches, void *stream, int64_t *sweeps_out);
 
 /* Run only the residual sweep of armed solves (the INIT step: rhs assembly

@@ -60,6 +60,7 @@ _SIGS = {
     "bs_ctx_create": ([_I, _I, ctypes.POINTER(BlockDesc), _I, ctypes.POINTER(_P)], _I),
     "bs_ctx_destroy": ([_P], _I),
     "bs_ctx_num_ctas": ([_P], _I),
+    "bs_block_pitch": ([_P, _I], _I),
     "bs_stencil_apply": ([_P, _I, _P, _P, _P], _I),
     "bs_cg_begin": ([_P, _I, ctypes.c_double, _I, _P, _P], _I),
     "bs_sweep_resid": ([_P, _P], _I),

@@ -1,8 +1,8 @@
 // bs_engine.cu — sm_100a engine for the block-Jacobi / CG 7-point stencil path.
 //
-// One translation unit: the matrix-free stencil sweep machinery, the fused CG
-// phase machine with device-side stopping, halo packing, and the C ABI
-// declared in include/blocksolve_b200.h.
+// One translation unit: the TMA-fed stencil sweep kernels, the fused CG phase
+// machine with device-side stopping (CUDA-graph WHILE loop), halo packing and
+// the C ABI declared in include/blocksolve_b200.h.
 //
 // Reference algorithm (file:line into /root/reference/pkg/src/blocksolve):
 //   SpMV            linalg.py:178-194 on the block system of problems.py:362-406
@@ -12,26 +12,31 @@
 //   sync halo       comm.py:332-365 + merge multisplit.py:341-369 (overlap 0)
 //
 // Design:
-//   * Every vector lives over the block's padded box, x-fastest.  A CTA owns a
-//     TX x TY column tile and marches CZ planes in z: the stencil input field
-//     u of plane k+1 is staged (tile + 1-cell x/y halo) into a 3-deep shared
-//     ring while plane k is computed; z-neighbours ride in registers.
-//   * The stencil input is produced on the fly: u = r + beta*p_old in CG
-//     sweep 1 (so p is written once and never re-read in the same sweep),
-//     u = p in sweep 2, u = x + alpha*p in residual sweeps (deferred x update).
-//     => one CG iteration moves 64 B/point of compulsory HBM traffic.
-//   * Reductions are fixed-order (per-thread z order, xor-butterfly warps,
-//     sequential warps, strided+tree across CTAs) so results are deterministic
-//     and independent of how many blocks share a GPU.
-//   * The scalar recurrences (alpha, beta, stop tests) run in the last CTA of
-//     every sweep launch ("last block" pattern), so the host only polls one
-//     counter per batch of sweeps.
-//   * All floating-point arithmetic is explicit round-to-nearest with no FMA
-//     contraction (__dadd_rn/__dmul_rn, and -fmad=false) to reproduce the
-//     reference's rounding: the SpMV is bit-identical.
+//   * Every vector lives over the block's padded box, x-fastest with a row
+//     pitch rounded up to 4 doubles (TMA needs 16-byte global strides).
+//   * A CTA owns a TX x TY column tile and marches CZ planes in z.  One
+//     thread issues cp.async.bulk.tensor (TMA) loads of whole planes — the
+//     tile plus a one-cell x/y halo for the stencil inputs, the bare tile for
+//     epilogue operands — into an NSTAGE-deep shared-memory ring completed on
+//     mbarriers, NSTAGE-2 planes ahead of the plane being computed.  Cells
+//     outside the padded box are zero-filled by TMA (= absent neighbours).
+//   * The stencil input u is formed from the staged operands: u = r + beta*p
+//     in CG sweep 1 (p written once, never re-read), u = p in sweep 2,
+//     u = x + alpha*p in residual sweeps (x += alpha p is deferred).  One CG
+//     iteration therefore moves 64 B/point of compulsory HBM traffic.
+//   * Reductions are fixed-order (thread z order, xor-butterfly warps,
+//     sequential warps, strided+tree across the block's tiles).  The last CTA
+//     of each block reduces that block and runs its scalar recurrence; the
+//     last CTA of the launch sets the graph's loop conditions.  Results are
+//     deterministic and independent of which other blocks share the GPU.
+//   * All arithmetic is explicit round-to-nearest without FMA contraction
+//     (__dadd_rn/__dmul_rn and -fmad=false): the SpMV is bit-identical to the
+//     reference's numpy reduceat.
 
 #include "blocksolve_b200.h"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -61,8 +66,17 @@ constexpr int TY = 8;
 constexpr int NT = TX * TY;
 constexpr int HX = TX + 2;
 constexpr int HY = TY + 2;
-constexpr int NHALO = 2 * TX + 2 * TY;
-constexpr int NQ = 4;  // partial sums per CTA
+constexpr int HC = HX * HY;            // haloed tile cells
+constexpr int NHALO = 2 * TX + 2 * TY; // halo cells
+constexpr int NQ = 4;                  // partial sums per CTA
+constexpr int NSTAGE = 5;              // TMA ring depth (NSTAGE-2 planes of lookahead)
+constexpr int PITCH_ALIGN = 4;         // doubles
+
+constexpr int SEG_H = ((HC * 8 + 127) / 128) * 128;  // haloed tile, 128B aligned
+constexpr int SEG_O = NT * 8;                         // bare tile
+constexpr int STAGE_BYTES = 2 * SEG_H + SEG_O;
+constexpr int RING_BYTES = ((3 * HC * 8 + 127) / 128) * 128;
+constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + RING_BYTES + NSTAGE * 8;
 
 enum Phase : int {
     PH_IDLE = 0,
@@ -76,10 +90,16 @@ enum Phase : int {
 
 enum Op : int { OP_RESID = 0, OP_S1 = 1, OP_S2 = 2, OP_APPLY = 3 };
 
+// tensor maps per block
+enum Tm : int { TM_XH = 0, TM_P0H = 1, TM_P1H = 2, TM_RH = 3, TM_XO = 4, TM_RO = 5, TM_BO = 6, NTM = 7 };
+
+constexpr int STOP_STALLED = 4;
+
 struct DBlock {
     int gn[3];
     int lo[3], hi[3];        // owned box
     int plo[3], pdim[3];     // padded box
+    int pitch;               // row pitch (doubles) >= pdim[0]
     int overlap;
     int cta_begin, cta_end;  // CTA range in sweep launches
     int tiles_x, tiles_y, tiles_z, cz;
@@ -96,11 +116,35 @@ struct DState {
     double q[NQ];
 };
 
+struct Control {
+    int cycles;      // WHILE-body iterations (S1 + S2 launches each)
+    int max_cycles;  // runaway guard (0 = unlimited)
+    int stalled;
+    int resid_runs;  // residual-sweep launches inside the graph
+};
+
+struct KParams {
+    const DBlock *blocks;
+    DState *states;
+    const CUtensorMap *tmaps;
+    const int *cta_block;
+    int nblocks;
+    int nctas;
+    double *partials;
+    unsigned *blk_counter;
+    unsigned *launch_counter;
+    int *n_active;
+    Control *ctl;
+    cudaGraphConditionalHandle h_loop;
+    cudaGraphConditionalHandle h_verify;
+    int use_graph;
+};
+
 // ------------------------------------------------------------------ geometry
 
 __device__ __forceinline__ long long sidx(const DBlock &B, int i, int j, int k) {
     return (long long)(i - B.plo[0]) +
-           (long long)B.pdim[0] * ((long long)(j - B.plo[1]) + (long long)B.pdim[1] * (long long)(k - B.plo[2]));
+           (long long)B.pitch * ((long long)(j - B.plo[1]) + (long long)B.pdim[1] * (long long)(k - B.plo[2]));
 }
 
 __device__ __forceinline__ bool in_grid(const DBlock &B, int i, int j, int k) {
@@ -165,6 +209,40 @@ __device__ __forceinline__ double stencil7(double zm, double ym, double xm, doub
     return add(t3, add(add(-xp, -yp), -zp));
 }
 
+// ------------------------------------------------------------------ TMA / mbarrier
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "BS_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra BS_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load3(void *dst, const CUtensorMap *map, int c0, int c1, int c2,
+                                          uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // ------------------------------------------------------------------ reductions
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -175,7 +253,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 // Deterministic CTA reduction of NQ values; result valid in thread 0.
 __device__ __forceinline__ void cta_sum(double (&acc)[NQ], double (*red)[NT / 32]) {
-    const int tid = threadIdx.y * TX + threadIdx.x;
+    const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
@@ -195,7 +273,7 @@ __device__ __forceinline__ void cta_sum(double (&acc)[NQ], double (*red)[NT / 32
 
 // Sum of partials[begin:end) with a fixed strided + tree order (whole CTA).
 __device__ double range_sum(const double *part, int begin, int end, double *scratch) {
-    const int tid = threadIdx.y * TX + threadIdx.x;
+    const int tid = threadIdx.x;
     double s = 0.0;
     for (int c = begin + tid; c < end; c += NT) s = add(s, __ldcg(part + c));
     scratch[tid] = s;
@@ -213,56 +291,64 @@ __device__ double range_sum(const double *part, int begin, int end, double *scra
 
 struct SweepCtx {
     const DBlock *B;
-    int op;
     bool pend, first, want_global;
     double alpha_pend, beta, alpha;
-    const double *pin;  // p[pcur]
-    double *pout;       // p[1-pcur]
-    const double *xin;  // OP_APPLY input
-    double *yout;       // OP_APPLY output
+    const CUtensorMap *map_a;  // stencil operand (haloed)
+    const CUtensorMap *map_b;  // second stencil operand (haloed) or null
+    const CUtensorMap *map_c;  // epilogue operand (bare tile) or null
+    double *pout;              // S1: p[1-pcur]
+    double *yout;              // APPLY output
 };
 
-// Stencil input field at storage index s of an in-region point.
+// Process one tile of one block.
 template <int OP>
-__device__ __forceinline__ double field(const SweepCtx &C, long long s) {
+__device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, double (&acc)[NQ]) {
     const DBlock &B = *C.B;
-    switch (OP) {
-        case OP_RESID: {
-            double v = B.x[s];
-            return C.pend ? add(v, mul(C.alpha_pend, C.pin[s])) : v;
-        }
-        case OP_S1: {
-            double v = B.r[s];
-            return C.first ? v : add(v, mul(C.beta, C.pin[s]));
-        }
-        case OP_S2:
-            return C.pin[s];
-        default:
-            return C.xin[s];
-    }
-}
-
-template <int OP>
-__device__ __forceinline__ double field_at(const SweepCtx &C, int i, int j, int k) {
-    return in_region(*C.B, i, j, k) ? field<OP>(C, sidx(*C.B, i, j, k)) : 0.0;
-}
-
-// Process one tile: accumulate partial sums into acc.
-template <int OP>
-__device__ void sweep_tile(const SweepCtx &C, int tile, double (*sm)[HY][HX], double (&acc)[NQ]) {
-    const DBlock &B = *C.B;
-    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
+    const int tid = threadIdx.x;
+    const int tx = tid % TX, ty = tid / TX;
     int t = tile;
     const int ix = t % B.tiles_x;
     t /= B.tiles_x;
     const int iy = t % B.tiles_y;
     const int iz = t / B.tiles_y;
-    const int x0 = B.plo[0] + ix * TX, y0 = B.plo[1] + iy * TY;
-    const int z0 = B.plo[2] + iz * B.cz;
-    const int z1 = min(z0 + B.cz, B.plo[2] + B.pdim[2]);
-    const int gi = x0 + tx, gj = y0 + ty;
-    const bool col_in = gi < B.plo[0] + B.pdim[0] && gj < B.plo[1] + B.pdim[1];
+    const int lx0 = ix * TX, ly0 = iy * TY;       // tile origin, padded-box coordinates
+    const int lz0 = iz * B.cz;
+    const int lz1 = min(lz0 + B.cz, B.pdim[2]);
+    const int nplanes = lz1 - lz0 + 2;            // q = 0..nplanes-1 <-> lz = lz0-1+q
+    const int gi = B.plo[0] + lx0 + tx, gj = B.plo[1] + ly0 + ty;
+    const bool col_in = lx0 + tx < B.pdim[0] && ly0 + ty < B.pdim[1];
 
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + NSTAGE * STAGE_BYTES + RING_BYTES);
+    double *ring = reinterpret_cast<double *>(smem + NSTAGE * STAGE_BYTES);
+    auto stage_a = [&](int s) { return reinterpret_cast<double *>(smem + s * STAGE_BYTES); };
+    auto stage_b = [&](int s) { return reinterpret_cast<double *>(smem + s * STAGE_BYTES + SEG_H); };
+    auto stage_c = [&](int s) { return reinterpret_cast<double *>(smem + s * STAGE_BYTES + 2 * SEG_H); };
+
+    const bool use_b = C.map_b != nullptr;
+    const bool use_c = C.map_c != nullptr;
+
+    if (tid == 0) {
+        for (int s = 0; s < NSTAGE; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+
+    auto issue = [&](int q) {  // thread 0 only
+        const int s = q % NSTAGE;
+        const int lz = lz0 - 1 + q;
+        const bool epi = use_c && q >= 1 && q <= nplanes - 2;
+        const uint32_t bytes = (uint32_t)(HC * 8) * (use_b ? 2u : 1u) + (epi ? (uint32_t)SEG_O : 0u);
+        mbar_expect_tx(&full[s], bytes);
+        tma_load3(stage_a(s), C.map_a, lx0 - 1, ly0 - 1, lz, &full[s]);
+        if (use_b) tma_load3(stage_b(s), C.map_b, lx0 - 1, ly0 - 1, lz, &full[s]);
+        if (epi) tma_load3(stage_c(s), C.map_c, lx0, ly0, lz, &full[s]);
+    };
+
+    if (tid == 0)
+        for (int q = 0; q < min(NSTAGE, nplanes); ++q) issue(q);
+
+    // halo cell owned by this thread (tile-local coordinates -1..TX, -1..TY)
     int hci = 0, hcj = 0;
     const bool has_halo = tid < NHALO;
     if (tid < TX) {
@@ -278,43 +364,66 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, double (*sm)[HY][HX], do
         hci = TX;
         hcj = tid - 2 * TX - TY;
     }
+    const int own_cell = (ty + 1) * HX + (tx + 1);
+    const int halo_cell = (hcj + 1) * HX + (hci + 1);
 
-    double u_prev = col_in ? field_at<OP>(C, gi, gj, z0 - 1) : 0.0;
-    int bc = 0;
-    double u_cur = col_in ? field_at<OP>(C, gi, gj, z0) : 0.0;
-    sm[bc][ty + 1][tx + 1] = u_cur;
-    if (has_halo) sm[bc][hcj + 1][hci + 1] = field_at<OP>(C, x0 + hci, y0 + hcj, z0);
+    // u at plane q for one cell: staged operands combined, masked to the region
+    auto u_of = [&](int s, int cell, int i, int j, int k) -> double {
+        const double a = stage_a(s)[cell];
+        double v;
+        if (OP == OP_RESID)
+            v = C.pend ? add(a, mul(C.alpha_pend, stage_b(s)[cell])) : a;
+        else if (OP == OP_S1)
+            v = C.first ? a : add(a, mul(C.beta, stage_b(s)[cell]));
+        else
+            v = a;
+        return in_region(B, i, j, k) ? v : 0.0;
+    };
 
-    for (int k = z0; k < z1; ++k) {
-        const int bn = bc == 2 ? 0 : bc + 1;
-        const double u_next = col_in ? field_at<OP>(C, gi, gj, k + 1) : 0.0;
-        sm[bn][ty + 1][tx + 1] = u_next;
-        if (has_halo) sm[bn][hcj + 1][hci + 1] = field_at<OP>(C, x0 + hci, y0 + hcj, k + 1);
+    auto stage_plane = [&](int q, double *uring) -> double {
+        const int s = q % NSTAGE;
+        mbar_wait(&full[s], (uint32_t)((q / NSTAGE) & 1));
+        const int gk = B.plo[2] + lz0 - 1 + q;
+        const double uo = u_of(s, own_cell, gi, gj, gk);
+        uring[own_cell] = uo;
+        if (has_halo) uring[halo_cell] = u_of(s, halo_cell, gi - tx + hci, gj - ty + hcj, gk);
+        return uo;
+    };
+
+    double u_prev = stage_plane(0, ring + 0 * HC);
+    double u_cur = stage_plane(1, ring + 1 * HC);
+
+    for (int q = 1; q <= nplanes - 2; ++q) {
+        double *rn = ring + ((q + 1) % 3) * HC;
+        const double u_next = stage_plane(q + 1, rn);
         __syncthreads();
-        if (col_in && in_region(B, gi, gj, k)) {
-            const double xm = sm[bc][ty + 1][tx], xp = sm[bc][ty + 1][tx + 2];
-            const double ym = sm[bc][ty][tx + 1], yp = sm[bc][ty + 2][tx + 1];
-            const bool pz = in_region(B, gi, gj, k - 1);
-            const bool py = in_region(B, gi, gj - 1, k);
-            const bool px = in_region(B, gi - 1, gj, k);
+        if (tid == 0 && q - 1 + NSTAGE < nplanes) issue(q - 1 + NSTAGE);  // stage of plane q-1 is free
+        const int gk = B.plo[2] + lz0 - 1 + q;
+        if (col_in && in_region(B, gi, gj, gk)) {
+            const double *rc = ring + (q % 3) * HC;
+            const double xm = rc[own_cell - 1], xp = rc[own_cell + 1];
+            const double ym = rc[own_cell - HX], yp = rc[own_cell + HX];
+            const bool pz = in_region(B, gi, gj, gk - 1);
+            const bool py = in_region(B, gi, gj - 1, gk);
+            const bool px = in_region(B, gi - 1, gj, gk);
             const double au = stencil7(u_prev, ym, xm, u_cur, xp, yp, u_next, pz, py, px);
-            const long long s = sidx(B, gi, gj, k);
+            const long long sx = sidx(B, gi, gj, gk);
+            const int s = q % NSTAGE;
             if (OP == OP_APPLY) {
-                C.yout[s] = au;
+                C.yout[sx] = au;
             } else if (OP == OP_S2) {
-                const double rn = sub(B.r[s], mul(C.alpha, au));
-                B.r[s] = rn;
-                acc[0] = add(acc[0], mul(rn, rn));
+                const double rnv = sub(stage_c(s)[tid], mul(C.alpha, au));
+                B.r[sx] = rnv;
+                acc[0] = add(acc[0], mul(rnv, rnv));
             } else if (OP == OP_S1) {
-                C.pout[s] = u_cur;
-                if (C.pend) B.x[s] = add(B.x[s], mul(C.alpha_pend, C.pin[s]));
+                C.pout[sx] = u_cur;
+                if (C.pend) B.x[sx] = add(stage_c(s)[tid], mul(C.alpha_pend, stage_b(s)[own_cell]));
                 acc[0] = add(acc[0], mul(u_cur, au));
             } else {  // OP_RESID: r = (b - C*halo) - A_ii u
-                const double bv = B.b[s];
-                // neighbours in ascending column order
+                const double bv = stage_c(s)[tid];
                 const int ni[6] = {gi, gi, gi - 1, gi + 1, gi, gi};
                 const int nj[6] = {gj, gj - 1, gj, gj, gj + 1, gj};
-                const int nk[6] = {k - 1, k, k, k, k, k + 1};
+                const int nk[6] = {gk - 1, gk, gk, gk, gk, gk + 1};
                 // coupling row sum C*halo (multisplit.py:333-338): entries of
                 // -1 in ascending column order, reduceat rule first + seq(rest)
                 double first = 0.0, rest = 0.0;
@@ -331,11 +440,11 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, double (*sm)[HY][HX], do
                 }
                 const double rhs = cnt == 0 ? bv : sub(bv, cnt == 1 ? first : add(first, rest));
                 const double rv = sub(rhs, au);
-                B.r[s] = rv;
+                B.r[sx] = rv;
                 acc[0] = add(acc[0], mul(rhs, rhs));
                 const double r2 = mul(rv, rv);
                 acc[1] = add(acc[1], r2);
-                if (in_owned(B, gi, gj, k)) {
+                if (in_owned(B, gi, gj, gk)) {
                     acc[2] = add(acc[2], r2);
                     if (C.want_global) {
                         // global operator row (residual_norms on the gathered
@@ -358,9 +467,8 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, double (*sm)[HY][HX], do
         }
         u_prev = u_cur;
         u_cur = u_next;
-        bc = bn;
     }
-    __syncthreads();  // ring reuse by the next tile of this CTA (none today)
+    __syncthreads();  // every TMA issued was consumed; smem may be reused
 }
 
 // ------------------------------------------------------------------ scalars
@@ -457,8 +565,6 @@ __device__ void transition(const DBlock &B, DState &S, int ph, const double *q) 
     }
 }
 
-
-// Which phases a sweep kernel of op OPK serves.
 template <int OPK>
 __device__ __forceinline__ bool serves(int ph) {
     if (OPK == OP_S1) return ph == PH_S1;
@@ -466,96 +572,130 @@ __device__ __forceinline__ bool serves(int ph) {
     return ph == PH_INIT || ph == PH_VERIFY || ph == PH_RESID;
 }
 
-// One sweep over every block whose phase this kernel serves; the last CTA
-// to finish runs the scalar recurrences of those blocks.  Launched as the
-// cycle RESID -> S1 -> S2, each block advances through its own phase machine
-// (a block in S1 at the start of a cycle completes one CG iteration).
+// One sweep over every block whose phase this kernel serves.  The last CTA of
+// each served block reduces its partials and advances its phase machine; the
+// last CTA of the launch publishes the loop conditions.
 template <int OPK>
-__global__ void __launch_bounds__(NT) k_sweep(const DBlock *__restrict__ blocks, DState *states,
-                                              const int *__restrict__ cta_block, int nblocks, int nctas,
-                                              double *partials, unsigned *counter, int *n_active,
-                                              int want_global) {
-    __shared__ double sm[3][HY][HX];
+__global__ void __launch_bounds__(NT, 4) k_sweep(const KParams P) {
+    extern __shared__ __align__(128) unsigned char smem[];
     __shared__ double red[NQ][NT / 32];
-    __shared__ double scratch[NT];
-    __shared__ bool am_last;
-    const int tid = threadIdx.y * TX + threadIdx.x;
-    const int b = cta_block[blockIdx.x];
-    const DBlock &B = blocks[b];
-    const int ph = states[b].phase;
+    __shared__ int flag;
+    const int tid = threadIdx.x;
+    const int b = P.cta_block[blockIdx.x];
+    const DBlock &B = P.blocks[b];
+    const int ph = P.states[b].phase;
 
-    double acc[NQ] = {0.0, 0.0, 0.0, 0.0};
     if (serves<OPK>(ph)) {
-        const DState S = states[b];
+        double acc[NQ] = {0.0, 0.0, 0.0, 0.0};
+        const DState S = P.states[b];
+        const CUtensorMap *tm = P.tmaps + (size_t)b * NTM;
         SweepCtx C;
         C.B = &B;
-        C.op = OPK;
         C.pend = S.pend != 0;
         C.first = S.first != 0;
-        C.want_global = want_global != 0;
+        C.want_global = true;
         C.alpha_pend = S.alpha_pend;
         C.alpha = S.alpha;
         C.beta = S.beta;
-        C.pin = B.p[S.pcur];
-        C.pout = B.p[S.pcur ^ 1];
-        C.xin = nullptr;
         C.yout = nullptr;
-        sweep_tile<OPK>(C, blockIdx.x - B.cta_begin, sm, acc);
-    }
-    cta_sum(acc, red);
-    if (tid == 0) {
+        C.pout = B.p[S.pcur ^ 1];
+        const CUtensorMap *tm_p = tm + (S.pcur ? TM_P1H : TM_P0H);
+        if (OPK == OP_RESID) {
+            C.map_a = tm + TM_XH;
+            C.map_b = C.pend ? tm_p : nullptr;
+            C.map_c = tm + TM_BO;
+        } else if (OPK == OP_S1) {
+            C.map_a = tm + TM_RH;
+            C.map_b = (!C.first || C.pend) ? tm_p : nullptr;
+            C.map_c = C.pend ? tm + TM_XO : nullptr;
+        } else {
+            C.map_a = tm_p;
+            C.map_b = nullptr;
+            C.map_c = tm + TM_RO;
+        }
+        sweep_tile<OPK>(C, blockIdx.x - B.cta_begin, smem, acc);
+        cta_sum(acc, red);
+        if (tid == 0) {
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) partials[(size_t)q * nctas + blockIdx.x] = acc[q];
-        __threadfence();
-        const unsigned prev = atomicAdd(counter, 1u);
-        am_last = (prev == (unsigned)nctas - 1u);
-    }
-    __syncthreads();
-    if (!am_last) return;
-    __threadfence();
-    int active = 0;
-    for (int bb = 0; bb < nblocks; ++bb) {
-        const int phb = states[bb].phase;
-        if (serves<OPK>(phb)) {
-            const DBlock &BB = blocks[bb];
+            for (int q = 0; q < NQ; ++q) P.partials[(size_t)q * P.nctas + blockIdx.x] = acc[q];
+            __threadfence();
+            const unsigned prev = atomicAdd(&P.blk_counter[b], 1u);
+            flag = (prev == (unsigned)(B.cta_end - B.cta_begin) - 1u);
+        }
+        __syncthreads();
+        if (flag) {  // last tile of block b: reduce and advance its recurrence
+            __threadfence();
+            double *scratch = reinterpret_cast<double *>(smem);
             double q[NQ];
             const int nq = (OPK == OP_RESID) ? NQ : 1;
             for (int i = 0; i < NQ; ++i)
-                q[i] = i < nq ? range_sum(partials + (size_t)i * nctas, BB.cta_begin, BB.cta_end, scratch) : 0.0;
+                q[i] = i < nq ? range_sum(P.partials + (size_t)i * P.nctas, B.cta_begin, B.cta_end, scratch) : 0.0;
             if (tid == 0) {
-                DState S = states[bb];
-                transition(BB, S, phb, q);
-                states[bb] = S;
+                DState Sn = P.states[b];
+                transition(B, Sn, ph, q);
+                P.states[b] = Sn;
+                P.blk_counter[b] = 0u;
+                __threadfence();
             }
-            __syncthreads();
-        }
-        if (tid == 0) {
-            const int p2 = states[bb].phase;
-            if (p2 != PH_DONE && p2 != PH_IDLE) ++active;
         }
     }
+    // launch-wide completion
     if (tid == 0) {
-        *n_active = active;
-        *counter = 0u;
+        __threadfence();
+        const unsigned prev = atomicAdd(P.launch_counter, 1u);
+        flag = (prev == (unsigned)P.nctas - 1u);
+    }
+    __syncthreads();
+    if (!flag || tid != 0) return;
+    __threadfence();
+    int active = 0, verify = 0;
+    for (int bb = 0; bb < P.nblocks; ++bb) {
+        const int p2 = ((volatile DState *)P.states)[bb].phase;
+        if (p2 != PH_DONE && p2 != PH_IDLE) ++active;
+        if (p2 == PH_VERIFY || p2 == PH_INIT || p2 == PH_RESID) ++verify;
+    }
+    if (OPK == OP_S2) {
+        Control &ctl = *P.ctl;
+        ctl.cycles += 1;
+        if (ctl.max_cycles > 0 && ctl.cycles > ctl.max_cycles && active) {
+            // runaway guard: never let a device-side loop spin forever
+            for (int bb = 0; bb < P.nblocks; ++bb) {
+                DState &Sb = P.states[bb];
+                if (Sb.phase != PH_DONE && Sb.phase != PH_IDLE) {
+                    Sb.phase = PH_DONE;
+                    Sb.stop = STOP_STALLED;
+                }
+            }
+            ctl.stalled = 1;
+            active = 0;
+            verify = 0;
+        }
+    }
+    if (OPK == OP_RESID && P.use_graph) P.ctl->resid_runs += 1;
+    *P.n_active = active;
+    *P.launch_counter = 0u;
+    if (P.use_graph) {
+        cudaGraphSetConditional(P.h_loop, active ? 1u : 0u);
+        if (OPK == OP_S2) cudaGraphSetConditional(P.h_verify, verify ? 1u : 0u);
     }
 }
 
-// y = A_ii x on one block (standalone a1).
-__global__ void __launch_bounds__(NT) k_apply(const DBlock *__restrict__ blocks, int b, const double *x,
-                                              double *y) {
-    __shared__ double sm[3][HY][HX];
+// y = A_ii x on one block (standalone a1); x, y in the block's pitched layout.
+__global__ void __launch_bounds__(NT, 4) k_apply(const DBlock *__restrict__ blocks, int b,
+                                                 const __grid_constant__ CUtensorMap xmap, double *y) {
+    extern __shared__ __align__(128) unsigned char smem[];
     const DBlock &B = blocks[b];
     SweepCtx C;
     C.B = &B;
-    C.op = OP_APPLY;
     C.pend = C.first = C.want_global = false;
     C.alpha_pend = C.alpha = C.beta = 0.0;
-    C.pin = nullptr;
+    C.map_a = &xmap;
+    C.map_b = nullptr;
+    C.map_c = nullptr;
     C.pout = nullptr;
-    C.xin = x;
     C.yout = y;
     double acc[NQ] = {0.0, 0.0, 0.0, 0.0};
-    sweep_tile<OP_APPLY>(C, blockIdx.x, sm, acc);
+    sweep_tile<OP_APPLY>(C, blockIdx.x, smem, acc);
 }
 
 // Arm solves / residual sweeps.
@@ -576,8 +716,15 @@ __global__ void k_arm(DState *states, const int *active, int nblocks, int phase,
     }
 }
 
+__global__ void k_reset_control(Control *ctl, int max_cycles) {
+    ctl->cycles = 0;
+    ctl->max_cycles = max_cycles;
+    ctl->stalled = 0;
+    ctl->resid_runs = 0;
+}
+
 // Deferred x += alpha p over every region point of blocks with a pending update.
-__global__ void k_flush(const DBlock *__restrict__ blocks, const DState *states, int nblocks) {
+__global__ void k_flush(const DBlock *__restrict__ blocks, const DState *states) {
     const int b = blockIdx.y;
     const DBlock &B = blocks[b];
     const DState &S = states[b];
@@ -585,13 +732,16 @@ __global__ void k_flush(const DBlock *__restrict__ blocks, const DState *states,
     const long long n = (long long)B.pdim[0] * B.pdim[1] * B.pdim[2];
     const double a = S.alpha_pend;
     const double *p = B.p[S.pcur];
-    for (long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x; s < n;
-         s += (long long)gridDim.x * blockDim.x) {
-        const int i = B.plo[0] + (int)(s % B.pdim[0]);
-        const long long t = s / B.pdim[0];
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < n;
+         c += (long long)gridDim.x * blockDim.x) {
+        const int i = B.plo[0] + (int)(c % B.pdim[0]);
+        const long long t = c / B.pdim[0];
         const int j = B.plo[1] + (int)(t % B.pdim[1]);
         const int k = B.plo[2] + (int)(t / B.pdim[1]);
-        if (B.overlap == 0 || in_region(B, i, j, k)) B.x[s] = add(B.x[s], mul(a, p[s]));
+        if (B.overlap == 0 || in_region(B, i, j, k)) {
+            const long long s = sidx(B, i, j, k);
+            B.x[s] = add(B.x[s], mul(a, p[s]));
+        }
     }
 }
 
@@ -640,33 +790,69 @@ __global__ void k_halo_pack(const DBlock *__restrict__ blocks, const DState *sta
     }
 }
 
+// ------------------------------------------------------------------ host helpers
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+int get_encoder() {
+    if (g_encode) return BS_OK;
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
+        return fail(BS_ECUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    return BS_OK;
+}
+
+// 3-D map over a block's pitched padded box; haloed (TX+2 x TY+2) or bare (TX x TY) plane boxes.
+int encode_map(CUtensorMap *m, const void *ptr, const DBlock &B, bool halo) {
+    if (int e = get_encoder()) return e;
+    cuuint64_t dims[3] = {(cuuint64_t)B.pdim[0], (cuuint64_t)B.pdim[1], (cuuint64_t)B.pdim[2]};
+    cuuint64_t strides[2] = {(cuuint64_t)B.pitch * 8, (cuuint64_t)B.pitch * B.pdim[1] * 8};
+    cuuint32_t box[3] = {(cuuint32_t)(halo ? HX : TX), (cuuint32_t)(halo ? HY : TY), 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void *>(ptr), dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(BS_EINVAL, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return BS_OK;
+}
+
 }  // namespace
 
-// ====================================================================== C ABI
+// ====================================================================== context
 
 static unsigned long long g_launches = 0;  // kernels launched by this library
 
 struct bs_ctx {
     int device = 0;
-    // optional CUDA-event timing of the S1 / S2 / RESID sweep kernels in bs_run
-    bool timing = false;
-    std::vector<cudaEvent_t> ev;   // pairs, reused across batches
-    double op_ms[3] = {0.0, 0.0, 0.0};
-    long long op_n[3] = {0, 0, 0};
     int nblocks = 0;
     int nctas = 0;
     std::vector<DBlock> hblocks;
     DBlock *dblocks = nullptr;
     DState *dstates = nullptr;
+    CUtensorMap *dtmaps = nullptr;
     int *dcta_block = nullptr;
     double *dpartials = nullptr;
-    unsigned *dcounter = nullptr;
+    unsigned *dblk_counter = nullptr;
+    unsigned *dlaunch_counter = nullptr;
     int *dnactive = nullptr;
+    Control *dctl = nullptr;
     int *dactive = nullptr;
     int *dplan = nullptr;
     int plan_cap = 0;
     int *hpinned = nullptr;  // [0]: n_active, [1..]: active mask staging
     DState *hstates = nullptr;
+    Control *hctl = nullptr;
+    // device-side solve loop: RESID ; WHILE(any active) { S1 ; S2 ; IF(any verify) RESID }
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t graph_exec = nullptr;
+    // optional CUDA-event timing of the sweep kernels (launch mode only)
+    bool timing = false;
+    std::vector<cudaEvent_t> ev;
+    double op_ms[3] = {0.0, 0.0, 0.0};
+    long long op_n[3] = {0, 0, 0};
 };
 
 namespace {
@@ -687,23 +873,42 @@ int upload_active(bs_ctx *c, const int32_t *active, cudaStream_t st, const int *
     return BS_OK;
 }
 
+KParams make_params(bs_ctx *c, bool graph, cudaGraphConditionalHandle hl = 0,
+                    cudaGraphConditionalHandle hv = 0) {
+    KParams P;
+    P.blocks = c->dblocks;
+    P.states = c->dstates;
+    P.tmaps = c->dtmaps;
+    P.cta_block = c->dcta_block;
+    P.nblocks = c->nblocks;
+    P.nctas = c->nctas;
+    P.partials = c->dpartials;
+    P.blk_counter = c->dblk_counter;
+    P.launch_counter = c->dlaunch_counter;
+    P.n_active = c->dnactive;
+    P.ctl = c->dctl;
+    P.h_loop = hl;
+    P.h_verify = hv;
+    P.use_graph = graph ? 1 : 0;
+    return P;
+}
+
 template <int OPK>
-static void launch_sweep(bs_ctx *c, cudaStream_t st, int slot) {
-    if (c->timing) cudaEventRecord(c->ev[2 * slot], st);
-    k_sweep<OPK><<<c->nctas, dim3(TX, TY), 0, st>>>(c->dblocks, c->dstates, c->dcta_block, c->nblocks, c->nctas,
-                                                    c->dpartials, c->dcounter, c->dnactive, 1);
-    if (c->timing) cudaEventRecord(c->ev[2 * slot + 1], st);
+void launch_sweep(bs_ctx *c, cudaStream_t st, int slot) {
+    const KParams P = make_params(c, false);
+    if (c->timing && slot >= 0) cudaEventRecord(c->ev[2 * slot], st);
+    k_sweep<OPK><<<c->nctas, NT, SMEM_BYTES, st>>>(P);
+    if (c->timing && slot >= 0) cudaEventRecord(c->ev[2 * slot + 1], st);
     ++g_launches;
 }
 
-static void launch_cycle(bs_ctx *c, cudaStream_t st, int cycle) {
+void launch_cycle(bs_ctx *c, cudaStream_t st, int cycle) {
     launch_sweep<OP_RESID>(c, st, 3 * cycle + 0);
     launch_sweep<OP_S1>(c, st, 3 * cycle + 1);
     launch_sweep<OP_S2>(c, st, 3 * cycle + 2);
 }
 
-// After the batch's stream sync: fold the recorded event pairs into the totals.
-static void harvest_timing(bs_ctx *c, int cycles) {
+void harvest_timing(bs_ctx *c, int cycles) {
     for (int i = 0; i < cycles; ++i)
         for (int o = 0; o < 3; ++o) {
             float ms = 0.f;
@@ -715,7 +920,66 @@ static void harvest_timing(bs_ctx *c, int cycles) {
         }
 }
 
+template <int OPK>
+int add_sweep_node(bs_ctx *c, cudaGraph_t g, cudaGraphNode_t *node, const cudaGraphNode_t *deps, int ndeps,
+                   cudaGraphConditionalHandle hl, cudaGraphConditionalHandle hv) {
+    KParams P = make_params(c, true, hl, hv);  // copied by the runtime at node creation
+    void *args[] = {&P};
+    cudaKernelNodeParams kp = {};
+    kp.func = (void *)k_sweep<OPK>;
+    kp.gridDim = dim3(c->nctas);
+    kp.blockDim = dim3(NT);
+    kp.sharedMemBytes = SMEM_BYTES;
+    kp.kernelParams = args;
+    BS_CU(cudaGraphAddKernelNode(node, g, deps, ndeps, &kp));
+    return BS_OK;
+}
+
+// Graph: RESID (serves INIT) -> WHILE(active) { S1 -> S2 -> IF(verify) { RESID } }
+int build_graph(bs_ctx *c) {
+    if (c->graph_exec) return BS_OK;
+    cudaGraph_t g;
+    BS_CU(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h_loop;
+    BS_CU(cudaGraphConditionalHandleCreate(&h_loop, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNode_t n_init;
+    if (int e = add_sweep_node<OP_RESID>(c, g, &n_init, nullptr, 0, h_loop, 0)) return e;
+
+    cudaGraphNodeParams wp = {};
+    wp.type = cudaGraphNodeTypeConditional;
+    wp.conditional.handle = h_loop;
+    wp.conditional.type = cudaGraphCondTypeWhile;
+    wp.conditional.size = 1;
+    cudaGraphNode_t n_while;
+    BS_CU(cudaGraphAddNode(&n_while, g, &n_init, 1, &wp));
+    cudaGraph_t body = wp.conditional.phGraph_out[0];
+
+    cudaGraphConditionalHandle h_verify;
+    BS_CU(cudaGraphConditionalHandleCreate(&h_verify, body, 0, 0));
+    cudaGraphNode_t n_s1, n_s2;
+    if (int e = add_sweep_node<OP_S1>(c, body, &n_s1, nullptr, 0, h_loop, h_verify)) return e;
+    if (int e = add_sweep_node<OP_S2>(c, body, &n_s2, &n_s1, 1, h_loop, h_verify)) return e;
+    cudaGraphNodeParams ip = {};
+    ip.type = cudaGraphNodeTypeConditional;
+    ip.conditional.handle = h_verify;
+    ip.conditional.type = cudaGraphCondTypeIf;
+    ip.conditional.size = 1;
+    cudaGraphNode_t n_if;
+    BS_CU(cudaGraphAddNode(&n_if, body, &n_s2, 1, &ip));
+    cudaGraph_t ifbody = ip.conditional.phGraph_out[0];
+    cudaGraphNode_t n_v;
+    if (int e = add_sweep_node<OP_RESID>(c, ifbody, &n_v, nullptr, 0, h_loop, h_verify)) return e;
+
+    cudaGraphExec_t ex;
+    BS_CU(cudaGraphInstantiate(&ex, g, 0));
+    c->graph = g;
+    c->graph_exec = ex;
+    return BS_OK;
+}
+
 }  // namespace
+
+// ====================================================================== C ABI
 
 extern "C" {
 
@@ -733,25 +997,28 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
         return e;
     }
     std::vector<int> cta_block;
+    std::vector<CUtensorMap> maps((size_t)nblocks * NTM);
     for (int b = 0; b < nblocks; ++b) {
         const bs_block_desc &d = blocks[b];
         DBlock B;
         std::memset(&B, 0, sizeof(B));
+        if (d.overlap < 0) {
+            delete c;
+            return fail(BS_EINVAL, "bs_ctx_create: overlap must be non-negative");
+        }
         for (int a = 0; a < 3; ++a) {
             B.gn[a] = d.global_dims[a];
             B.lo[a] = d.owned_lo[a];
             B.hi[a] = d.owned_hi[a];
             if (B.gn[a] < 1 || B.lo[a] < 0 || B.hi[a] > B.gn[a] || B.lo[a] >= B.hi[a]) {
                 delete c;
-                return fail(BS_EINVAL, "bs_ctx_create: block " + std::to_string(b) + " has an empty or out-of-grid owned box");
+                return fail(BS_EINVAL,
+                            "bs_ctx_create: block " + std::to_string(b) + " has an empty or out-of-grid owned box");
             }
             B.plo[a] = std::max(0, B.lo[a] - d.overlap);
             B.pdim[a] = std::min(B.gn[a], B.hi[a] + d.overlap) - B.plo[a];
         }
-        if (d.overlap < 0) {
-            delete c;
-            return fail(BS_EINVAL, "bs_ctx_create: overlap must be non-negative");
-        }
+        B.pitch = (B.pdim[0] + PITCH_ALIGN - 1) / PITCH_ALIGN * PITCH_ALIGN;
         B.overlap = d.overlap;
         B.x = d.x;
         B.r = d.r;
@@ -765,16 +1032,22 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
             delete c;
             return fail(BS_EINVAL, "bs_ctx_create: null vector pointer for block " + std::to_string(b));
         }
+        for (const void *ptr :
+             {(const void *)B.x, (const void *)B.r, (const void *)B.p[0], (const void *)B.p[1], (const void *)B.b})
+            if (reinterpret_cast<uintptr_t>(ptr) % 16) {
+                delete c;
+                return fail(BS_EINVAL, "bs_ctx_create: vectors must be 16-byte aligned");
+            }
         B.tiles_x = (B.pdim[0] + TX - 1) / TX;
         B.tiles_y = (B.pdim[1] + TY - 1) / TY;
         int cz = z_chunk;
         if (cz <= 0) {
-            // aim for >= ~16 resident CTAs' worth of work per SM without
-            // chopping z into slivers (each chunk re-stages 2 planes)
+            // enough CTAs for ~4 waves of 4 CTAs/SM, without chopping z into
+            // slivers (each chunk stages 2 extra planes)
             const long long cols = (long long)B.tiles_x * B.tiles_y * nblocks;
-            const long long want = 148LL * 12;
-            long long chunks = (want + cols - 1) / cols;
-            cz = (int)std::max<long long>(16, (B.pdim[2] + chunks - 1) / chunks);
+            const long long want = 148LL * 16;
+            const long long chunks = std::max<long long>(1, (want + cols - 1) / cols);
+            cz = (int)std::max<long long>(24, (B.pdim[2] + chunks - 1) / chunks);
         }
         B.cz = std::min(cz, B.pdim[2]);
         B.tiles_z = (B.pdim[2] + B.cz - 1) / B.cz;
@@ -782,26 +1055,54 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
         const long long ntile = (long long)B.tiles_x * B.tiles_y * B.tiles_z;
         for (long long t = 0; t < ntile; ++t) cta_block.push_back(b);
         B.cta_end = (int)cta_block.size();
+        CUtensorMap *m = &maps[(size_t)b * NTM];
+        int e = 0;
+        if (!e) e = encode_map(&m[TM_XH], B.x, B, true);
+        if (!e) e = encode_map(&m[TM_P0H], B.p[0], B, true);
+        if (!e) e = encode_map(&m[TM_P1H], B.p[1], B, true);
+        if (!e) e = encode_map(&m[TM_RH], B.r, B, true);
+        if (!e) e = encode_map(&m[TM_XO], B.x, B, false);
+        if (!e) e = encode_map(&m[TM_RO], B.r, B, false);
+        if (!e) e = encode_map(&m[TM_BO], B.b, B, false);
+        if (e) {
+            delete c;
+            return e;
+        }
         c->hblocks.push_back(B);
     }
     c->nctas = (int)cta_block.size();
     cudaError_t e = cudaSuccess;
     e = cudaMalloc(&c->dblocks, sizeof(DBlock) * nblocks);
     if (e == cudaSuccess) e = cudaMalloc(&c->dstates, sizeof(DState) * nblocks);
+    if (e == cudaSuccess) e = cudaMalloc(&c->dtmaps, sizeof(CUtensorMap) * maps.size());
     if (e == cudaSuccess) e = cudaMalloc(&c->dcta_block, sizeof(int) * c->nctas);
     if (e == cudaSuccess) e = cudaMalloc(&c->dpartials, sizeof(double) * NQ * c->nctas);
-    if (e == cudaSuccess) e = cudaMalloc(&c->dcounter, sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMalloc(&c->dblk_counter, sizeof(unsigned) * nblocks);
+    if (e == cudaSuccess) e = cudaMalloc(&c->dlaunch_counter, sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMalloc(&c->dnactive, sizeof(int));
+    if (e == cudaSuccess) e = cudaMalloc(&c->dctl, sizeof(Control));
     if (e == cudaSuccess) e = cudaMalloc(&c->dactive, sizeof(int) * nblocks);
     if (e == cudaSuccess) e = cudaHostAlloc(&c->hpinned, sizeof(int) * (nblocks + 1), cudaHostAllocDefault);
     if (e == cudaSuccess) e = cudaHostAlloc(&c->hstates, sizeof(DState) * nblocks, cudaHostAllocDefault);
+    if (e == cudaSuccess) e = cudaHostAlloc(&c->hctl, sizeof(Control), cudaHostAllocDefault);
     if (e == cudaSuccess)
         e = cudaMemcpy(c->dblocks, c->hblocks.data(), sizeof(DBlock) * nblocks, cudaMemcpyHostToDevice);
     if (e == cudaSuccess)
+        e = cudaMemcpy(c->dtmaps, maps.data(), sizeof(CUtensorMap) * maps.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
         e = cudaMemcpy(c->dcta_block, cta_block.data(), sizeof(int) * c->nctas, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemset(c->dstates, 0, sizeof(DState) * nblocks);
-    if (e == cudaSuccess) e = cudaMemset(c->dcounter, 0, sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMemset(c->dblk_counter, 0, sizeof(unsigned) * nblocks);
+    if (e == cudaSuccess) e = cudaMemset(c->dlaunch_counter, 0, sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemset(c->dnactive, 0, sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(c->dctl, 0, sizeof(Control));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_sweep<OP_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_sweep<OP_S1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_sweep<OP_S2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) {
         bs_ctx_destroy(c);
         return fail(BS_ECUDA, std::string("bs_ctx_create: ") + cudaGetErrorString(e));
@@ -813,22 +1114,33 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
 int bs_ctx_destroy(bs_ctx *c) {
     if (!c) return BS_OK;
     cudaSetDevice(c->device);
+    if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+    if (c->graph) cudaGraphDestroy(c->graph);
     cudaFree(c->dblocks);
     cudaFree(c->dstates);
+    cudaFree(c->dtmaps);
     cudaFree(c->dcta_block);
     cudaFree(c->dpartials);
-    cudaFree(c->dcounter);
+    cudaFree(c->dblk_counter);
+    cudaFree(c->dlaunch_counter);
     cudaFree(c->dnactive);
+    cudaFree(c->dctl);
     cudaFree(c->dactive);
     cudaFree(c->dplan);
     for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
     if (c->hpinned) cudaFreeHost(c->hpinned);
     if (c->hstates) cudaFreeHost(c->hstates);
+    if (c->hctl) cudaFreeHost(c->hctl);
     delete c;
     return BS_OK;
 }
 
 int bs_ctx_num_ctas(const bs_ctx *c) { return c ? c->nctas : 0; }
+
+int bs_block_pitch(const bs_ctx *c, int block) {
+    if (!c || block < 0 || block >= c->nblocks) return fail(BS_EINVAL, "bs_block_pitch: bad arguments");
+    return c->hblocks[block].pitch;
+}
 
 unsigned long long bs_launch_count(void) { return g_launches; }
 
@@ -850,10 +1162,13 @@ int bs_timing(bs_ctx *c, int enable, double *ms_out, long long *n_out) {
 
 int bs_stencil_apply(bs_ctx *c, int block, const double *x, double *y, void *stream) {
     if (!c || block < 0 || block >= c->nblocks || !x || !y) return fail(BS_EINVAL, "bs_stencil_apply: bad arguments");
+    if (reinterpret_cast<uintptr_t>(x) % 16) return fail(BS_EINVAL, "bs_stencil_apply: x must be 16-byte aligned");
     if (int e = set_dev(c)) return e;
     const DBlock &B = c->hblocks[block];
+    CUtensorMap xmap;
+    if (int e = encode_map(&xmap, x, B, true)) return e;
     ++g_launches;
-    k_apply<<<B.cta_end - B.cta_begin, dim3(TX, TY), 0, (cudaStream_t)stream>>>(c->dblocks, block, x, y);
+    k_apply<<<B.cta_end - B.cta_begin, NT, SMEM_BYTES, (cudaStream_t)stream>>>(c->dblocks, block, xmap, y);
     BS_CU(cudaGetLastError());
     return BS_OK;
 }
@@ -875,26 +1190,10 @@ int bs_cg_begin(bs_ctx *c, int max_iterations, double tolerance, int basis, cons
     return BS_OK;
 }
 
-int bs_residual(bs_ctx *c, const int32_t *active, void *stream) {
-    if (!c) return fail(BS_EINVAL, "bs_residual: null context");
-    if (int e = set_dev(c)) return e;
-    cudaStream_t st = (cudaStream_t)stream;
-    const int *dact = nullptr;
-    if (int e = upload_active(c, active, st, &dact)) return e;
-    ++g_launches;
-    k_arm<<<(c->nblocks + 127) / 128, 128, 0, st>>>(c->dstates, dact, c->nblocks, PH_RESID, 0, 0.0, 0);
-    ++g_launches;
-    k_sweep<OP_RESID><<<c->nctas, dim3(TX, TY), 0, st>>>(c->dblocks, c->dstates, c->dcta_block, c->nblocks,
-                                                         c->nctas, c->dpartials, c->dcounter, c->dnactive, 1);
-    BS_CU(cudaGetLastError());
-    return BS_OK;
-}
-
 int bs_sweep_resid(bs_ctx *c, void *stream) {
     if (!c) return fail(BS_EINVAL, "bs_sweep_resid: null context");
     if (int e = set_dev(c)) return e;
-    cudaStream_t st = (cudaStream_t)stream;
-    launch_sweep<OP_RESID>(c, st, 0);
+    launch_sweep<OP_RESID>(c, (cudaStream_t)stream, -1);
     BS_CU(cudaGetLastError());
     return BS_OK;
 }
@@ -911,26 +1210,55 @@ int bs_cancel(bs_ctx *c, const int32_t *active, void *stream) {
     return BS_OK;
 }
 
+int bs_residual(bs_ctx *c, const int32_t *active, void *stream) {
+    if (!c) return fail(BS_EINVAL, "bs_residual: null context");
+    if (int e = set_dev(c)) return e;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int *dact = nullptr;
+    if (int e = upload_active(c, active, st, &dact)) return e;
+    ++g_launches;
+    k_arm<<<(c->nblocks + 127) / 128, 128, 0, st>>>(c->dstates, dact, c->nblocks, PH_RESID, 0, 0.0, 0);
+    launch_sweep<OP_RESID>(c, st, -1);
+    BS_CU(cudaGetLastError());
+    return BS_OK;
+}
+
 int bs_run(bs_ctx *c, int batch, int max_launches, void *stream, int64_t *sweeps_out) {
     if (!c) return fail(BS_EINVAL, "bs_run: null context");
     if (batch < 1) batch = 1;
     if (int e = set_dev(c)) return e;
     cudaStream_t st = (cudaStream_t)stream;
+    if (!c->timing) {
+        // device-side loop: one graph launch runs the solves to completion
+        if (int e = build_graph(c)) return e;
+        ++g_launches;
+        k_reset_control<<<1, 1, 0, st>>>(c->dctl, max_launches > 0 ? (max_launches + 2) / 3 : 0);
+        BS_CU(cudaGraphLaunch(c->graph_exec, st));
+        BS_CU(cudaMemcpyAsync(c->hctl, c->dctl, sizeof(Control), cudaMemcpyDeviceToHost, st));
+        BS_CU(cudaStreamSynchronize(st));
+        const Control ctl = *c->hctl;
+        // kernels the graph ran: per cycle S1 + S2, plus every residual sweep
+        g_launches += (long long)ctl.resid_runs + 2LL * ctl.cycles;
+        if (sweeps_out) *sweeps_out = (long long)ctl.resid_runs + 2LL * ctl.cycles;
+        if (ctl.stalled) return fail(BS_ESTATE, "bs_run: solves still active after max_launches sweeps");
+        return BS_OK;
+    }
+    // launch mode with per-kernel CUDA events (profiling)
     int64_t launched = 0;
-    for (;;) {
-        if (c->timing && (int)c->ev.size() < 6 * batch) {
-            for (int i = (int)c->ev.size(); i < 6 * batch; ++i) {
-                cudaEvent_t e;
-                BS_CU(cudaEventCreate(&e));
-                c->ev.push_back(e);
-            }
+    if ((int)c->ev.size() < 6 * batch) {
+        for (int i = (int)c->ev.size(); i < 6 * batch; ++i) {
+            cudaEvent_t e;
+            BS_CU(cudaEventCreate(&e));
+            c->ev.push_back(e);
         }
+    }
+    for (;;) {
         for (int i = 0; i < batch; ++i) launch_cycle(c, st, i);
         launched += 3LL * batch;
         BS_CU(cudaGetLastError());
         BS_CU(cudaMemcpyAsync(c->hpinned, c->dnactive, sizeof(int), cudaMemcpyDeviceToHost, st));
         BS_CU(cudaStreamSynchronize(st));
-        if (c->timing) harvest_timing(c, batch);
+        harvest_timing(c, batch);
         if (c->hpinned[0] == 0) break;
         if (max_launches > 0 && launched >= max_launches) {
             if (sweeps_out) *sweeps_out = launched;
@@ -945,9 +1273,8 @@ int bs_flush(bs_ctx *c, void *stream) {
     if (!c) return fail(BS_EINVAL, "bs_flush: null context");
     if (int e = set_dev(c)) return e;
     cudaStream_t st = (cudaStream_t)stream;
-    ++g_launches;
-    k_flush<<<dim3(592, c->nblocks), 256, 0, st>>>(c->dblocks, c->dstates, c->nblocks);
-    ++g_launches;
+    g_launches += 2;
+    k_flush<<<dim3(592, c->nblocks), 256, 0, st>>>(c->dblocks, c->dstates);
     k_clear_pend<<<(c->nblocks + 127) / 128, 128, 0, st>>>(c->dstates, c->nblocks);
     BS_CU(cudaGetLastError());
     return BS_OK;

@@ -35,10 +35,20 @@ def require_cuda(device) -> "torch.device":
     return dev
 
 
+PITCH_ALIGN = 4  # doubles; must match csrc/bs_engine.cu
+
+
+def row_pitch(nx: int) -> int:
+    return (nx + PITCH_ALIGN - 1) // PITCH_ALIGN * PITCH_ALIGN
+
+
 @dataclass
 class BlockBuffers:
+    """Padded-box vectors of one block, x-fastest with a row pitch."""
+
     owned: Box
     padded: Box
+    pitch: int
     x: "torch.Tensor"
     r: "torch.Tensor"
     p0: "torch.Tensor"
@@ -52,8 +62,22 @@ class BlockBuffers:
         return tuple(self.padded.hi[d] - self.padded.lo[d] for d in range(3))
 
     def view3(self, t: "torch.Tensor") -> "torch.Tensor":
+        """(nz, ny, nx) view of a pitched padded-box vector (non-contiguous)."""
         nx, ny, nz = self.dims
-        return t.view(nz, ny, nx)
+        return t.view(nz, ny, self.pitch)[:, :, :nx]
+
+    def put(self, name: str, flat: "torch.Tensor") -> None:
+        """Store an unpitched x-fastest padded-box vector into ``name``."""
+        nx, ny, nz = self.dims
+        self.view3(getattr(self, name)).copy_(flat.reshape(nz, ny, nx))
+
+    def take(self, name: str) -> "torch.Tensor":
+        """Unpitched contiguous copy of ``name``."""
+        return self.view3(getattr(self, name)).contiguous().reshape(-1)
+
+    def zeros_pitched(self) -> "torch.Tensor":
+        nx, ny, nz = self.dims
+        return torch.zeros(nz * ny * self.pitch, dtype=torch.float64, device=self.x.device)
 
     def owned_slices(self) -> tuple:
         lo, plo = self.owned.lo, self.padded.lo
@@ -80,7 +104,8 @@ class BlockEngine:
             hi = tuple(min(self.grid_shape[d], box.hi[d] + overlap) for d in range(3))
             pad = Box(lo, hi)
             px, py, pz = (hi[d] - lo[d] for d in range(3))
-            n = px * py * pz
+            pitch = row_pitch(px)
+            n = pitch * py * pz
             ghosts = []
             faces = (  # dir -> (exists, plane size)
                 (lo[2] > 0, px * py), (lo[1] > 0, px * pz), (lo[0] > 0, py * pz),
@@ -88,7 +113,7 @@ class BlockEngine:
             for exists, size in faces:
                 ghosts.append(torch.zeros(size, **opts) if exists else None)
             bb = BlockBuffers(
-                owned=box, padded=pad, x=torch.zeros(n, **opts), r=torch.zeros(n, **opts),
+                owned=box, padded=pad, pitch=pitch, x=torch.zeros(n, **opts), r=torch.zeros(n, **opts),
                 p0=torch.zeros(n, **opts), p1=torch.zeros(n, **opts), b=torch.zeros(n, **opts),
                 ghost=ghosts, history=torch.zeros(cap, **opts))
             self.blocks.append(bb)
@@ -110,6 +135,9 @@ class BlockEngine:
                                               ctypes.byref(ctx)))
         self.ctx = ctx
         self.nblocks = len(owned)
+        for i, bb in enumerate(self.blocks):
+            if self.lib.bs_block_pitch(ctx, i) != bb.pitch:
+                raise DeviceError("row pitch mismatch between host and engine")
         self._reports = (_lib.BlockReport * self.nblocks)()
 
     # -- plumbing ---------------------------------------------------------

@@ -90,15 +90,15 @@ def cg_solve(a: StencilOperator, b, x0, spec: InnerSolverSpec, tolerance_basis: 
     xd, _ = as_device_vector(x0, n, eng.device)
     bb = eng.blocks[0]
     with torch.cuda.device(eng.device):
-        bb.b.copy_(bd)
-        bb.x.copy_(xd)
+        bb.put("b", bd)
+        bb.put("x", xd)
         eng.cg_begin(spec.max_iterations, spec.tolerance, tolerance_basis)
         eng.run(batch=batch, max_launches=launch_bound(spec.max_iterations, batch))
         eng.flush()
         rep = eng.reports()[0]
         its = int(rep.iterations_used)
         hist = bb.history[:its].tolist() if its else []
-        x = bb.x  # engine buffer: copied out below, never aliased to the caller
+        x = bb.take("x")  # unpitched copy, never aliased to the engine
     report = InnerSolveReport(its, float(rep.final_relative_residual), STOP_NAMES[int(rep.stop_reason)],
                               hist)
     if host:
@@ -111,7 +111,7 @@ def cg_solve(a: StencilOperator, b, x0, spec: InnerSolverSpec, tolerance_basis: 
     if out is not None:
         out.copy_(x)
         return out, report
-    return x.clone(), report
+    return x, report
 
 
 def gmres_solve(a: StencilOperator, b, x0, spec: InnerSolverSpec, tolerance_basis: str = "rhs"):

@@ -62,10 +62,13 @@ def spmv(a: StencilOperator, x):
     eng = single_block_engine(a, None if not isinstance(x, getattr(torch, "Tensor", ())) or not x.is_cuda
                               else x.device)
     xd, host = as_device_vector(x, n, eng.device)
-    xd = xd.contiguous()
-    y = torch.empty_like(xd)
+    bb = eng.blocks[0]
     with torch.cuda.device(eng.device):
-        eng.apply(0, xd, y)
+        xp = bb.zeros_pitched()
+        yp = bb.zeros_pitched()
+        bb.view3(xp).copy_(xd.reshape(a.nz, a.ny, a.nx))
+        eng.apply(0, xp, yp)
+        y = bb.view3(yp).contiguous().reshape(-1)
     return y.cpu().numpy() if host else y
 
 
@@ -77,8 +80,8 @@ def residual_norms(a: StencilOperator, x, b) -> tuple:
     bd, _ = as_device_vector(b, n, eng.device)
     bb = eng.blocks[0]
     with torch.cuda.device(eng.device):
-        bb.b.copy_(bd)
-        bb.x.copy_(xd)
+        bb.put("b", bd)
+        bb.put("x", xd)
         eng.residual()
         rep = eng.reports()[0]
     absolute = float(np.sqrt(rep.r_sq))
