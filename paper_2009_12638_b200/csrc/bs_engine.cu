@@ -76,7 +76,8 @@ constexpr int SEG_H = ((HC * 8 + 127) / 128) * 128;  // haloed tile, 128B aligne
 constexpr int SEG_O = NT * 8;                         // bare tile
 constexpr int STAGE_BYTES = 2 * SEG_H + SEG_O;
 constexpr int RING_BYTES = ((3 * HC * 8 + 127) / 128) * 128;
-constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + RING_BYTES + NSTAGE * 8;
+constexpr int SMEM_USED = NSTAGE * STAGE_BYTES + RING_BYTES + NSTAGE * 8;
+constexpr int SMEM_BYTES = SMEM_USED + 128;  // + slack to realign the dynamic base
 
 enum Phase : int {
     PH_IDLE = 0,
@@ -224,14 +225,33 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
                  : "memory");
 }
 
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+__device__ __forceinline__ bool mbar_try(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
     asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "BS_WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra BS_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
+    return ok != 0;
+}
+
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Wait for a TMA stage.  A transfer that never completes (a bug, never a
+// legal state) traps after ~4 s instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    if (mbar_try(bar, parity)) return;
+    const unsigned long long t0 = global_ns();
+    for (unsigned n = 1;; ++n) {
+        if (mbar_try(bar, parity)) return;
+        if ((n & 1023u) == 0 && global_ns() - t0 > 4000000000ull) asm volatile("trap;");
+    }
 }
 
 __device__ __forceinline__ void tma_load3(void *dst, const CUtensorMap *map, int c0, int c1, int c2,
@@ -575,9 +595,14 @@ __device__ __forceinline__ bool serves(int ph) {
 // One sweep over every block whose phase this kernel serves.  The last CTA of
 // each served block reduces its partials and advances its phase machine; the
 // last CTA of the launch publishes the loop conditions.
+__device__ __forceinline__ unsigned char *aligned_smem(unsigned char *raw) {
+    return reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(raw) + 127) & ~uintptr_t(127));
+}
+
 template <int OPK>
 __global__ void __launch_bounds__(NT, 4) k_sweep(const KParams P) {
-    extern __shared__ __align__(128) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    unsigned char *smem = aligned_smem(smem_raw);
     __shared__ double red[NQ][NT / 32];
     __shared__ int flag;
     const int tid = threadIdx.x;
@@ -683,7 +708,8 @@ __global__ void __launch_bounds__(NT, 4) k_sweep(const KParams P) {
 // y = A_ii x on one block (standalone a1); x, y in the block's pitched layout.
 __global__ void __launch_bounds__(NT, 4) k_apply(const DBlock *__restrict__ blocks, int b,
                                                  const __grid_constant__ CUtensorMap xmap, double *y) {
-    extern __shared__ __align__(128) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    unsigned char *smem = aligned_smem(smem_raw);
     const DBlock &B = blocks[b];
     SweepCtx C;
     C.B = &B;
