@@ -64,15 +64,19 @@ int fail(int code, const std::string &msg) {
 constexpr int TX = 32;
 constexpr int TY = 8;
 constexpr int NT = TX * TY;
-constexpr int HX = TX + 2;
+constexpr int HX = TX + 2;             // u-ring row: tile + 1-cell halo
 constexpr int HY = TY + 2;
-constexpr int HC = HX * HY;            // haloed tile cells
+constexpr int HC = HX * HY;            // u-ring cells
+// TMA boxes must start on a 16-byte boundary in the innermost dimension, so
+// the staged haloed box spans x in [x0-2, x0+TX+2): 2 cells left, 2 right.
+constexpr int SX = TX + 4;
+constexpr int SC = SX * HY;            // staged haloed-box cells
 constexpr int NHALO = 2 * TX + 2 * TY; // halo cells
 constexpr int NQ = 4;                  // partial sums per CTA
 constexpr int NSTAGE = 5;              // TMA ring depth (NSTAGE-2 planes of lookahead)
 constexpr int PITCH_ALIGN = 4;         // doubles
 
-constexpr int SEG_H = ((HC * 8 + 127) / 128) * 128;  // haloed tile, 128B aligned
+constexpr int SEG_H = ((SC * 8 + 127) / 128) * 128;  // staged haloed box, 128B aligned
 constexpr int SEG_O = NT * 8;                         // bare tile
 constexpr int STAGE_BYTES = 2 * SEG_H + SEG_O;
 constexpr int RING_BYTES = ((3 * HC * 8 + 127) / 128) * 128;
@@ -358,10 +362,10 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
         const int s = q % NSTAGE;
         const int lz = lz0 - 1 + q;
         const bool epi = use_c && q >= 1 && q <= nplanes - 2;
-        const uint32_t bytes = (uint32_t)(HC * 8) * (use_b ? 2u : 1u) + (epi ? (uint32_t)SEG_O : 0u);
+        const uint32_t bytes = (uint32_t)(SC * 8) * (use_b ? 2u : 1u) + (epi ? (uint32_t)SEG_O : 0u);
         mbar_expect_tx(&full[s], bytes);
-        tma_load3(stage_a(s), C.map_a, lx0 - 1, ly0 - 1, lz, &full[s]);
-        if (use_b) tma_load3(stage_b(s), C.map_b, lx0 - 1, ly0 - 1, lz, &full[s]);
+        tma_load3(stage_a(s), C.map_a, lx0 - 2, ly0 - 1, lz, &full[s]);
+        if (use_b) tma_load3(stage_b(s), C.map_b, lx0 - 2, ly0 - 1, lz, &full[s]);
         if (epi) tma_load3(stage_c(s), C.map_c, lx0, ly0, lz, &full[s]);
     };
 
@@ -384,8 +388,10 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
         hci = TX;
         hcj = tid - 2 * TX - TY;
     }
-    const int own_cell = (ty + 1) * HX + (tx + 1);
+    const int own_cell = (ty + 1) * HX + (tx + 1);     // u ring
     const int halo_cell = (hcj + 1) * HX + (hci + 1);
+    const int own_st = (ty + 1) * SX + (tx + 2);       // staged haloed box
+    const int halo_st = (hcj + 1) * SX + (hci + 2);
 
     // u at plane q for one cell: staged operands combined, masked to the region
     auto u_of = [&](int s, int cell, int i, int j, int k) -> double {
@@ -404,9 +410,9 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
         const int s = q % NSTAGE;
         mbar_wait(&full[s], (uint32_t)((q / NSTAGE) & 1));
         const int gk = B.plo[2] + lz0 - 1 + q;
-        const double uo = u_of(s, own_cell, gi, gj, gk);
+        const double uo = u_of(s, own_st, gi, gj, gk);
         uring[own_cell] = uo;
-        if (has_halo) uring[halo_cell] = u_of(s, halo_cell, gi - tx + hci, gj - ty + hcj, gk);
+        if (has_halo) uring[halo_cell] = u_of(s, halo_st, gi - tx + hci, gj - ty + hcj, gk);
         return uo;
     };
 
@@ -437,7 +443,7 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
                 acc[0] = add(acc[0], mul(rnv, rnv));
             } else if (OP == OP_S1) {
                 C.pout[sx] = u_cur;
-                if (C.pend) B.x[sx] = add(stage_c(s)[tid], mul(C.alpha_pend, stage_b(s)[own_cell]));
+                if (C.pend) B.x[sx] = add(stage_c(s)[tid], mul(C.alpha_pend, stage_b(s)[own_st]));
                 acc[0] = add(acc[0], mul(u_cur, au));
             } else {  // OP_RESID: r = (b - C*halo) - A_ii u
                 const double bv = stage_c(s)[tid];
@@ -831,12 +837,13 @@ int get_encoder() {
     return BS_OK;
 }
 
-// 3-D map over a block's pitched padded box; haloed (TX+2 x TY+2) or bare (TX x TY) plane boxes.
+// 3-D map over a block's pitched padded box; haloed (TX+4 x TY+2) or bare (TX x TY) plane boxes.
+// Box starts are 16-byte aligned in x: tile origins are multiples of TX, haloed boxes start at x0-2.
 int encode_map(CUtensorMap *m, const void *ptr, const DBlock &B, bool halo) {
     if (int e = get_encoder()) return e;
     cuuint64_t dims[3] = {(cuuint64_t)B.pdim[0], (cuuint64_t)B.pdim[1], (cuuint64_t)B.pdim[2]};
     cuuint64_t strides[2] = {(cuuint64_t)B.pitch * 8, (cuuint64_t)B.pitch * B.pdim[1] * 8};
-    cuuint32_t box[3] = {(cuuint32_t)(halo ? HX : TX), (cuuint32_t)(halo ? HY : TY), 1};
+    cuuint32_t box[3] = {(cuuint32_t)(halo ? SX : TX), (cuuint32_t)(halo ? HY : TY), 1};
     cuuint32_t es[3] = {1, 1, 1};
     CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void *>(ptr), dims, strides, box, es,
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
