@@ -61,27 +61,23 @@ int fail(int code, const std::string &msg) {
             return fail(BS_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
-constexpr int TX = 32;
-constexpr int TY = 8;
-constexpr int NT = TX * TY;
-constexpr int HX = TX + 2;             // u-ring row: tile + 1-cell halo
+constexpr int TX = 32;                 // tile width  (one consumer lane per column)
+constexpr int TY = 8;                  // tile height (one consumer warp per row)
+constexpr int NT = TX * TY;            // consumer threads
+constexpr int NTHR = NT + 32;          // + one TMA producer warp
 constexpr int HY = TY + 2;
-constexpr int HC = HX * HY;            // u-ring cells
 // TMA boxes must start on a 16-byte boundary in the innermost dimension, so
 // the staged haloed box spans x in [x0-2, x0+TX+2): 2 cells left, 2 right.
 constexpr int SX = TX + 4;
 constexpr int SC = SX * HY;            // staged haloed-box cells
-constexpr int NHALO = 2 * TX + 2 * TY; // halo cells
 constexpr int NQ = 4;                  // partial sums per CTA
-constexpr int NSTAGE = 5;              // TMA ring depth (NSTAGE-2 planes of lookahead)
+constexpr int NSTAGE = 6;              // TMA ring depth
 constexpr int PITCH_ALIGN = 4;         // doubles
 
 constexpr int SEG_H = ((SC * 8 + 127) / 128) * 128;  // staged haloed box, 128B aligned
 constexpr int SEG_O = NT * 8;                         // bare tile
 constexpr int STAGE_BYTES = 2 * SEG_H + SEG_O;
-constexpr int RING_BYTES = ((3 * HC * 8 + 127) / 128) * 128;
-constexpr int SMEM_USED = NSTAGE * STAGE_BYTES + RING_BYTES + NSTAGE * 8;
-constexpr int SMEM_BYTES = SMEM_USED + 128;  // + slack to realign the dynamic base
+constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + 2 * NSTAGE * 8;
 
 enum Phase : int {
     PH_IDLE = 0,
@@ -275,34 +271,39 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-// Deterministic CTA reduction of NQ values; result valid in thread 0.
-__device__ __forceinline__ void cta_sum(double (&acc)[NQ], double (*red)[NT / 32]) {
+// Deterministic CTA reduction of NQ values over all NTHR threads; result
+// valid in thread 0.  `red` is NQ x (NTHR/32) doubles of shared memory.
+__device__ __forceinline__ void cta_sum(double (&acc)[NQ], double *red) {
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = NTHR / 32;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
         double v = warp_sum(acc[q]);
-        if (lane == 0) red[q][warp] = v;
+        if (lane == 0) red[q * NW + warp] = v;
     }
     __syncthreads();
     if (tid == 0) {
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
-            double s = red[q][0];
-            for (int w = 1; w < NT / 32; ++w) s = add(s, red[q][w]);
+            double s = red[q * NW];
+            for (int w = 1; w < NW; ++w) s = add(s, red[q * NW + w]);
             acc[q] = s;
         }
     }
 }
 
-// Sum of partials[begin:end) with a fixed strided + tree order (whole CTA).
+// Sum of partials[begin:end) with a fixed strided + tree order (whole CTA);
+// scratch holds 256 doubles.
 __device__ double range_sum(const double *part, int begin, int end, double *scratch) {
     const int tid = threadIdx.x;
-    double s = 0.0;
-    for (int c = begin + tid; c < end; c += NT) s = add(s, __ldcg(part + c));
-    scratch[tid] = s;
+    if (tid < 256) {
+        double s = 0.0;
+        for (int c = begin + tid; c < end; c += 256) s = add(s, __ldcg(part + c));
+        scratch[tid] = s;
+    }
     __syncthreads();
-    for (int w = NT / 2; w > 0; w >>= 1) {
+    for (int w = 128; w > 0; w >>= 1) {
         if (tid < w) scratch[tid] = add(scratch[tid], scratch[tid + w]);
         __syncthreads();
     }
@@ -324,177 +325,187 @@ struct SweepCtx {
     double *yout;              // APPLY output
 };
 
-// Process one tile of one block.
-template <int OP>
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Process one tile (TX x TY columns, planes [lz0, lz1) of the padded box).
+//
+// Warp roles: warps 0..TY-1 consume (lane = x, warp = y of the tile), warp TY
+// produces: its lane 0 streams plane q = 0..nplanes-1 (lz = lz0-1+q) into
+// stage q % NSTAGE with TMA, after every consumer warp released that stage's
+// previous plane (empty mbarrier, count TY).  Consumers never block on each
+// other — only on `full` — so there is no CTA-wide barrier per plane.
+//
+// BOX (overlap 0, region == padded box): TMA zero-fill supplies the absent
+// neighbours, presence tests are local-coordinate compares and couplings only
+// exist on the box faces.  !BOX evaluates the L1-dilated region analytically.
+template <int OP, bool BOX>
 __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, double (&acc)[NQ]) {
     const DBlock &B = *C.B;
     const int tid = threadIdx.x;
-    const int tx = tid % TX, ty = tid / TX;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int pdx = B.pdim[0], pdy = B.pdim[1], pdz = B.pdim[2];
+    const int tiles_x = B.tiles_x, tiles_y = B.tiles_y, cz = B.cz;
     int t = tile;
-    const int ix = t % B.tiles_x;
-    t /= B.tiles_x;
-    const int iy = t % B.tiles_y;
-    const int iz = t / B.tiles_y;
-    const int lx0 = ix * TX, ly0 = iy * TY;       // tile origin, padded-box coordinates
-    const int lz0 = iz * B.cz;
-    const int lz1 = min(lz0 + B.cz, B.pdim[2]);
-    const int nplanes = lz1 - lz0 + 2;            // q = 0..nplanes-1 <-> lz = lz0-1+q
-    const int gi = B.plo[0] + lx0 + tx, gj = B.plo[1] + ly0 + ty;
-    const bool col_in = lx0 + tx < B.pdim[0] && ly0 + ty < B.pdim[1];
+    const int ix = t % tiles_x;
+    t /= tiles_x;
+    const int iy = t % tiles_y;
+    const int iz = t / tiles_y;
+    const int lx0 = ix * TX, ly0 = iy * TY;  // tile origin, padded-box coordinates
+    const int lz0 = iz * cz;
+    const int lz1 = min(lz0 + cz, pdz);
+    const int nplanes = lz1 - lz0 + 2;       // q = 0..nplanes-1 <-> lz = lz0-1+q
 
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + NSTAGE * STAGE_BYTES + RING_BYTES);
-    double *ring = reinterpret_cast<double *>(smem + NSTAGE * STAGE_BYTES);
-    auto stage_a = [&](int s) { return reinterpret_cast<double *>(smem + s * STAGE_BYTES); };
-    auto stage_b = [&](int s) { return reinterpret_cast<double *>(smem + s * STAGE_BYTES + SEG_H); };
-    auto stage_c = [&](int s) { return reinterpret_cast<double *>(smem + s * STAGE_BYTES + 2 * SEG_H); };
-
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + NSTAGE * STAGE_BYTES);
+    uint64_t *empty = full + NSTAGE;
     const bool use_b = C.map_b != nullptr;
     const bool use_c = C.map_c != nullptr;
 
     if (tid == 0) {
-        for (int s = 0; s < NSTAGE; ++s) mbar_init(&full[s], 1);
+        for (int s = 0; s < NSTAGE; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], TY);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncthreads();
 
-    auto issue = [&](int q) {  // thread 0 only
-        const int s = q % NSTAGE;
-        const int lz = lz0 - 1 + q;
-        const bool epi = use_c && q >= 1 && q <= nplanes - 2;
-        const uint32_t bytes = (uint32_t)(SC * 8) * (use_b ? 2u : 1u) + (epi ? (uint32_t)SEG_O : 0u);
-        mbar_expect_tx(&full[s], bytes);
-        tma_load3(stage_a(s), C.map_a, lx0 - 2, ly0 - 1, lz, &full[s]);
-        if (use_b) tma_load3(stage_b(s), C.map_b, lx0 - 2, ly0 - 1, lz, &full[s]);
-        if (epi) tma_load3(stage_c(s), C.map_c, lx0, ly0, lz, &full[s]);
-    };
-
-    if (tid == 0)
-        for (int q = 0; q < min(NSTAGE, nplanes); ++q) issue(q);
-
-    // halo cell owned by this thread (tile-local coordinates -1..TX, -1..TY)
-    int hci = 0, hcj = 0;
-    const bool has_halo = tid < NHALO;
-    if (tid < TX) {
-        hci = tid;
-        hcj = -1;
-    } else if (tid < 2 * TX) {
-        hci = tid - TX;
-        hcj = TY;
-    } else if (tid < 2 * TX + TY) {
-        hci = -1;
-        hcj = tid - 2 * TX;
-    } else {
-        hci = TX;
-        hcj = tid - 2 * TX - TY;
+    if (warp == TY) {  // ---------------- TMA producer warp
+        if (lane == 0) {
+            for (int q = 0; q < nplanes; ++q) {
+                const int s = q % NSTAGE;
+                if (q >= NSTAGE) mbar_wait(&empty[s], (uint32_t)((q / NSTAGE - 1) & 1));
+                const int lz = lz0 - 1 + q;
+                const bool epi = use_c && q >= 1 && q <= nplanes - 2;
+                unsigned char *st = smem + s * STAGE_BYTES;
+                const uint32_t bytes = (uint32_t)(SC * 8) * (use_b ? 2u : 1u) + (epi ? (uint32_t)SEG_O : 0u);
+                mbar_expect_tx(&full[s], bytes);
+                tma_load3(st, C.map_a, lx0 - 2, ly0 - 1, lz, &full[s]);
+                if (use_b) tma_load3(st + SEG_H, C.map_b, lx0 - 2, ly0 - 1, lz, &full[s]);
+                if (epi) tma_load3(st + 2 * SEG_H, C.map_c, lx0, ly0, lz, &full[s]);
+            }
+        }
+        __syncwarp();
+        return;
     }
-    const int own_cell = (ty + 1) * HX + (tx + 1);     // u ring
-    const int halo_cell = (hcj + 1) * HX + (hci + 1);
-    const int own_st = (ty + 1) * SX + (tx + 2);       // staged haloed box
-    const int halo_st = (hcj + 1) * SX + (hci + 2);
 
-    // u at plane q for one cell: staged operands combined, masked to the region
-    auto u_of = [&](int s, int cell, int i, int j, int k) -> double {
-        const double a = stage_a(s)[cell];
-        double v;
-        if (OP == OP_RESID)
-            v = C.pend ? add(a, mul(C.alpha_pend, stage_b(s)[cell])) : a;
-        else if (OP == OP_S1)
-            v = C.first ? a : add(a, mul(C.beta, stage_b(s)[cell]));
-        else
-            v = a;
-        return in_region(B, i, j, k) ? v : 0.0;
+    // ---------------- consumers
+    const int tx = lane, ty = warp;
+    const int lx = lx0 + tx, ly = ly0 + ty;
+    const bool col_in = lx < pdx && ly < pdy;
+    const int gi = B.plo[0] + lx, gj = B.plo[1] + ly;
+    const int own = (ty + 1) * SX + (tx + 2);
+    const long long plane = (long long)B.pitch * pdy;
+    long long sx = (long long)lx + (long long)B.pitch * ((long long)ly + (long long)pdy * lz0);
+    const double beta = C.beta, alpha = C.alpha, alpha_pend = C.alpha_pend;
+    const bool pend = C.pend, first = C.first;
+
+    auto val = [&](const unsigned char *st, int cell) -> double {
+        const double a = reinterpret_cast<const double *>(st)[cell];
+        if (OP == OP_RESID) return pend ? add(a, mul(alpha_pend, reinterpret_cast<const double *>(st + SEG_H)[cell])) : a;
+        if (OP == OP_S1) return first ? a : add(a, mul(beta, reinterpret_cast<const double *>(st + SEG_H)[cell]));
+        return a;
+    };
+    // u at a cell of plane lz (local z), masked to the region for !BOX
+    auto uval = [&](const unsigned char *st, int cell, int dx, int dy, int lz) -> double {
+        const double v = val(st, cell);
+        if (BOX) return v;
+        return in_region(B, gi + dx, gj + dy, B.plo[2] + lz) ? v : 0.0;
     };
 
-    auto stage_plane = [&](int q, double *uring) -> double {
-        const int s = q % NSTAGE;
-        mbar_wait(&full[s], (uint32_t)((q / NSTAGE) & 1));
-        const int gk = B.plo[2] + lz0 - 1 + q;
-        const double uo = u_of(s, own_st, gi, gj, gk);
-        uring[own_cell] = uo;
-        if (has_halo) uring[halo_cell] = u_of(s, halo_st, gi - tx + hci, gj - ty + hcj, gk);
-        return uo;
-    };
+    mbar_wait(&full[0], 0u);
+    double u_prev = uval(smem, own, 0, 0, lz0 - 1);
+    mbar_wait(&full[1 % NSTAGE], 0u);
+    double u_cur = uval(smem + (1 % NSTAGE) * STAGE_BYTES, own, 0, 0, lz0);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[0]);
 
-    double u_prev = stage_plane(0, ring + 0 * HC);
-    double u_cur = stage_plane(1, ring + 1 * HC);
-
+    const bool px_box = lx > 0, py_box = ly > 0;
     for (int q = 1; q <= nplanes - 2; ++q) {
-        double *rn = ring + ((q + 1) % 3) * HC;
-        const double u_next = stage_plane(q + 1, rn);
-        __syncthreads();
-        if (tid == 0 && q - 1 + NSTAGE < nplanes) issue(q - 1 + NSTAGE);  // stage of plane q-1 is free
-        const int gk = B.plo[2] + lz0 - 1 + q;
-        if (col_in && in_region(B, gi, gj, gk)) {
-            const double *rc = ring + (q % 3) * HC;
-            const double xm = rc[own_cell - 1], xp = rc[own_cell + 1];
-            const double ym = rc[own_cell - HX], yp = rc[own_cell + HX];
-            const bool pz = in_region(B, gi, gj, gk - 1);
-            const bool py = in_region(B, gi, gj - 1, gk);
-            const bool px = in_region(B, gi - 1, gj, gk);
+        const int s = q % NSTAGE, sn = (q + 1) % NSTAGE;
+        const int lz = lz0 - 1 + q;
+        const unsigned char *st = smem + s * STAGE_BYTES;
+        mbar_wait(&full[sn], (uint32_t)(((q + 1) / NSTAGE) & 1));
+        const double u_next = uval(smem + sn * STAGE_BYTES, own, 0, 0, lz + 1);
+        const bool here = BOX ? col_in : (col_in && in_region(B, gi, gj, B.plo[2] + lz));
+        if (here) {
+            const double xm = uval(st, own - 1, -1, 0, lz), xp = uval(st, own + 1, 1, 0, lz);
+            const double ym = uval(st, own - SX, 0, -1, lz), yp = uval(st, own + SX, 0, 1, lz);
+            bool pz, py, px;
+            if (BOX) {
+                pz = lz > 0;
+                py = py_box;
+                px = px_box;
+            } else {
+                const int gk = B.plo[2] + lz;
+                pz = in_region(B, gi, gj, gk - 1);
+                py = in_region(B, gi, gj - 1, gk);
+                px = in_region(B, gi - 1, gj, gk);
+            }
             const double au = stencil7(u_prev, ym, xm, u_cur, xp, yp, u_next, pz, py, px);
-            const long long sx = sidx(B, gi, gj, gk);
-            const int s = q % NSTAGE;
+            const double *cst = reinterpret_cast<const double *>(st + 2 * SEG_H);
             if (OP == OP_APPLY) {
                 C.yout[sx] = au;
             } else if (OP == OP_S2) {
-                const double rnv = sub(stage_c(s)[tid], mul(C.alpha, au));
+                const double rnv = sub(cst[tid], mul(alpha, au));
                 B.r[sx] = rnv;
                 acc[0] = add(acc[0], mul(rnv, rnv));
             } else if (OP == OP_S1) {
                 C.pout[sx] = u_cur;
-                if (C.pend) B.x[sx] = add(stage_c(s)[tid], mul(C.alpha_pend, stage_b(s)[own_st]));
+                if (pend) B.x[sx] = add(cst[tid], mul(alpha_pend, reinterpret_cast<const double *>(st + SEG_H)[own]));
                 acc[0] = add(acc[0], mul(u_cur, au));
             } else {  // OP_RESID: r = (b - C*halo) - A_ii u
-                const double bv = stage_c(s)[tid];
-                const int ni[6] = {gi, gi, gi - 1, gi + 1, gi, gi};
-                const int nj[6] = {gj, gj - 1, gj, gj, gj + 1, gj};
-                const int nk[6] = {gk - 1, gk, gk, gk, gk, gk + 1};
-                // coupling row sum C*halo (multisplit.py:333-338): entries of
-                // -1 in ascending column order, reduceat rule first + seq(rest)
-                double first = 0.0, rest = 0.0;
-                int cnt = 0;
+                const double bv = cst[tid];
+                const int gk = B.plo[2] + lz;
+                const bool face = !BOX || lx == 0 || ly == 0 || lz == 0 || lx == pdx - 1 || ly == pdy - 1 ||
+                                  lz == pdz - 1;
+                double rhs = bv, rg_au = au;
+                if (face) {
+                    const int ni[6] = {gi, gi, gi - 1, gi + 1, gi, gi};
+                    const int nj[6] = {gj, gj - 1, gj, gj, gj + 1, gj};
+                    const int nk[6] = {gk - 1, gk, gk, gk, gk, gk + 1};
+                    // coupling row sum C*halo (multisplit.py:333-338): entries of
+                    // -1 in ascending column order, reduceat rule first + seq(rest)
+                    double firstc = 0.0, rest = 0.0;
+                    int cnt = 0;
+                    double v[6] = {u_prev, ym, xm, xp, yp, u_next};
+                    bool pg[6];
 #pragma unroll
-                for (int d = 0; d < 6; ++d) {
-                    if (in_grid(B, ni[d], nj[d], nk[d]) && !in_region(B, ni[d], nj[d], nk[d])) {
-                        const double term = -ghost_at(B, ni[d], nj[d], nk[d], d);
-                        if (cnt == 0) first = term;
-                        else if (cnt == 1) rest = term;
-                        else rest = add(rest, term);
-                        ++cnt;
+                    for (int d = 0; d < 6; ++d) {
+                        pg[d] = in_grid(B, ni[d], nj[d], nk[d]);
+                        if (pg[d] && !in_region(B, ni[d], nj[d], nk[d])) {
+                            const double h = ghost_at(B, ni[d], nj[d], nk[d], d);
+                            v[d] = h;  // global operator sees the coupled value
+                            if (cnt == 0) firstc = -h;
+                            else if (cnt == 1) rest = -h;
+                            else rest = add(rest, -h);
+                            ++cnt;
+                        }
                     }
+                    if (cnt) rhs = sub(bv, cnt == 1 ? firstc : add(firstc, rest));
+                    // global operator row (residual_norms on the gathered iterate)
+                    rg_au = stencil7(v[0], v[1], v[2], u_cur, v[3], v[4], v[5], pg[0], pg[1], pg[2]);
                 }
-                const double rhs = cnt == 0 ? bv : sub(bv, cnt == 1 ? first : add(first, rest));
                 const double rv = sub(rhs, au);
                 B.r[sx] = rv;
                 acc[0] = add(acc[0], mul(rhs, rhs));
                 const double r2 = mul(rv, rv);
                 acc[1] = add(acc[1], r2);
-                if (in_owned(B, gi, gj, gk)) {
+                if (BOX || in_owned(B, gi, gj, gk)) {
                     acc[2] = add(acc[2], r2);
-                    if (C.want_global) {
-                        // global operator row (residual_norms on the gathered
-                        // iterate): couplings enter the stencil as present terms
-                        double v[6] = {u_prev, ym, xm, xp, yp, u_next};
-                        bool pg[6];
-#pragma unroll
-                        for (int d = 0; d < 6; ++d) {
-                            pg[d] = in_grid(B, ni[d], nj[d], nk[d]);
-                            if (pg[d] && !in_region(B, ni[d], nj[d], nk[d]))
-                                v[d] = ghost_at(B, ni[d], nj[d], nk[d], d);
-                        }
-                        const double ag =
-                            stencil7(v[0], v[1], v[2], u_cur, v[3], v[4], v[5], pg[0], pg[1], pg[2]);
-                        const double rg = sub(bv, ag);
-                        acc[3] = add(acc[3], mul(rg, rg));
-                    }
+                    const double rg = sub(bv, rg_au);
+                    acc[3] = add(acc[3], mul(rg, rg));
                 }
             }
         }
+        sx += plane;
         u_prev = u_cur;
         u_cur = u_next;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
     }
-    __syncthreads();  // every TMA issued was consumed; smem may be reused
 }
 
 // ------------------------------------------------------------------ scalars
@@ -601,20 +612,19 @@ __device__ __forceinline__ bool serves(int ph) {
 // One sweep over every block whose phase this kernel serves.  The last CTA of
 // each served block reduces its partials and advances its phase machine; the
 // last CTA of the launch publishes the loop conditions.
-__device__ __forceinline__ unsigned char *aligned_smem(unsigned char *raw) {
-    return reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(raw) + 127) & ~uintptr_t(127));
-}
-
-template <int OPK>
-__global__ void __launch_bounds__(NT, 4) k_sweep(const KParams P) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    unsigned char *smem = aligned_smem(smem_raw);
-    __shared__ double red[NQ][NT / 32];
-    __shared__ int flag;
+// One sweep over every block whose phase this kernel serves.  The last CTA of
+// each served block reduces its partials and advances its phase machine; the
+// last CTA of the launch publishes the loop conditions.
+template <int OPK, bool BOX>
+__global__ void __launch_bounds__(NTHR, 3) k_sweep(const KParams P) {
+    extern __shared__ __align__(1024) unsigned char smem[];
     const int tid = threadIdx.x;
     const int b = P.cta_block[blockIdx.x];
     const DBlock &B = P.blocks[b];
     const int ph = P.states[b].phase;
+    double *red = reinterpret_cast<double *>(smem);       // reused after the tile
+    double *scratch = red + NQ * (NTHR / 32);
+    int *flag = reinterpret_cast<int *>(scratch + 256);
 
     if (serves<OPK>(ph)) {
         double acc[NQ] = {0.0, 0.0, 0.0, 0.0};
@@ -644,19 +654,19 @@ __global__ void __launch_bounds__(NT, 4) k_sweep(const KParams P) {
             C.map_b = nullptr;
             C.map_c = tm + TM_RO;
         }
-        sweep_tile<OPK>(C, blockIdx.x - B.cta_begin, smem, acc);
+        sweep_tile<OPK, BOX>(C, blockIdx.x - B.cta_begin, smem, acc);
+        __syncthreads();  // all planes consumed: the stage ring is free for reuse
         cta_sum(acc, red);
         if (tid == 0) {
 #pragma unroll
             for (int q = 0; q < NQ; ++q) P.partials[(size_t)q * P.nctas + blockIdx.x] = acc[q];
             __threadfence();
             const unsigned prev = atomicAdd(&P.blk_counter[b], 1u);
-            flag = (prev == (unsigned)(B.cta_end - B.cta_begin) - 1u);
+            *flag = (prev == (unsigned)(B.cta_end - B.cta_begin) - 1u);
         }
         __syncthreads();
-        if (flag) {  // last tile of block b: reduce and advance its recurrence
+        if (*flag) {  // last tile of block b: reduce and advance its recurrence
             __threadfence();
-            double *scratch = reinterpret_cast<double *>(smem);
             double q[NQ];
             const int nq = (OPK == OP_RESID) ? NQ : 1;
             for (int i = 0; i < NQ; ++i)
@@ -669,15 +679,16 @@ __global__ void __launch_bounds__(NT, 4) k_sweep(const KParams P) {
                 __threadfence();
             }
         }
+        __syncthreads();
     }
     // launch-wide completion
     if (tid == 0) {
         __threadfence();
         const unsigned prev = atomicAdd(P.launch_counter, 1u);
-        flag = (prev == (unsigned)P.nctas - 1u);
+        *flag = (prev == (unsigned)P.nctas - 1u);
     }
     __syncthreads();
-    if (!flag || tid != 0) return;
+    if (!*flag || tid != 0) return;
     __threadfence();
     int active = 0, verify = 0;
     for (int bb = 0; bb < P.nblocks; ++bb) {
@@ -712,10 +723,10 @@ __global__ void __launch_bounds__(NT, 4) k_sweep(const KParams P) {
 }
 
 // y = A_ii x on one block (standalone a1); x, y in the block's pitched layout.
-__global__ void __launch_bounds__(NT, 4) k_apply(const DBlock *__restrict__ blocks, int b,
-                                                 const __grid_constant__ CUtensorMap xmap, double *y) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    unsigned char *smem = aligned_smem(smem_raw);
+template <bool BOX>
+__global__ void __launch_bounds__(NTHR, 3) k_apply(const DBlock *__restrict__ blocks, int b,
+                                                   const __grid_constant__ CUtensorMap xmap, double *y) {
+    extern __shared__ __align__(1024) unsigned char smem[];
     const DBlock &B = blocks[b];
     SweepCtx C;
     C.B = &B;
@@ -727,7 +738,7 @@ __global__ void __launch_bounds__(NT, 4) k_apply(const DBlock *__restrict__ bloc
     C.pout = nullptr;
     C.yout = y;
     double acc[NQ] = {0.0, 0.0, 0.0, 0.0};
-    sweep_tile<OP_APPLY>(C, blockIdx.x, smem, acc);
+    sweep_tile<OP_APPLY, BOX>(C, blockIdx.x, smem, acc);
 }
 
 // Arm solves / residual sweeps.
@@ -860,6 +871,7 @@ static unsigned long long g_launches = 0;  // kernels launched by this library
 
 struct bs_ctx {
     int device = 0;
+    bool box = true;  // every block has overlap 0: compile-time box-region kernels
     int nblocks = 0;
     int nctas = 0;
     std::vector<DBlock> hblocks;
@@ -927,10 +939,18 @@ KParams make_params(bs_ctx *c, bool graph, cudaGraphConditionalHandle hl = 0,
 }
 
 template <int OPK>
+void *sweep_fn(bool box) {
+    return box ? (void *)k_sweep<OPK, true> : (void *)k_sweep<OPK, false>;
+}
+
+template <int OPK>
 void launch_sweep(bs_ctx *c, cudaStream_t st, int slot) {
     const KParams P = make_params(c, false);
     if (c->timing && slot >= 0) cudaEventRecord(c->ev[2 * slot], st);
-    k_sweep<OPK><<<c->nctas, NT, SMEM_BYTES, st>>>(P);
+    if (c->box)
+        k_sweep<OPK, true><<<c->nctas, NTHR, SMEM_BYTES, st>>>(P);
+    else
+        k_sweep<OPK, false><<<c->nctas, NTHR, SMEM_BYTES, st>>>(P);
     if (c->timing && slot >= 0) cudaEventRecord(c->ev[2 * slot + 1], st);
     ++g_launches;
 }
@@ -959,9 +979,9 @@ int add_sweep_node(bs_ctx *c, cudaGraph_t g, cudaGraphNode_t *node, const cudaGr
     KParams P = make_params(c, true, hl, hv);  // copied by the runtime at node creation
     void *args[] = {&P};
     cudaKernelNodeParams kp = {};
-    kp.func = (void *)k_sweep<OPK>;
+    kp.func = sweep_fn<OPK>(c->box);
     kp.gridDim = dim3(c->nctas);
-    kp.blockDim = dim3(NT);
+    kp.blockDim = dim3(NTHR);
     kp.sharedMemBytes = SMEM_BYTES;
     kp.kernelParams = args;
     BS_CU(cudaGraphAddKernelNode(node, g, deps, ndeps, &kp));
@@ -1053,6 +1073,7 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
         }
         B.pitch = (B.pdim[0] + PITCH_ALIGN - 1) / PITCH_ALIGN * PITCH_ALIGN;
         B.overlap = d.overlap;
+        if (d.overlap != 0) c->box = false;
         B.x = d.x;
         B.r = d.r;
         B.p[0] = d.p0;
@@ -1129,13 +1150,13 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
     if (e == cudaSuccess) e = cudaMemset(c->dlaunch_counter, 0, sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemset(c->dnactive, 0, sizeof(int));
     if (e == cudaSuccess) e = cudaMemset(c->dctl, 0, sizeof(Control));
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_sweep<OP_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_sweep<OP_S1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_sweep<OP_S2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    {
+        const void *fns[] = {sweep_fn<OP_RESID>(true), sweep_fn<OP_RESID>(false), sweep_fn<OP_S1>(true),
+                             sweep_fn<OP_S1>(false),   sweep_fn<OP_S2>(true),     sweep_fn<OP_S2>(false),
+                             (const void *)k_apply<true>, (const void *)k_apply<false>};
+        for (const void *f : fns)
+            if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    }
     if (e != cudaSuccess) {
         bs_ctx_destroy(c);
         return fail(BS_ECUDA, std::string("bs_ctx_create: ") + cudaGetErrorString(e));
@@ -1201,7 +1222,10 @@ int bs_stencil_apply(bs_ctx *c, int block, const double *x, double *y, void *str
     CUtensorMap xmap;
     if (int e = encode_map(&xmap, x, B, true)) return e;
     ++g_launches;
-    k_apply<<<B.cta_end - B.cta_begin, NT, SMEM_BYTES, (cudaStream_t)stream>>>(c->dblocks, block, xmap, y);
+    if (B.overlap == 0)
+        k_apply<true><<<B.cta_end - B.cta_begin, NTHR, SMEM_BYTES, (cudaStream_t)stream>>>(c->dblocks, block, xmap, y);
+    else
+        k_apply<false><<<B.cta_end - B.cta_begin, NTHR, SMEM_BYTES, (cudaStream_t)stream>>>(c->dblocks, block, xmap, y);
     BS_CU(cudaGetLastError());
     return BS_OK;
 }
