@@ -13,7 +13,7 @@ import os
 from .errors import ConfigurationError, DeviceError, ProtocolError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libbsgpu.so")
+LIB_PATH = os.environ.get("BS_LIB") or os.path.join(HERE, "_lib", "libbsgpu.so")
 
 NDIR = 6
 STOP_NAMES = {0: "none", 1: "tolerance_met", 2: "max_iterations", 3: "breakdown"}

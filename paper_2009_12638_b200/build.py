@@ -21,15 +21,16 @@ FLAGS = [
 ]
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(os.path.dirname(OUT), exist_ok=True)
+def build(verbose: bool = False, force: bool = False, out: str = OUT, defines=()) -> str:
+    os.makedirs(os.path.dirname(out), exist_ok=True)
     deps = SRC + [os.path.join(ROOT, "include", "blocksolve_b200.h"), __file__]
-    if not force and os.path.exists(OUT):
-        if os.path.getmtime(OUT) >= max(os.path.getmtime(d) for d in deps):
-            return OUT
-    cmd = [NVCC] + FLAGS + (["-Xptxas", "-v"] if verbose else []) + SRC + ["-o", OUT]
+    if not force and os.path.exists(out):
+        if os.path.getmtime(out) >= max(os.path.getmtime(d) for d in deps):
+            return out
+    cmd = ([NVCC] + FLAGS + ["-D" + d for d in defines] + (["-Xptxas", "-v"] if verbose else [])
+           + SRC + ["-o", out])
     subprocess.run(cmd, check=True)
-    return OUT
+    return out
 
 
 if __name__ == "__main__":

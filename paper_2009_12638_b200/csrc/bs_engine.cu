@@ -17,8 +17,9 @@
 //   * A CTA owns a TX x TY column tile and marches CZ planes in z.  One
 //     thread issues cp.async.bulk.tensor (TMA) loads of whole planes — the
 //     tile plus a one-cell x/y halo for the stencil inputs, the bare tile for
-//     epilogue operands — into an NSTAGE-deep shared-memory ring completed on
-//     mbarriers, NSTAGE-2 planes ahead of the plane being computed.  Cells
+//     epilogue operands — into an 8..12-deep shared-memory ring completed on
+//     mbarriers (a dedicated producer warp; consumers release stages through
+//     `empty` mbarriers, so there is no CTA-wide barrier per plane).  Cells
 //     outside the padded box are zero-filled by TMA (= absent neighbours).
 //   * The stencil input u is formed from the staged operands: u = r + beta*p
 //     in CG sweep 1 (p written once, never re-read), u = p in sweep 2,
@@ -71,13 +72,16 @@ constexpr int HY = TY + 2;
 constexpr int SX = TX + 4;
 constexpr int SC = SX * HY;            // staged haloed-box cells
 constexpr int NQ = 4;                  // partial sums per CTA
-constexpr int NSTAGE = 6;              // TMA ring depth
+#ifndef BS_NSTAGE_AB
+#define BS_NSTAGE_AB 8   // ring depth of sweeps staging two haloed operands
+#endif
+#ifndef BS_NSTAGE_A
+#define BS_NSTAGE_A 12   // ring depth of sweeps staging one haloed operand
+#endif
 constexpr int PITCH_ALIGN = 4;         // doubles
 
 constexpr int SEG_H = ((SC * 8 + 127) / 128) * 128;  // staged haloed box, 128B aligned
 constexpr int SEG_O = NT * 8;                         // bare tile
-constexpr int STAGE_BYTES = 2 * SEG_H + SEG_O;
-constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + 2 * NSTAGE * 8;
 
 enum Phase : int {
     PH_IDLE = 0,
@@ -90,6 +94,16 @@ enum Phase : int {
 };
 
 enum Op : int { OP_RESID = 0, OP_S1 = 1, OP_S2 = 2, OP_APPLY = 3 };
+
+// Stage layout per op: [A haloed][B haloed, if the op has one][C bare tile].
+// Fewer bytes per stage buys a deeper ring in about the same shared memory,
+// so every op keeps ~60 KB of loads in flight per CTA.
+__host__ __device__ constexpr bool op_has_b(int op) { return op == OP_RESID || op == OP_S1; }
+__host__ __device__ constexpr int op_stages(int op) { return op_has_b(op) ? BS_NSTAGE_AB : BS_NSTAGE_A; }
+__host__ __device__ constexpr int op_coff(int op) { return op_has_b(op) ? 2 * SEG_H : SEG_H; }
+__host__ __device__ constexpr int op_stage_bytes(int op) { return op_coff(op) + SEG_O; }
+__host__ __device__ constexpr int op_smem(int op) { return op_stages(op) * (op_stage_bytes(op) + 16); }
+constexpr int SMEM_MAX = op_smem(OP_S1) > op_smem(OP_S2) ? op_smem(OP_S1) : op_smem(OP_S2);
 
 // tensor maps per block
 enum Tm : int { TM_XH = 0, TM_P0H = 1, TM_P1H = 2, TM_RH = 3, TM_XO = 4, TM_RO = 5, TM_BO = 6, NTM = 7 };
@@ -333,7 +347,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 //
 // Warp roles: warps 0..TY-1 consume (lane = x, warp = y of the tile), warp TY
 // produces: its lane 0 streams plane q = 0..nplanes-1 (lz = lz0-1+q) into
-// stage q % NSTAGE with TMA, after every consumer warp released that stage's
+// stage q % NS with TMA, after every consumer warp released that stage's
 // previous plane (empty mbarrier, count TY).  Consumers never block on each
 // other — only on `full` — so there is no CTA-wide barrier per plane.
 //
@@ -357,13 +371,16 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
     const int lz1 = min(lz0 + cz, pdz);
     const int nplanes = lz1 - lz0 + 2;       // q = 0..nplanes-1 <-> lz = lz0-1+q
 
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + NSTAGE * STAGE_BYTES);
-    uint64_t *empty = full + NSTAGE;
+    constexpr int NS = op_stages(OP);
+    constexpr int STB = op_stage_bytes(OP);
+    constexpr int COFF = op_coff(OP);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + NS * STB);
+    uint64_t *empty = full + NS;
     const bool use_b = C.map_b != nullptr;
     const bool use_c = C.map_c != nullptr;
 
     if (tid == 0) {
-        for (int s = 0; s < NSTAGE; ++s) {
+        for (int s = 0; s < NS; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], TY);
         }
@@ -375,16 +392,16 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
     if (warp == TY) {  // ---------------- TMA producer warp
         if (lane == 0) {
             for (int q = 0; q < nplanes; ++q) {
-                const int s = q % NSTAGE;
-                if (q >= NSTAGE) mbar_wait(&empty[s], (uint32_t)((q / NSTAGE - 1) & 1));
+                const int s = q % NS;
+                if (q >= NS) mbar_wait(&empty[s], (uint32_t)((q / NS - 1) & 1));
                 const int lz = lz0 - 1 + q;
                 const bool epi = use_c && q >= 1 && q <= nplanes - 2;
-                unsigned char *st = smem + s * STAGE_BYTES;
+                unsigned char *st = smem + s * STB;
                 const uint32_t bytes = (uint32_t)(SC * 8) * (use_b ? 2u : 1u) + (epi ? (uint32_t)SEG_O : 0u);
                 mbar_expect_tx(&full[s], bytes);
                 tma_load3(st, C.map_a, lx0 - 2, ly0 - 1, lz, &full[s]);
                 if (use_b) tma_load3(st + SEG_H, C.map_b, lx0 - 2, ly0 - 1, lz, &full[s]);
-                if (epi) tma_load3(st + 2 * SEG_H, C.map_c, lx0, ly0, lz, &full[s]);
+                if (epi) tma_load3(st + COFF, C.map_c, lx0, ly0, lz, &full[s]);
             }
         }
         __syncwarp();
@@ -417,18 +434,18 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
 
     mbar_wait(&full[0], 0u);
     double u_prev = uval(smem, own, 0, 0, lz0 - 1);
-    mbar_wait(&full[1 % NSTAGE], 0u);
-    double u_cur = uval(smem + (1 % NSTAGE) * STAGE_BYTES, own, 0, 0, lz0);
+    mbar_wait(&full[1], 0u);
+    double u_cur = uval(smem + STB, own, 0, 0, lz0);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[0]);
 
     const bool px_box = lx > 0, py_box = ly > 0;
     for (int q = 1; q <= nplanes - 2; ++q) {
-        const int s = q % NSTAGE, sn = (q + 1) % NSTAGE;
+        const int s = q % NS, sn = (q + 1) % NS;
         const int lz = lz0 - 1 + q;
-        const unsigned char *st = smem + s * STAGE_BYTES;
-        mbar_wait(&full[sn], (uint32_t)(((q + 1) / NSTAGE) & 1));
-        const double u_next = uval(smem + sn * STAGE_BYTES, own, 0, 0, lz + 1);
+        const unsigned char *st = smem + s * STB;
+        mbar_wait(&full[sn], (uint32_t)(((q + 1) / NS) & 1));
+        const double u_next = uval(smem + sn * STB, own, 0, 0, lz + 1);
         const bool here = BOX ? col_in : (col_in && in_region(B, gi, gj, B.plo[2] + lz));
         if (here) {
             const double xm = uval(st, own - 1, -1, 0, lz), xp = uval(st, own + 1, 1, 0, lz);
@@ -445,7 +462,7 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
                 px = in_region(B, gi - 1, gj, gk);
             }
             const double au = stencil7(u_prev, ym, xm, u_cur, xp, yp, u_next, pz, py, px);
-            const double *cst = reinterpret_cast<const double *>(st + 2 * SEG_H);
+            const double *cst = reinterpret_cast<const double *>(st + COFF);
             if (OP == OP_APPLY) {
                 C.yout[sx] = au;
             } else if (OP == OP_S2) {
@@ -948,9 +965,9 @@ void launch_sweep(bs_ctx *c, cudaStream_t st, int slot) {
     const KParams P = make_params(c, false);
     if (c->timing && slot >= 0) cudaEventRecord(c->ev[2 * slot], st);
     if (c->box)
-        k_sweep<OPK, true><<<c->nctas, NTHR, SMEM_BYTES, st>>>(P);
+        k_sweep<OPK, true><<<c->nctas, NTHR, op_smem(OPK), st>>>(P);
     else
-        k_sweep<OPK, false><<<c->nctas, NTHR, SMEM_BYTES, st>>>(P);
+        k_sweep<OPK, false><<<c->nctas, NTHR, op_smem(OPK), st>>>(P);
     if (c->timing && slot >= 0) cudaEventRecord(c->ev[2 * slot + 1], st);
     ++g_launches;
 }
@@ -982,7 +999,7 @@ int add_sweep_node(bs_ctx *c, cudaGraph_t g, cudaGraphNode_t *node, const cudaGr
     kp.func = sweep_fn<OPK>(c->box);
     kp.gridDim = dim3(c->nctas);
     kp.blockDim = dim3(NTHR);
-    kp.sharedMemBytes = SMEM_BYTES;
+    kp.sharedMemBytes = op_smem(OPK);
     kp.kernelParams = args;
     BS_CU(cudaGraphAddKernelNode(node, g, deps, ndeps, &kp));
     return BS_OK;
@@ -1096,12 +1113,14 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
         B.tiles_y = (B.pdim[1] + TY - 1) / TY;
         int cz = z_chunk;
         if (cz <= 0) {
-            // enough CTAs for ~4 waves of 4 CTAs/SM, without chopping z into
-            // slivers (each chunk stages 2 extra planes)
+            // Long z-marches amortise the 2 re-staged planes and the pipeline
+            // ramp of every CTA; all tiles of a launch should be resident at
+            // once (3 CTAs/SM) or span several waves.  Full depth unless that
+            // leaves a deep block with only 1-3 ragged waves.
             const long long cols = (long long)B.tiles_x * B.tiles_y * nblocks;
-            const long long want = 148LL * 16;
-            const long long chunks = std::max<long long>(1, (want + cols - 1) / cols);
-            cz = (int)std::max<long long>(24, (B.pdim[2] + chunks - 1) / chunks);
+            const long long slots = 148LL * 3;
+            cz = B.pdim[2];
+            if (cols > slots && B.pdim[2] > 128) cz = 128;
         }
         B.cz = std::min(cz, B.pdim[2]);
         B.tiles_z = (B.pdim[2] + B.cz - 1) / B.cz;
@@ -1155,7 +1174,7 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
                              sweep_fn<OP_S1>(false),   sweep_fn<OP_S2>(true),     sweep_fn<OP_S2>(false),
                              (const void *)k_apply<true>, (const void *)k_apply<false>};
         for (const void *f : fns)
-            if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+            if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
     }
     if (e != cudaSuccess) {
         bs_ctx_destroy(c);
@@ -1223,9 +1242,9 @@ int bs_stencil_apply(bs_ctx *c, int block, const double *x, double *y, void *str
     if (int e = encode_map(&xmap, x, B, true)) return e;
     ++g_launches;
     if (B.overlap == 0)
-        k_apply<true><<<B.cta_end - B.cta_begin, NTHR, SMEM_BYTES, (cudaStream_t)stream>>>(c->dblocks, block, xmap, y);
+        k_apply<true><<<B.cta_end - B.cta_begin, NTHR, op_smem(OP_APPLY), (cudaStream_t)stream>>>(c->dblocks, block, xmap, y);
     else
-        k_apply<false><<<B.cta_end - B.cta_begin, NTHR, SMEM_BYTES, (cudaStream_t)stream>>>(c->dblocks, block, xmap, y);
+        k_apply<false><<<B.cta_end - B.cta_begin, NTHR, op_smem(OP_APPLY), (cudaStream_t)stream>>>(c->dblocks, block, xmap, y);
     BS_CU(cudaGetLastError());
     return BS_OK;
 }

@@ -10,6 +10,7 @@ the hand-written sm_100a kernels of ``csrc/bs_engine.cu``.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -129,6 +130,8 @@ class BlockEngine:
             d.history = bb.history.data_ptr()
             d.history_cap = cap
         self._descs = descs
+        if not z_chunk:
+            z_chunk = int(os.environ.get("BS_ZCHUNK", "0"))
         ctx = ctypes.c_void_p()
         with torch.cuda.device(self.device):
             _lib.check(self.lib.bs_ctx_create(self.device.index, len(owned), descs, int(z_chunk),
