@@ -114,6 +114,30 @@ int bs_stencil_apply(bs_ctx *ctx, int block, const double *x, double *y, void *s
 int bs_cg_begin(bs_ctx *ctx, int max_iterations, double tolerance, int basis,
                 const int32_t *active, void *stream);
 
+/* a3: restarted GMRES(m) workspace.  Per block: V = m Krylov vectors in the
+ * block's pitched layout, V[j] = V + j*vstride; W = the Arnoldi work vector.
+ * m <= 64.  (inner_solvers.py:149-251; V is fp64[(m+1) x n] there.) */
+typedef struct bs_gmres_desc {
+    double *V;
+    int64_t vstride;  /* elements between consecutive Krylov vectors */
+    double *W;
+} bs_gmres_desc;
+
+int bs_gmres_setup(bs_ctx *ctx, int m, const bs_gmres_desc *per_block);
+
+/* Arm restarted GMRES(m) on the active blocks (same rhs assembly and warm
+ * start as bs_cg_begin; stop rules of inner_solvers.py:153-243: happy
+ * breakdown, recurrence claim verified against the true residual, restart,
+ * stagnation -> breakdown). */
+int bs_gmres_begin(bs_ctx *ctx, int max_iterations, double tolerance, int basis,
+                   const int32_t *active, void *stream);
+
+/* Run armed GMRES solves: per restart cycle the host enqueues every Arnoldi
+ * step (v_j = w/||w||, w = A v_j fused with h_0j, j modified Gram-Schmidt
+ * passes, ||w|| + Givens), x += V y and the true residual, then polls one
+ * counter.  Finished blocks skip the remaining launches.  Blocking. */
+int bs_gmres_run(bs_ctx *ctx, int max_cycles, void *stream, int64_t *kernels_out);
+
 /* Run armed solves to completion with device-side stopping.  Default: one
  * CUDA-graph launch whose WHILE node iterates {CG sweep 1, CG sweep 2,
  * IF(any block verifying) residual sweep} until no block is active — no host

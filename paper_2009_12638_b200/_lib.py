@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BS_LIB") or os.path.join(HERE, "_lib", "libbsgpu.so")
 
 NDIR = 6
-STOP_NAMES = {0: "none", 1: "tolerance_met", 2: "max_iterations", 3: "breakdown"}
+STOP_NAMES = {0: "none", 1: "tolerance_met", 2: "max_iterations", 3: "breakdown", 4: "stalled"}
 BASIS = {"rhs": 0, "initial": 1}
 
 
@@ -35,6 +35,10 @@ class BlockDesc(ctypes.Structure):
         ("history", ctypes.c_void_p),
         ("history_cap", ctypes.c_int32),
     ]
+
+
+class GmresDesc(ctypes.Structure):
+    _fields_ = [("V", ctypes.c_void_p), ("vstride", ctypes.c_int64), ("W", ctypes.c_void_p)]
 
 
 class BlockReport(ctypes.Structure):
@@ -71,6 +75,9 @@ _SIGS = {
     "bs_halo_pack": ([_P, _I, _P, _P], _I),
     "bs_read_reports": ([_P, ctypes.POINTER(BlockReport), _P], _I),
     "bs_launch_count": ([], ctypes.c_ulonglong),
+    "bs_gmres_setup": ([_P, _I, ctypes.POINTER(GmresDesc)], _I),
+    "bs_gmres_begin": ([_P, _I, ctypes.c_double, _I, _P, _P], _I),
+    "bs_gmres_run": ([_P, _I, _P, ctypes.POINTER(ctypes.c_int64)], _I),
     "bs_timing": ([_P, _I, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_longlong)], _I),
 }
 

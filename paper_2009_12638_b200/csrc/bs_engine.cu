@@ -91,9 +91,25 @@ enum Phase : int {
     PH_VERIFY = 4,  // true-residual check on claimed convergence
     PH_DONE = 5,
     PH_RESID = 6,   // standalone residual sweep (outer residual / checks)
+    // restarted GMRES(m) (inner_solvers.py:149-243), one Arnoldi step j =
+    // NORM(j) -> SPMV(j) -> MGS(j, 1..j) -> FINAL(j); a cycle ends FORM -> G_RESID
+    PH_G_NORM = 7,    // v_j = w / ||w||   (v_0 = r / beta)
+    PH_G_SPMV = 8,    // w = A v_j ; h_0j = v_0 . w
+    PH_G_MGS = 9,     // w -= h_{i-1,j} v_{i-1} ; h_ij = v_i . w
+    PH_G_FINAL = 10,  // w -= h_jj v_j ; ||w|| ; Givens ; stop tests
+    PH_G_FORM = 11,   // x += V y
+    PH_G_RESID = 12,  // true residual of the formed iterate ; restart or stop
 };
 
-enum Op : int { OP_RESID = 0, OP_S1 = 1, OP_S2 = 2, OP_APPLY = 3 };
+enum Kind : int { KIND_CG = 0, KIND_GMRES = 1 };
+
+enum Op : int { OP_RESID = 0, OP_S1 = 1, OP_S2 = 2, OP_APPLY = 3, OP_GSPMV = 4 };
+
+// pointwise (non-stencil) GMRES passes
+enum Pk : int { PK_NORM = 0, PK_MGS = 1, PK_FINAL = 2, PK_FORM = 3 };
+
+constexpr int MAXM = 64;  // largest supported GMRES restart length
+enum GFlag : int { GF_NONE = 0, GF_HAPPY = 1, GF_CHECK = 2, GF_CYCLE = 3 };
 
 // Stage layout per op: [A haloed][B haloed, if the op has one][C bare tile].
 // Fewer bytes per stage buys a deeper ring in about the same shared memory,
@@ -123,12 +139,25 @@ struct DBlock {
     double *ghost[BS_NDIR];
     double *hist;
     int hist_cap;
+    double *V;          // GMRES basis: V[j] = V + j * vstride (pitched padded box)
+    long long vstride;
+    double *W;          // GMRES work vector w
 };
 
 struct DState {
     int phase, stop, it, first, pend, pcur, max_its, basis;
     double tol, tol_eff, scale, rel, rr, alpha, beta, alpha_pend;
     double q[NQ];
+    int kind, gj, gi, gflag, gm, gpad;
+    double cycle_start, gnrm;
+};
+
+// Small dense GMRES state of one block (inner_solvers.py:167-171).
+struct GState {
+    double H[(MAXM + 1) * MAXM];  // H[row * MAXM + col]
+    double cs[MAXM], sn[MAXM];
+    double g[MAXM + 1];
+    double y[MAXM + 1];
 };
 
 struct Control {
@@ -153,6 +182,9 @@ struct KParams {
     cudaGraphConditionalHandle h_loop;
     cudaGraphConditionalHandle h_verify;
     int use_graph;
+    GState *gstates;
+    const CUtensorMap *gmaps;  // per block: V[0..MAXM-1] haloed, [MAXM] = V[0] bare
+    int launch_j, launch_i;    // GMRES step served by this launch
 };
 
 // ------------------------------------------------------------------ geometry
@@ -285,12 +317,13 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-// Deterministic CTA reduction of NQ values over all NTHR threads; result
-// valid in thread 0.  `red` is NQ x (NTHR/32) doubles of shared memory.
+// Deterministic CTA reduction of NQ values over all NTH threads; result
+// valid in thread 0.  `red` holds NQ x (NTH/32) doubles of shared memory.
+template <int NTH>
 __device__ __forceinline__ void cta_sum(double (&acc)[NQ], double *red) {
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
-    constexpr int NW = NTHR / 32;
+    constexpr int NW = NTH / 32;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
         double v = warp_sum(acc[q]);
@@ -307,8 +340,9 @@ __device__ __forceinline__ void cta_sum(double (&acc)[NQ], double *red) {
     }
 }
 
-// Sum of partials[begin:end) with a fixed strided + tree order (whole CTA);
-// scratch holds 256 doubles.
+// Sum of partials[begin:end) with a fixed strided + tree order (whole CTA,
+// NTH >= 256 threads); scratch holds 256 doubles.
+template <int NTH>
 __device__ double range_sum(const double *part, int begin, int end, double *scratch) {
     const int tid = threadIdx.x;
     if (tid < 256) {
@@ -465,6 +499,10 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
             const double *cst = reinterpret_cast<const double *>(st + COFF);
             if (OP == OP_APPLY) {
                 C.yout[sx] = au;
+            } else if (OP == OP_GSPMV) {  // w = A v_j ; h_0j = v_0 . w (inner_solvers.py:187-190)
+                B.W[sx] = au;
+                const double v0 = first ? u_cur : cst[tid];
+                acc[0] = add(acc[0], mul(v0, au));
             } else if (OP == OP_S2) {
                 const double rnv = sub(cst[tid], mul(alpha, au));
                 B.r[sx] = rnv;
@@ -527,7 +565,144 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
 
 // ------------------------------------------------------------------ scalars
 
-__device__ void transition(const DBlock &B, DState &S, int ph, const double *q) {
+// ---- restarted GMRES(m) scalar recurrences (inner_solvers.py:149-251)
+
+__device__ void gmres_start_cycle(DState &S, GState &G, double beta, double rel) {
+    S.cycle_start = rel;  // inner_solvers.py:159
+    G.g[0] = beta;
+    S.gnrm = beta;        // v_0 = r / beta
+    S.gj = 0;
+    S.gi = 0;
+    S.gflag = GF_NONE;
+    S.phase = PH_G_NORM;
+}
+
+// y = H[:j+1,:j+1] \ g[:j+1] (inner_solvers.py:246-251)
+__device__ void gmres_back_substitute(GState &G, int j) {
+    for (int i = j; i >= 0; --i) {
+        double s = 0.0;
+        for (int k = i + 1; k <= j; ++k) s = add(s, mul(G.H[i * MAXM + k], G.y[k]));
+        G.y[i] = __ddiv_rn(sub(G.g[i], s), G.H[i * MAXM + i]);
+    }
+}
+
+__device__ __noinline__ void gmres_transition(const DBlock &B, DState &S, GState &G, int ph, const double *q) {
+    switch (ph) {
+        case PH_INIT: {  // inner_solvers.py:153-164
+            for (int i = 0; i < NQ; ++i) S.q[i] = q[i];
+            const double bn = sqrt(q[0]);
+            S.scale = bn > 0.0 ? bn : 1.0;
+            const double beta = sqrt(q[1]);
+            const double rel = beta / S.scale;
+            S.rel = rel;
+            S.tol_eff = S.basis == BS_BASIS_INITIAL ? S.tol * rel : S.tol;
+            S.it = 0;
+            if (rel <= S.tol_eff) {
+                S.stop = BS_STOP_TOLERANCE_MET;
+                S.phase = PH_DONE;
+            } else {
+                gmres_start_cycle(S, G, beta, rel);
+            }
+            break;
+        }
+        case PH_G_NORM:
+            S.phase = PH_G_SPMV;
+            break;
+        case PH_G_SPMV:
+            G.H[0 * MAXM + S.gj] = q[0];
+            if (S.gj >= 1) {
+                S.gi = 1;
+                S.phase = PH_G_MGS;
+            } else {
+                S.phase = PH_G_FINAL;
+            }
+            break;
+        case PH_G_MGS:
+            G.H[S.gi * MAXM + S.gj] = q[0];
+            if (S.gi < S.gj) S.gi += 1;
+            else S.phase = PH_G_FINAL;
+            break;
+        case PH_G_FINAL: {  // inner_solvers.py:194-236
+            const int j = S.gj;
+            const double wnorm = sqrt(q[0]);
+            G.H[(j + 1) * MAXM + j] = wnorm;
+            double cn = 0.0;
+            for (int r = 0; r <= j + 1; ++r) cn = add(cn, mul(G.H[r * MAXM + j], G.H[r * MAXM + j]));
+            const bool happy = wnorm <= 1e-14 * fmax(sqrt(cn), 1e-300);
+            for (int i = 0; i < j; ++i) {
+                const double hi = G.H[i * MAXM + j], hi1 = G.H[(i + 1) * MAXM + j];
+                const double hij = add(mul(G.cs[i], hi), mul(G.sn[i], hi1));
+                G.H[(i + 1) * MAXM + j] = add(mul(-G.sn[i], hi), mul(G.cs[i], hi1));
+                G.H[i * MAXM + j] = hij;
+            }
+            const double hjj = G.H[j * MAXM + j], hj1 = G.H[(j + 1) * MAXM + j];
+            const double denom = hypot(hjj, hj1);
+            G.cs[j] = __ddiv_rn(hjj, denom);
+            G.sn[j] = __ddiv_rn(hj1, denom);
+            G.H[j * MAXM + j] = denom;
+            G.H[(j + 1) * MAXM + j] = 0.0;
+            G.g[j + 1] = mul(-G.sn[j], G.g[j]);
+            G.g[j] = mul(G.cs[j], G.g[j]);
+            S.it += 1;
+            const double rel = fabs(G.g[j + 1]) / S.scale;
+            S.rel = rel;
+            if (S.it - 1 < B.hist_cap) B.hist[S.it - 1] = rel;
+            int flag = GF_NONE;
+            if (happy) flag = GF_HAPPY;
+            else if (rel <= S.tol_eff || S.it >= S.max_its) flag = GF_CHECK;
+            else if (j == S.gm - 1) flag = GF_CYCLE;
+            if (flag != GF_NONE) {
+                gmres_back_substitute(G, j);
+                S.gflag = flag;
+                S.phase = PH_G_FORM;
+            } else {
+                S.gnrm = wnorm;  // v_{j+1} = w / wnorm (inner_solvers.py:237)
+                S.gj = j + 1;
+                S.gi = 0;
+                S.phase = PH_G_NORM;
+            }
+            break;
+        }
+        case PH_G_FORM:
+            S.phase = PH_G_RESID;
+            break;
+        case PH_G_RESID: {  // inner_solvers.py:215-243
+            for (int i = 0; i < NQ; ++i) S.q[i] = q[i];
+            const double rel_true = sqrt(q[1]) / S.scale;
+            S.rel = rel_true;
+            if (S.gflag == GF_HAPPY) {
+                if (S.it - 1 < B.hist_cap) B.hist[S.it - 1] = rel_true;
+                S.stop = BS_STOP_TOLERANCE_MET;
+                S.phase = PH_DONE;
+                break;
+            }
+            if (S.gflag == GF_CHECK) {
+                if (rel_true <= S.tol_eff) {
+                    if (S.it - 1 < B.hist_cap) B.hist[S.it - 1] = rel_true;
+                    S.stop = BS_STOP_TOLERANCE_MET;
+                    S.phase = PH_DONE;
+                    break;
+                }
+                if (S.it >= S.max_its) {
+                    S.stop = BS_STOP_MAX_ITERATIONS;
+                    S.phase = PH_DONE;
+                    break;
+                }
+            }
+            if (!isfinite(rel_true) || S.cycle_start - rel_true < 1e-14 * S.cycle_start) {
+                S.stop = BS_STOP_BREAKDOWN;  // non-finite or stagnation over a cycle
+                S.phase = PH_DONE;
+                break;
+            }
+            gmres_start_cycle(S, G, sqrt(q[1]), rel_true);  // restart from r = b - A x
+            break;
+        }
+        default:
+            break;
+    }
+}
+
+__device__ __noinline__ void cg_transition(const DBlock &B, DState &S, int ph, const double *q) {
     switch (ph) {
         case PH_INIT: {
             for (int i = 0; i < NQ; ++i) S.q[i] = q[i];
@@ -619,61 +794,40 @@ __device__ void transition(const DBlock &B, DState &S, int ph, const double *q) 
     }
 }
 
-template <int OPK>
-__device__ __forceinline__ bool serves(int ph) {
-    if (OPK == OP_S1) return ph == PH_S1;
-    if (OPK == OP_S2) return ph == PH_S2;
-    return ph == PH_INIT || ph == PH_VERIFY || ph == PH_RESID;
+__device__ void transition(const DBlock &B, DState &S, GState *G, int ph, const double *q) {
+    const bool gm = ph >= PH_G_NORM || (ph == PH_INIT && S.kind == KIND_GMRES);
+    if (gm) gmres_transition(B, S, *G, ph, q);
+    else cg_transition(B, S, ph, q);
 }
 
-// One sweep over every block whose phase this kernel serves.  The last CTA of
-// each served block reduces its partials and advances its phase machine; the
-// last CTA of the launch publishes the loop conditions.
-// One sweep over every block whose phase this kernel serves.  The last CTA of
-// each served block reduces its partials and advances its phase machine; the
-// last CTA of the launch publishes the loop conditions.
-template <int OPK, bool BOX>
-__global__ void __launch_bounds__(NTHR, 3) k_sweep(const KParams P) {
-    extern __shared__ __align__(1024) unsigned char smem[];
-    const int tid = threadIdx.x;
-    const int b = P.cta_block[blockIdx.x];
-    const DBlock &B = P.blocks[b];
-    const int ph = P.states[b].phase;
-    double *red = reinterpret_cast<double *>(smem);       // reused after the tile
-    double *scratch = red + NQ * (NTHR / 32);
-    int *flag = reinterpret_cast<int *>(scratch + 256);
+// Does a launch of sweep op OPK (or pointwise pass PK when OPK < 0) serve this block?
+template <int OPK, int PKK>
+__device__ __forceinline__ bool serves(const DState &S, const KParams &P) {
+    const int ph = S.phase;
+    if (OPK == OP_S1) return ph == PH_S1;
+    if (OPK == OP_S2) return ph == PH_S2;
+    if (OPK == OP_RESID) return ph == PH_INIT || ph == PH_VERIFY || ph == PH_RESID || ph == PH_G_RESID;
+    if (OPK == OP_GSPMV) return ph == PH_G_SPMV && S.gj == P.launch_j;
+    if (PKK == PK_NORM) return ph == PH_G_NORM && S.gj == P.launch_j;
+    if (PKK == PK_MGS) return ph == PH_G_MGS && S.gj == P.launch_j && S.gi == P.launch_i;
+    if (PKK == PK_FINAL) return ph == PH_G_FINAL && S.gj == P.launch_j;
+    if (PKK == PK_FORM) return ph == PH_G_FORM;
+    return false;
+}
 
-    if (serves<OPK>(ph)) {
-        double acc[NQ] = {0.0, 0.0, 0.0, 0.0};
-        const DState S = P.states[b];
-        const CUtensorMap *tm = P.tmaps + (size_t)b * NTM;
-        SweepCtx C;
-        C.B = &B;
-        C.pend = S.pend != 0;
-        C.first = S.first != 0;
-        C.want_global = true;
-        C.alpha_pend = S.alpha_pend;
-        C.alpha = S.alpha;
-        C.beta = S.beta;
-        C.yout = nullptr;
-        C.pout = B.p[S.pcur ^ 1];
-        const CUtensorMap *tm_p = tm + (S.pcur ? TM_P1H : TM_P0H);
-        if (OPK == OP_RESID) {
-            C.map_a = tm + TM_XH;
-            C.map_b = C.pend ? tm_p : nullptr;
-            C.map_c = tm + TM_BO;
-        } else if (OPK == OP_S1) {
-            C.map_a = tm + TM_RH;
-            C.map_b = (!C.first || C.pend) ? tm_p : nullptr;
-            C.map_c = C.pend ? tm + TM_XO : nullptr;
-        } else {
-            C.map_a = tm_p;
-            C.map_b = nullptr;
-            C.map_c = tm + TM_RO;
-        }
-        sweep_tile<OPK, BOX>(C, blockIdx.x - B.cta_begin, smem, acc);
-        __syncthreads();  // all planes consumed: the stage ring is free for reuse
-        cta_sum(acc, red);
+// Per-tile partials -> the block's last CTA reduces them in tile order and
+// advances the block's recurrence.  Every CTA then counts into the launch;
+// the launch's last CTA publishes the loop conditions.  NTH = CTA threads.
+template <int NTH, int OPK>
+__device__ void finish(const KParams &P, int b, int ph, bool served, double (&acc)[NQ], int nq,
+                       unsigned char *smem) {
+    const int tid = threadIdx.x;
+    double *red = reinterpret_cast<double *>(smem);
+    double *scratch = red + NQ * (NTH / 32);
+    int *flag = reinterpret_cast<int *>(scratch + 256);
+    if (served) {
+        const DBlock &B = P.blocks[b];
+        cta_sum<NTH>(acc, red);
         if (tid == 0) {
 #pragma unroll
             for (int q = 0; q < NQ; ++q) P.partials[(size_t)q * P.nctas + blockIdx.x] = acc[q];
@@ -682,15 +836,15 @@ __global__ void __launch_bounds__(NTHR, 3) k_sweep(const KParams P) {
             *flag = (prev == (unsigned)(B.cta_end - B.cta_begin) - 1u);
         }
         __syncthreads();
-        if (*flag) {  // last tile of block b: reduce and advance its recurrence
+        if (*flag) {  // last tile of block b
             __threadfence();
             double q[NQ];
-            const int nq = (OPK == OP_RESID) ? NQ : 1;
             for (int i = 0; i < NQ; ++i)
-                q[i] = i < nq ? range_sum(P.partials + (size_t)i * P.nctas, B.cta_begin, B.cta_end, scratch) : 0.0;
+                q[i] = i < nq ? range_sum<NTH>(P.partials + (size_t)i * P.nctas, B.cta_begin, B.cta_end, scratch)
+                              : 0.0;
             if (tid == 0) {
                 DState Sn = P.states[b];
-                transition(B, Sn, ph, q);
+                transition(B, Sn, P.gstates ? P.gstates + b : nullptr, ph, q);
                 P.states[b] = Sn;
                 P.blk_counter[b] = 0u;
                 __threadfence();
@@ -698,7 +852,6 @@ __global__ void __launch_bounds__(NTHR, 3) k_sweep(const KParams P) {
         }
         __syncthreads();
     }
-    // launch-wide completion
     if (tid == 0) {
         __threadfence();
         const unsigned prev = atomicAdd(P.launch_counter, 1u);
@@ -739,6 +892,128 @@ __global__ void __launch_bounds__(NTHR, 3) k_sweep(const KParams P) {
     }
 }
 
+// One sweep over every block whose phase this kernel serves.
+template <int OPK, bool BOX>
+__global__ void __launch_bounds__(NTHR, 3) k_sweep(const KParams P) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int b = P.cta_block[blockIdx.x];
+    const DBlock &B = P.blocks[b];
+    const DState S = P.states[b];
+    const int ph = S.phase;
+    const bool served = serves<OPK, -1>(S, P);
+    double acc[NQ] = {0.0, 0.0, 0.0, 0.0};
+    if (served) {
+        const CUtensorMap *tm = P.tmaps + (size_t)b * NTM;
+        SweepCtx C;
+        C.B = &B;
+        C.pend = S.pend != 0;
+        C.first = S.first != 0;
+        C.want_global = true;
+        C.alpha_pend = S.alpha_pend;
+        C.alpha = S.alpha;
+        C.beta = S.beta;
+        C.yout = nullptr;
+        C.pout = B.p[S.pcur ^ 1];
+        const CUtensorMap *tm_p = tm + (S.pcur ? TM_P1H : TM_P0H);
+        if (OPK == OP_RESID) {
+            C.map_a = tm + TM_XH;
+            C.map_b = C.pend ? tm_p : nullptr;
+            C.map_c = tm + TM_BO;
+        } else if (OPK == OP_S1) {
+            C.map_a = tm + TM_RH;
+            C.map_b = (!C.first || C.pend) ? tm_p : nullptr;
+            C.map_c = C.pend ? tm + TM_XO : nullptr;
+        } else if (OPK == OP_S2) {
+            C.map_a = tm_p;
+            C.map_b = nullptr;
+            C.map_c = tm + TM_RO;
+        } else {  // OP_GSPMV: u = v_j (haloed), epilogue operand v_0 (bare)
+            const CUtensorMap *gm = P.gmaps + (size_t)b * (MAXM + 1);
+            C.first = S.gj == 0;
+            C.map_a = gm + S.gj;
+            C.map_b = nullptr;
+            C.map_c = C.first ? nullptr : gm + MAXM;
+        }
+        sweep_tile<OPK, BOX>(C, blockIdx.x - B.cta_begin, smem, acc);
+        __syncthreads();  // all planes consumed: the stage ring is free for reuse
+    }
+    finish<NTHR, OPK>(P, b, ph, served, acc, OPK == OP_RESID ? NQ : 1, smem);
+}
+
+// Pointwise GMRES passes over a block's region, tile by tile (same CTA table
+// and deterministic reduction order as the sweeps).
+template <int PKK, bool BOX>
+__global__ void __launch_bounds__(NT) k_point(const KParams P) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int b = P.cta_block[blockIdx.x];
+    const DBlock &B = P.blocks[b];
+    const DState S = P.states[b];
+    const int ph = S.phase;
+    const bool served = serves<-1, PKK>(S, P);
+    double acc[NQ] = {0.0, 0.0, 0.0, 0.0};
+    if (served) {
+        const GState &G = P.gstates[b];
+        const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
+        int t = blockIdx.x - B.cta_begin;
+        const int ix = t % B.tiles_x;
+        t /= B.tiles_x;
+        const int iy = t % B.tiles_y;
+        const int iz = t / B.tiles_y;
+        const int lx = ix * TX + tx, ly = iy * TY + ty;
+        const int lz0 = iz * B.cz, lz1 = min(lz0 + B.cz, B.pdim[2]);
+        const bool col_in = lx < B.pdim[0] && ly < B.pdim[1];
+        const int gi = B.plo[0] + lx, gj = B.plo[1] + ly;
+        const long long plane = (long long)B.pitch * B.pdim[1];
+        long long sx = (long long)lx + (long long)B.pitch * ((long long)ly + (long long)B.pdim[1] * lz0);
+        const int j = S.gj, i = S.gi;
+        const long long vs = B.vstride;
+        double *W = B.W;
+        const double *V = B.V;
+        if (col_in) {
+            if (PKK == PK_NORM) {  // v_j = src / nrm (inner_solvers.py:164, 237)
+                const double *src = j == 0 ? B.r : W;
+                double *vj = B.V + j * vs;
+                const double nrm = S.gnrm;
+                for (int lz = lz0; lz < lz1; ++lz, sx += plane)
+                    if (BOX || in_region(B, gi, gj, B.plo[2] + lz)) vj[sx] = __ddiv_rn(src[sx], nrm);
+            } else if (PKK == PK_MGS) {  // w -= h_{i-1,j} v_{i-1} ; h_ij = v_i . w (189-193)
+                const double h = G.H[(i - 1) * MAXM + j];
+                const double *va = V + (i - 1) * vs, *vb = V + i * vs;
+#pragma unroll 4
+                for (int lz = lz0; lz < lz1; ++lz) {
+                    const long long q = sx + (long long)(lz - lz0) * plane;
+                    if (BOX || in_region(B, gi, gj, B.plo[2] + lz)) {
+                        const double w = sub(W[q], mul(h, va[q]));
+                        W[q] = w;
+                        acc[0] = add(acc[0], mul(vb[q], w));
+                    }
+                }
+            } else if (PKK == PK_FINAL) {  // w -= h_jj v_j ; ||w||^2 (193-195)
+                const double h = G.H[j * MAXM + j];
+                const double *vj = V + j * vs;
+#pragma unroll 4
+                for (int lz = lz0; lz < lz1; ++lz) {
+                    const long long q = sx + (long long)(lz - lz0) * plane;
+                    if (BOX || in_region(B, gi, gj, B.plo[2] + lz)) {
+                        const double w = sub(W[q], mul(h, vj[q]));
+                        W[q] = w;
+                        acc[0] = add(acc[0], mul(w, w));
+                    }
+                }
+            } else {  // PK_FORM: x = x + V[:j+1]^T y (inner_solvers.py:173-175)
+                for (int lz = lz0; lz < lz1; ++lz, sx += plane) {
+                    if (BOX || in_region(B, gi, gj, B.plo[2] + lz)) {
+                        double acc_t = mul(V[sx], G.y[0]);
+                        for (int k = 1; k <= j; ++k) acc_t = add(acc_t, mul(V[k * vs + sx], G.y[k]));
+                        B.x[sx] = add(B.x[sx], acc_t);
+                    }
+                }
+            }
+        }
+    }
+    finish<NT, -1>(P, b, ph, served, acc, 1, smem);
+}
+
 // y = A_ii x on one block (standalone a1); x, y in the block's pitched layout.
 template <bool BOX>
 __global__ void __launch_bounds__(NTHR, 3) k_apply(const DBlock *__restrict__ blocks, int b,
@@ -760,7 +1035,7 @@ __global__ void __launch_bounds__(NTHR, 3) k_apply(const DBlock *__restrict__ bl
 
 // Arm solves / residual sweeps.
 __global__ void k_arm(DState *states, const int *active, int nblocks, int phase, int max_its, double tol,
-                      int basis) {
+                      int basis, int kind, int gm) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= nblocks) return;
     if (active && !active[b]) return;
@@ -773,6 +1048,8 @@ __global__ void k_arm(DState *states, const int *active, int nblocks, int phase,
         S.max_its = max_its;
         S.tol = tol;
         S.basis = basis;
+        S.kind = kind;
+        S.gm = gm;
     }
 }
 
@@ -907,6 +1184,10 @@ struct bs_ctx {
     int *hpinned = nullptr;  // [0]: n_active, [1..]: active mask staging
     DState *hstates = nullptr;
     Control *hctl = nullptr;
+    // GMRES(m) workspace (bs_gmres_setup)
+    int gm = 0;
+    GState *dgstates = nullptr;
+    CUtensorMap *dgmaps = nullptr;
     // device-side solve loop: RESID ; WHILE(any active) { S1 ; S2 ; IF(any verify) RESID }
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t graph_exec = nullptr;
@@ -952,7 +1233,34 @@ KParams make_params(bs_ctx *c, bool graph, cudaGraphConditionalHandle hl = 0,
     P.h_loop = hl;
     P.h_verify = hv;
     P.use_graph = graph ? 1 : 0;
+    P.gstates = c->dgstates;
+    P.gmaps = c->dgmaps;
+    P.launch_j = 0;
+    P.launch_i = 0;
     return P;
+}
+
+template <int PKK>
+void launch_point(bs_ctx *c, cudaStream_t st, int j, int i) {
+    KParams P = make_params(c, false);
+    P.launch_j = j;
+    P.launch_i = i;
+    constexpr int smem = (NQ * (NT / 32) + 256 + 8) * 8;
+    if (c->box)
+        k_point<PKK, true><<<c->nctas, NT, smem, st>>>(P);
+    else
+        k_point<PKK, false><<<c->nctas, NT, smem, st>>>(P);
+    ++g_launches;
+}
+
+void launch_gspmv(bs_ctx *c, cudaStream_t st, int j) {
+    KParams P = make_params(c, false);
+    P.launch_j = j;
+    if (c->box)
+        k_sweep<OP_GSPMV, true><<<c->nctas, NTHR, op_smem(OP_GSPMV), st>>>(P);
+    else
+        k_sweep<OP_GSPMV, false><<<c->nctas, NTHR, op_smem(OP_GSPMV), st>>>(P);
+    ++g_launches;
 }
 
 template <int OPK>
@@ -1170,9 +1478,10 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
     if (e == cudaSuccess) e = cudaMemset(c->dnactive, 0, sizeof(int));
     if (e == cudaSuccess) e = cudaMemset(c->dctl, 0, sizeof(Control));
     {
-        const void *fns[] = {sweep_fn<OP_RESID>(true), sweep_fn<OP_RESID>(false), sweep_fn<OP_S1>(true),
-                             sweep_fn<OP_S1>(false),   sweep_fn<OP_S2>(true),     sweep_fn<OP_S2>(false),
-                             (const void *)k_apply<true>, (const void *)k_apply<false>};
+        const void *fns[] = {sweep_fn<OP_RESID>(true),    sweep_fn<OP_RESID>(false), sweep_fn<OP_S1>(true),
+                             sweep_fn<OP_S1>(false),      sweep_fn<OP_S2>(true),     sweep_fn<OP_S2>(false),
+                             sweep_fn<OP_GSPMV>(true),    sweep_fn<OP_GSPMV>(false), (const void *)k_apply<true>,
+                             (const void *)k_apply<false>};
         for (const void *f : fns)
             if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
     }
@@ -1200,6 +1509,8 @@ int bs_ctx_destroy(bs_ctx *c) {
     cudaFree(c->dctl);
     cudaFree(c->dactive);
     cudaFree(c->dplan);
+    cudaFree(c->dgstates);
+    cudaFree(c->dgmaps);
     for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
     if (c->hpinned) cudaFreeHost(c->hpinned);
     if (c->hstates) cudaFreeHost(c->hstates);
@@ -1261,7 +1572,7 @@ int bs_cg_begin(bs_ctx *c, int max_iterations, double tolerance, int basis, cons
     if (int e = upload_active(c, active, st, &dact)) return e;
     ++g_launches;
     k_arm<<<(c->nblocks + 127) / 128, 128, 0, st>>>(c->dstates, dact, c->nblocks, PH_INIT, max_iterations,
-                                                   tolerance, basis);
+                                                   tolerance, basis, KIND_CG, 0);
     BS_CU(cudaGetLastError());
     return BS_OK;
 }
@@ -1281,7 +1592,7 @@ int bs_cancel(bs_ctx *c, const int32_t *active, void *stream) {
     const int *dact = nullptr;
     if (int e = upload_active(c, active, st, &dact)) return e;
     ++g_launches;
-    k_arm<<<(c->nblocks + 127) / 128, 128, 0, st>>>(c->dstates, dact, c->nblocks, PH_DONE, 0, 0.0, 0);
+    k_arm<<<(c->nblocks + 127) / 128, 128, 0, st>>>(c->dstates, dact, c->nblocks, PH_DONE, 0, 0.0, 0, 0, 0);
     BS_CU(cudaGetLastError());
     return BS_OK;
 }
@@ -1293,7 +1604,7 @@ int bs_residual(bs_ctx *c, const int32_t *active, void *stream) {
     const int *dact = nullptr;
     if (int e = upload_active(c, active, st, &dact)) return e;
     ++g_launches;
-    k_arm<<<(c->nblocks + 127) / 128, 128, 0, st>>>(c->dstates, dact, c->nblocks, PH_RESID, 0, 0.0, 0);
+    k_arm<<<(c->nblocks + 127) / 128, 128, 0, st>>>(c->dstates, dact, c->nblocks, PH_RESID, 0, 0.0, 0, 0, 0);
     launch_sweep<OP_RESID>(c, st, -1);
     BS_CU(cudaGetLastError());
     return BS_OK;
@@ -1342,6 +1653,83 @@ int bs_run(bs_ctx *c, int batch, int max_launches, void *stream, int64_t *sweeps
         }
     }
     if (sweeps_out) *sweeps_out = launched;
+    return BS_OK;
+}
+
+int bs_gmres_setup(bs_ctx *c, int m, const bs_gmres_desc *descs) {
+    if (!c || !descs) return fail(BS_EINVAL, "bs_gmres_setup: bad arguments");
+    if (m < 1 || m > MAXM) return fail(BS_EINVAL, "restart: GMRES restart must be in 1.." + std::to_string(MAXM));
+    if (int e = set_dev(c)) return e;
+    std::vector<CUtensorMap> maps((size_t)c->nblocks * (MAXM + 1));
+    for (int b = 0; b < c->nblocks; ++b) {
+        DBlock &B = c->hblocks[b];
+        const bs_gmres_desc &d = descs[b];
+        if (!d.V || !d.W) return fail(BS_EINVAL, "bs_gmres_setup: null V or W");
+        const long long n = (long long)B.pitch * B.pdim[1] * B.pdim[2];
+        if (d.vstride < n || (d.vstride * 8) % 16) return fail(BS_EINVAL, "bs_gmres_setup: bad V stride");
+        B.V = d.V;
+        B.vstride = d.vstride;
+        B.W = d.W;
+        for (int j = 0; j < m; ++j)
+            if (int e = encode_map(&maps[(size_t)b * (MAXM + 1) + j], B.V + (size_t)j * d.vstride, B, true)) return e;
+        if (int e = encode_map(&maps[(size_t)b * (MAXM + 1) + MAXM], B.V, B, false)) return e;
+    }
+    cudaFree(c->dgmaps);
+    c->dgmaps = nullptr;
+    if (!c->dgstates) BS_CU(cudaMalloc(&c->dgstates, sizeof(GState) * c->nblocks));
+    BS_CU(cudaMalloc(&c->dgmaps, sizeof(CUtensorMap) * maps.size()));
+    BS_CU(cudaMemcpy(c->dgmaps, maps.data(), sizeof(CUtensorMap) * maps.size(), cudaMemcpyHostToDevice));
+    BS_CU(cudaMemcpy(c->dblocks, c->hblocks.data(), sizeof(DBlock) * c->nblocks, cudaMemcpyHostToDevice));
+    c->gm = m;
+    return BS_OK;
+}
+
+int bs_gmres_begin(bs_ctx *c, int max_iterations, double tolerance, int basis, const int32_t *active,
+                   void *stream) {
+    if (!c) return fail(BS_EINVAL, "bs_gmres_begin: null context");
+    if (!c->gm) return fail(BS_ESTATE, "bs_gmres_begin: call bs_gmres_setup first");
+    if (max_iterations < 1) return fail(BS_EINVAL, "max_iterations must be at least 1");
+    if (!(tolerance >= 0.0)) return fail(BS_EINVAL, "tolerance must be non-negative");
+    if (basis != BS_BASIS_RHS && basis != BS_BASIS_INITIAL) return fail(BS_EINVAL, "unknown tolerance basis");
+    if (int e = set_dev(c)) return e;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int *dact = nullptr;
+    if (int e = upload_active(c, active, st, &dact)) return e;
+    ++g_launches;
+    k_arm<<<(c->nblocks + 127) / 128, 128, 0, st>>>(c->dstates, dact, c->nblocks, PH_INIT, max_iterations,
+                                                   tolerance, basis, KIND_GMRES, c->gm);
+    BS_CU(cudaGetLastError());
+    return BS_OK;
+}
+
+int bs_gmres_run(bs_ctx *c, int max_cycles, void *stream, int64_t *kernels_out) {
+    if (!c) return fail(BS_EINVAL, "bs_gmres_run: null context");
+    if (!c->gm) return fail(BS_ESTATE, "bs_gmres_run: call bs_gmres_setup first");
+    if (int e = set_dev(c)) return e;
+    cudaStream_t st = (cudaStream_t)stream;
+    const unsigned long long l0 = g_launches;
+    launch_sweep<OP_RESID>(c, st, -1);  // INIT: rhs assembly + r0 (inner_solvers.py:153-159)
+    int cycles = 0;
+    for (;;) {
+        for (int j = 0; j < c->gm; ++j) {  // one Arnoldi step per j; finished blocks skip
+            launch_point<PK_NORM>(c, st, j, 0);
+            launch_gspmv(c, st, j);
+            for (int i = 1; i <= j; ++i) launch_point<PK_MGS>(c, st, j, i);
+            launch_point<PK_FINAL>(c, st, j, 0);
+        }
+        launch_point<PK_FORM>(c, st, 0, 0);
+        launch_sweep<OP_RESID>(c, st, -1);  // true residual -> stop or restart
+        BS_CU(cudaGetLastError());
+        BS_CU(cudaMemcpyAsync(c->hpinned, c->dnactive, sizeof(int), cudaMemcpyDeviceToHost, st));
+        BS_CU(cudaStreamSynchronize(st));
+        ++cycles;
+        if (c->hpinned[0] == 0) break;
+        if (max_cycles > 0 && cycles >= max_cycles) {
+            if (kernels_out) *kernels_out = (int64_t)(g_launches - l0);
+            return fail(BS_ESTATE, "bs_gmres_run: solves still active after max_cycles restart cycles");
+        }
+    }
+    if (kernels_out) *kernels_out = (int64_t)(g_launches - l0);
     return BS_OK;
 }
 

@@ -219,6 +219,34 @@ class BlockEngine:
     def flush(self) -> None:
         _lib.check(self.lib.bs_flush(self.ctx, self.stream))
 
+    # -- GMRES(m) workspace ----------------------------------------------
+    def gmres_setup(self, m: int) -> None:
+        """Allocate m Krylov vectors + the work vector per block (idempotent)."""
+        if getattr(self, "_gm", 0) == m:
+            return
+        descs = (_lib.GmresDesc * self.nblocks)()
+        self._gbufs = []
+        for i, bb in enumerate(self.blocks):
+            n = bb.x.numel()
+            V = torch.zeros(m, n, dtype=torch.float64, device=self.device)
+            W = torch.zeros(n, dtype=torch.float64, device=self.device)
+            self._gbufs.append((V, W))
+            descs[i].V = V.data_ptr()
+            descs[i].vstride = n
+            descs[i].W = W.data_ptr()
+        _lib.check(self.lib.bs_gmres_setup(self.ctx, int(m), descs))
+        self._gm = m
+
+    def gmres_begin(self, max_iterations: int, tolerance: float, basis: str = "rhs", active=None) -> None:
+        m = self._mask(active)
+        _lib.check(self.lib.bs_gmres_begin(self.ctx, int(max_iterations), float(tolerance),
+                                           _lib.BASIS[basis], m[0] if m else None, self.stream))
+
+    def gmres_run(self, max_cycles: int = 0) -> int:
+        n = ctypes.c_int64(0)
+        _lib.check(self.lib.bs_gmres_run(self.ctx, int(max_cycles), self.stream, ctypes.byref(n)))
+        return n.value
+
     def halo_pack(self, plan: np.ndarray) -> None:
         plan = np.ascontiguousarray(plan, dtype=np.int32)
         if plan.size == 0:

@@ -114,9 +114,43 @@ def cg_solve(a: StencilOperator, b, x0, spec: InnerSolverSpec, tolerance_basis: 
     return x, report
 
 
-def gmres_solve(a: StencilOperator, b, x0, spec: InnerSolverSpec, tolerance_basis: str = "rhs"):
-    """Restarted GMRES(m) (inner_solvers.py:149-243) — device path pending."""
-    raise ConfigurationError("inner: gmres is not available on the device engine yet")
+def gmres_solve(a: StencilOperator, b, x0, spec: InnerSolverSpec, tolerance_basis: str = "rhs",
+                out=None):
+    """Restarted GMRES(m) with MGS Arnoldi and Givens rotations on the GPU
+    (inner_solvers.py:149-243): restart = min(spec.restart or 30, n); happy
+    breakdown returns the exact iterate; a claimed convergence is verified
+    against the true residual; a restart cycle without progress reports
+    ``breakdown`` (stagnation)."""
+    _check_basis(tolerance_basis)
+    n = a.num_rows
+    restart = min(spec.restart if spec.restart is not None else DEFAULT_RESTART, n)
+    is_tensor = torch is not None and isinstance(b, torch.Tensor)
+    on_device = is_tensor and b.is_cuda
+    eng = single_block_engine(a, b.device if on_device else None, history_cap=spec.max_iterations)
+    bd, host = as_device_vector(b, n, eng.device)
+    xd, _ = as_device_vector(x0, n, eng.device)
+    bb = eng.blocks[0]
+    max_cycles = spec.max_iterations + 2  # every cycle consumes >= 1 iteration
+    with torch.cuda.device(eng.device):
+        eng.gmres_setup(restart)
+        bb.put("b", bd)
+        bb.put("x", xd)
+        eng.gmres_begin(spec.max_iterations, spec.tolerance, tolerance_basis)
+        eng.gmres_run(max_cycles=max_cycles)
+        rep = eng.reports()[0]
+        its = int(rep.iterations_used)
+        hist = bb.history[:its].tolist() if its else []
+        x = bb.take("x")
+    report = InnerSolveReport(its, float(rep.final_relative_residual), STOP_NAMES[int(rep.stop_reason)],
+                              hist)
+    if host:
+        return x.cpu().numpy(), report
+    if out is not None:
+        out.copy_(x)
+        return out, report
+    if is_tensor and not on_device:
+        return x.cpu(), report
+    return x, report
 
 
 def solve(a: StencilOperator, b, x0, spec: InnerSolverSpec, tolerance_basis: str = "rhs"):

@@ -205,8 +205,9 @@ def check_termination(estimate: float, tol: float, completed: int, max_outer: in
 def _validate_device_path(config: OuterConfig) -> None:
     if config.mode != "sync":
         raise ConfigurationError("mode: the device engine runs 'sync' (async pending)")
-    if config.inner.kind != "cg":
-        raise ConfigurationError(f"inner: {config.inner.kind!r} not yet on the device engine (cg)")
+    if config.inner.kind not in ("cg", "gmres"):
+        raise ConfigurationError(
+            f"inner: {config.inner.kind!r} is outside the accelerated path (device kinds: cg, gmres)")
     if config.overlap != 0:
         raise ConfigurationError("overlap: the device engine supports overlap 0 (pending)")
     if config.delay.kind != "none":
@@ -253,11 +254,27 @@ def outer_solve(problem: LinearProblem, config: OuterConfig) -> SolveResult:
         eng.load_global("b", b_dev)
         plan = box_halo_plan(decomp.owned, decomp.block_grid)
 
-        def arm():
-            eng.cg_begin(spec.max_iterations, spec.tolerance, config.tolerance_basis)
+        if spec.kind == "gmres":
+            # _make_inner_solver (multisplit.py:532-536): one cycle of the configured
+            # length unless a restart is given; gmres_solve caps it at n (162)
+            restart = spec.restart if spec.restart is not None else spec.max_iterations
+            restart = min(restart, min(bb.padded.size for bb in eng.blocks))
+            eng.gmres_setup(restart)
+
+            def arm():
+                eng.gmres_begin(spec.max_iterations, spec.tolerance, config.tolerance_basis)
+
+            def solve():
+                eng.gmres_run(max_cycles=spec.max_iterations + 2)
+        else:
+            def arm():
+                eng.cg_begin(spec.max_iterations, spec.tolerance, config.tolerance_basis)
+
+            def solve():
+                eng.run(batch=config.batch, max_launches=launch_bound(spec.max_iterations, config.batch))
 
         arm()
-        eng.run(batch=config.batch, max_launches=launch_bound(spec.max_iterations, config.batch))  # sweep 0: rhs = b (zero halos), x0 = 0
+        solve()  # sweep 0: rhs = b (zero halos), x0 = 0
         rows, per_block, snapshots = [], [], []
         converged = False
         k = 0
@@ -295,7 +312,7 @@ def outer_solve(problem: LinearProblem, config: OuterConfig) -> SolveResult:
                 converged = True
                 eng.cancel()
                 break
-            eng.run(batch=config.batch, max_launches=launch_bound(spec.max_iterations, config.batch))
+            solve()
             k += 1
         eng.flush()
         sol = torch.empty(nz, ny, nx, dtype=torch.float64, device=dev)

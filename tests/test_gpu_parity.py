@@ -257,3 +257,60 @@ def test_outer_block_count_invariance_of_counts():
     tot, tot_o = np.sum(r1.inner_iterations_per_block), np.sum(ro.per_block_inner)
     assert abs(tot - tot_o) <= 1e-3 * tot_o
     assert np.linalg.norm(r1.solution - ro.solution) <= 1e-8 * np.linalg.norm(ro.solution)
+
+
+# ------------------------------------------------------------------ GMRES (a3)
+
+
+@pytest.mark.parametrize("key", ["gmres/8_200_10", "gmres/10_30_30", "gmres/6_40_7"])
+def test_gmres_matches_reference(key):
+    A, M = arrays(), meta()[key]
+    _, n, its, restart = key.replace("/", "_").split("_")
+    n, its, restart = int(n), int(its), int(restart)
+    tol = {"gmres/8_200_10": 1e-10, "gmres/10_30_30": 1e-3, "gmres/6_40_7": 0.0}[key]
+    prob = bs.build_laplace_3d(bs.Grid3D(n, n, n, bs.DirichletBoundary({"x_lo": 1.0, "y_hi": 0.5})))
+    x, rep = bs.gmres_solve(prob.matrix, prob.rhs, np.zeros(n ** 3), bs.InnerSolverSpec("gmres", its, tol, restart))
+    assert rep.iterations_used == M["iterations_used"]
+    assert rep.stop_reason == M["stop_reason"]
+    assert np.allclose(rep.residual_history, M["residual_history"], rtol=1e-8, atol=1e-13)
+    ref = A[key + "/x"]
+    assert np.abs(x - ref).max() <= 1e-10 * max(1.0, np.abs(ref).max())
+
+
+def test_gmres_edge_cases_and_oracle():
+    # 1x1x1: Krylov space closes after one step (happy breakdown, inner_solvers.py:196-198)
+    x, rep = bs.gmres_solve(bs.StencilOperator(1, 1, 1), np.array([3.0]), np.zeros(1),
+                            bs.InnerSolverSpec("gmres", 10, 0.0))
+    assert (rep.iterations_used, rep.stop_reason) == (1, "tolerance_met") and x[0] == 0.5
+    # zero rhs from a non-zero start
+    rng = np.random.default_rng(7)
+    op = bs.StencilOperator(5, 4, 3)
+    x, rep = bs.gmres_solve(op, np.zeros(60), rng.standard_normal(60), bs.InnerSolverSpec("gmres", 500, 1e-12))
+    assert rep.stop_reason == "tolerance_met" and np.abs(x).max() <= 1e-10
+    # restarted solve against the oracle on a ragged grid, warm start, r0 basis
+    shape = (37, 21, 13)
+    n = 37 * 21 * 13
+    b = O.seeded_rhs(n, 4)
+    x0 = rng.uniform(-1, 1, n)
+    a = O.laplace_csr(*shape)
+    xo, ro = O.gmres(lambda v: O.csr_spmv(a, v), b, x0, 120, 1e-6, 25, basis="initial")
+    x, rep = bs.gmres_solve(bs.StencilOperator(*shape), b, x0, bs.InnerSolverSpec("gmres", 120, 1e-6, 25),
+                            tolerance_basis="initial")
+    assert rep.iterations_used == ro.iterations_used and rep.stop_reason == ro.stop_reason
+    assert np.allclose(rep.residual_history, ro.residual_history, rtol=1e-7, atol=1e-14)
+    assert np.linalg.norm(x - xo) <= 1e-9 * np.linalg.norm(xo)
+
+
+def test_outer_sync_gmres_matches_oracle():
+    """GMRES(10) one cycle per sweep (multisplit.py:532-536), 2x2x2 boxes, overlap 0."""
+    n = 12
+    prob = bs.build_laplace_3d(bs.Grid3D(n, n, n, bs.DirichletBoundary({"z_lo": 1.0})))
+    cfg = bs.OuterConfig(block_grid=(2, 2, 2), inner=bs.InnerSolverSpec("gmres", 10), tol=1e-8)
+    res = bs.outer_solve(prob, cfg)
+    ro = O.outer_solve_sync((n, n, n), prob.rhs, (2, 2, 2), 0, dict(kind="gmres", max_iterations=10),
+                            tol=1e-8)
+    assert res.converged == ro.converged and res.outer_iterations == ro.outer_iterations
+    assert res.inner_iterations_per_block == ro.per_block_inner
+    for row, ref in zip(res.trace.rows, ro.rows):
+        assert row.estimated_residual == pytest.approx(ref.estimated_residual, rel=1e-8)
+    assert np.linalg.norm(res.solution - ro.solution) <= 1e-9 * np.linalg.norm(ro.solution)
