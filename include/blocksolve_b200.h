@@ -172,6 +172,20 @@ int bs_flush(bs_ctx *ctx, void *stream);
  * ghost[dir] plane (comm.py:332-365 + multisplit.py:341-369 with m=1). */
 int bs_halo_pack(bs_ctx *ctx, int nplan, const int32_t *plan, void *stream);
 
+/* a6 (overlap > 0): equal-weight merge of overlapping values
+ * (multisplit.py:341-369).  Requires every block's x to be final (bs_flush).
+ * Snapshots x into r (the post-solve payloads), then writes the 1/m average
+ * over covering blocks — own value first, neighbours in ascending id — into
+ * x at shared points, and the average over covering blocks into the halo
+ * cells (x cells outside the region, face planes). */
+int bs_overlap_merge(bs_ctx *ctx, void *stream);
+
+/* a7 (overlap > 0): local residual with owner-canonical values
+ * (multisplit.py:372-396) = b - A x_gathered on each block's owned rows,
+ * read from the snapshots of bs_overlap_merge; reported in r_owned_sq and
+ * rglob_owned_sq. */
+int bs_owner_residual(bs_ctx *ctx, void *stream);
+
 /* Number of kernels this library has launched (process lifetime). */
 unsigned long long bs_launch_count(void);
 

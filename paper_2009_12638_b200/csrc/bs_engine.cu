@@ -99,6 +99,7 @@ enum Phase : int {
     PH_G_FINAL = 10,  // w -= h_jj v_j ; ||w|| ; Givens ; stop tests
     PH_G_FORM = 11,   // x += V y
     PH_G_RESID = 12,  // true residual of the formed iterate ; restart or stop
+    PH_OWNRES = 13,   // residual of the gathered (owner) iterate on owned rows
 };
 
 enum Kind : int { KIND_CG = 0, KIND_GMRES = 1 };
@@ -106,9 +107,10 @@ enum Kind : int { KIND_CG = 0, KIND_GMRES = 1 };
 enum Op : int { OP_RESID = 0, OP_S1 = 1, OP_S2 = 2, OP_APPLY = 3, OP_GSPMV = 4 };
 
 // pointwise (non-stencil) GMRES passes
-enum Pk : int { PK_NORM = 0, PK_MGS = 1, PK_FINAL = 2, PK_FORM = 3 };
+enum Pk : int { PK_NORM = 0, PK_MGS = 1, PK_FINAL = 2, PK_FORM = 3, PK_OWNRES = 4 };
 
-constexpr int MAXM = 64;  // largest supported GMRES restart length
+constexpr int MAXM = 64;    // largest supported GMRES restart length
+constexpr int MAXNBR = 32;  // neighbour list capacity per block (overlapping merge)
 enum GFlag : int { GF_NONE = 0, GF_HAPPY = 1, GF_CHECK = 2, GF_CYCLE = 3 };
 
 // Stage layout per op: [A haloed][B haloed, if the op has one][C bare tile].
@@ -142,6 +144,8 @@ struct DBlock {
     double *V;          // GMRES basis: V[j] = V + j * vstride (pitched padded box)
     long long vstride;
     double *W;          // GMRES work vector w
+    int nnbr;           // neighbours, ascending ids (problems.py:343-349)
+    int nbr[MAXNBR];
 };
 
 struct DState {
@@ -784,7 +788,8 @@ __device__ __noinline__ void cg_transition(const DBlock &B, DState &S, int ph, c
             }
             break;
         }
-        case PH_RESID: {
+        case PH_RESID:
+        case PH_OWNRES: {
             for (int i = 0; i < NQ; ++i) S.q[i] = q[i];
             S.phase = PH_DONE;
             break;
@@ -795,7 +800,7 @@ __device__ __noinline__ void cg_transition(const DBlock &B, DState &S, int ph, c
 }
 
 __device__ void transition(const DBlock &B, DState &S, GState *G, int ph, const double *q) {
-    const bool gm = ph >= PH_G_NORM || (ph == PH_INIT && S.kind == KIND_GMRES);
+    const bool gm = (ph >= PH_G_NORM && ph <= PH_G_RESID) || (ph == PH_INIT && S.kind == KIND_GMRES);
     if (gm) gmres_transition(B, S, *G, ph, q);
     else cg_transition(B, S, ph, q);
 }
@@ -812,6 +817,7 @@ __device__ __forceinline__ bool serves(const DState &S, const KParams &P) {
     if (PKK == PK_MGS) return ph == PH_G_MGS && S.gj == P.launch_j && S.gi == P.launch_i;
     if (PKK == PK_FINAL) return ph == PH_G_FINAL && S.gj == P.launch_j;
     if (PKK == PK_FORM) return ph == PH_G_FORM;
+    if (PKK == PK_OWNRES) return ph == PH_OWNRES;
     return false;
 }
 
@@ -1000,6 +1006,42 @@ __global__ void __launch_bounds__(NT) k_point(const KParams P) {
                         acc[0] = add(acc[0], mul(w, w));
                     }
                 }
+            } else if (PKK == PK_OWNRES) {
+                // Local residual with owner-canonical values (multisplit.py:372-396): on
+                // owned rows every stencil neighbour is a region point (o >= 1), so this
+                // is b - A x_gathered, x_gathered[p] = owner's post-solve value
+                // (snapshot in each block's r).  acc[2] = acc[3] = ||r_owned||^2.
+                for (int lz = lz0; lz < lz1; ++lz, sx += plane) {
+                    const int gk = B.plo[2] + lz;
+                    if (!in_owned(B, gi, gj, gk)) continue;
+                    const int ni[6] = {gi, gi, gi - 1, gi + 1, gi, gi};
+                    const int nj[6] = {gj, gj - 1, gj, gj, gj + 1, gj};
+                    const int nk[6] = {gk - 1, gk, gk, gk, gk, gk + 1};
+                    double v[6];
+                    bool pg[6];
+#pragma unroll
+                    for (int d = 0; d < 6; ++d) {
+                        pg[d] = in_grid(B, ni[d], nj[d], nk[d]);
+                        v[d] = 0.0;
+                        if (!pg[d]) continue;
+                        if (in_owned(B, ni[d], nj[d], nk[d])) {
+                            v[d] = B.r[sidx(B, ni[d], nj[d], nk[d])];
+                        } else {
+                            for (int u = 0; u < B.nnbr; ++u) {
+                                const DBlock &U = P.blocks[B.nbr[u]];
+                                if (in_owned(U, ni[d], nj[d], nk[d])) {
+                                    v[d] = U.r[sidx(U, ni[d], nj[d], nk[d])];
+                                    break;
+                                }
+                            }
+                        }
+                    }
+                    const double ag = stencil7(v[0], v[1], v[2], B.r[sx], v[3], v[4], v[5], pg[0], pg[1], pg[2]);
+                    const double rg = sub(B.b[sx], ag);
+                    const double r2 = mul(rg, rg);
+                    acc[2] = add(acc[2], r2);
+                    acc[3] = add(acc[3], r2);
+                }
             } else {  // PK_FORM: x = x + V[:j+1]^T y (inner_solvers.py:173-175)
                 for (int lz = lz0; lz < lz1; ++lz, sx += plane) {
                     if (BOX || in_region(B, gi, gj, B.plo[2] + lz)) {
@@ -1011,7 +1053,84 @@ __global__ void __launch_bounds__(NT) k_point(const KParams P) {
             }
         }
     }
-    finish<NT, -1>(P, b, ph, served, acc, 1, smem);
+    finish<NT, -1>(P, b, ph, served, acc, PKK == PK_OWNRES ? NQ : 1, smem);
+}
+
+// ---- overlapping merge (multisplit.py:341-369), overlap > 0.  Inputs are the
+// post-solve snapshots (each block's r := x over its region); outputs are
+// written into x (shared points; coupled halo cells inside the padded box) and
+// the face planes (coupled cells just outside it).
+
+__global__ void k_snapshot(const DBlock *__restrict__ blocks) {
+    const DBlock &B = blocks[blockIdx.y];
+    const long long n = (long long)B.pitch * B.pdim[1] * B.pdim[2];
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += (long long)gridDim.x * blockDim.x)
+        B.r[c] = B.x[c];
+}
+
+// (own? + sum over covering neighbours in ascending id order) / cover count
+__device__ __forceinline__ double merged_value(const DBlock *blocks, const DBlock &T, bool own, double own_val,
+                                               int i, int j, int k) {
+    double acc = own ? own_val : 0.0;
+    int m = own ? 1 : 0;
+    for (int u = 0; u < T.nnbr; ++u) {
+        const DBlock &U = blocks[T.nbr[u]];
+        if (in_region(U, i, j, k)) {
+            acc = add(acc, U.r[sidx(U, i, j, k)]);
+            ++m;
+        }
+    }
+    return m ? __ddiv_rn(acc, (double)m) : 0.0;
+}
+
+__global__ void k_merge(const DBlock *__restrict__ blocks) {
+    const DBlock &T = blocks[blockIdx.y];
+    const long long n = (long long)T.pitch * T.pdim[1] * T.pdim[2];
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < n;
+         c += (long long)gridDim.x * blockDim.x) {
+        const int lx = (int)(c % T.pitch);
+        if (lx >= T.pdim[0]) continue;
+        const long long t = c / T.pitch;
+        const int i = T.plo[0] + lx, j = T.plo[1] + (int)(t % T.pdim[1]), k = T.plo[2] + (int)(t / T.pdim[1]);
+        if (in_owned(T, i, j, k) || !in_grid(T, i, j, k)) continue;
+        if (in_region(T, i, j, k)) {  // shared point: own value first, then neighbours
+            T.x[c] = merged_value(blocks, T, true, T.r[c], i, j, k);
+        } else if (in_region(T, i - 1, j, k) || in_region(T, i + 1, j, k) || in_region(T, i, j - 1, k) ||
+                   in_region(T, i, j + 1, k) || in_region(T, i, j, k - 1) || in_region(T, i, j, k + 1)) {
+            T.x[c] = merged_value(blocks, T, false, 0.0, i, j, k);  // coupled halo column
+        }
+    }
+}
+
+__global__ void k_merge_faces(const DBlock *__restrict__ blocks) {
+    const DBlock &T = blocks[blockIdx.y];
+    const int dir = blockIdx.z;
+    if (!T.ghost[dir]) return;
+    int nu, nv;
+    if (dir == 0 || dir == 5) {
+        nu = T.pdim[0];
+        nv = T.pdim[1];
+    } else if (dir == 1 || dir == 4) {
+        nu = T.pdim[0];
+        nv = T.pdim[2];
+    } else {
+        nu = T.pdim[1];
+        nv = T.pdim[2];
+    }
+    const long long n = (long long)nu * nv;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += (long long)gridDim.x * blockDim.x) {
+        const int u = (int)(c % nu), v = (int)(c / nu);
+        int i, j, k, di = 0, dj = 0, dk = 0;
+        switch (dir) {
+            case 0: i = T.plo[0] + u; j = T.plo[1] + v; k = T.plo[2] - 1; dk = 1; break;
+            case 5: i = T.plo[0] + u; j = T.plo[1] + v; k = T.plo[2] + T.pdim[2]; dk = -1; break;
+            case 1: i = T.plo[0] + u; j = T.plo[1] - 1; k = T.plo[2] + v; dj = 1; break;
+            case 4: i = T.plo[0] + u; j = T.plo[1] + T.pdim[1]; k = T.plo[2] + v; dj = -1; break;
+            case 2: i = T.plo[0] - 1; j = T.plo[1] + u; k = T.plo[2] + v; di = 1; break;
+            default: i = T.plo[0] + T.pdim[0]; j = T.plo[1] + u; k = T.plo[2] + v; di = -1; break;
+        }
+        if (in_region(T, i + di, j + dj, k + dk)) T.ghost[dir][c] = merged_value(blocks, T, false, 0.0, i, j, k);
+    }
 }
 
 // y = A_ii x on one block (standalone a1); x, y in the block's pitched layout.
@@ -1451,6 +1570,26 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
         }
         c->hblocks.push_back(B);
     }
+    // neighbour lists (problems.py:343-349): extended regions within one stencil
+    // step, i.e. L1 gap between owned boxes <= 2o+1; ascending block ids
+    for (int a = 0; a < nblocks; ++a) {
+        DBlock &A = c->hblocks[a];
+        A.nnbr = 0;
+        for (int b = 0; b < nblocks; ++b) {
+            if (b == a) continue;
+            const DBlock &Bn = c->hblocks[b];
+            int gap = 0;
+            for (int d = 0; d < 3; ++d)
+                gap += std::max(0, std::max(A.lo[d] - (Bn.hi[d] - 1), Bn.lo[d] - (A.hi[d] - 1)));
+            if (gap <= A.overlap + Bn.overlap + 1) {
+                if (A.nnbr >= MAXNBR) {
+                    delete c;
+                    return fail(BS_EINVAL, "bs_ctx_create: too many neighbours for block " + std::to_string(a));
+                }
+                A.nbr[A.nnbr++] = b;
+            }
+        }
+    }
     c->nctas = (int)cta_block.size();
     cudaError_t e = cudaSuccess;
     e = cudaMalloc(&c->dblocks, sizeof(DBlock) * nblocks);
@@ -1730,6 +1869,29 @@ int bs_gmres_run(bs_ctx *c, int max_cycles, void *stream, int64_t *kernels_out) 
         }
     }
     if (kernels_out) *kernels_out = (int64_t)(g_launches - l0);
+    return BS_OK;
+}
+
+int bs_overlap_merge(bs_ctx *c, void *stream) {
+    if (!c) return fail(BS_EINVAL, "bs_overlap_merge: null context");
+    if (int e = set_dev(c)) return e;
+    cudaStream_t st = (cudaStream_t)stream;
+    g_launches += 3;
+    k_snapshot<<<dim3(296, c->nblocks), 256, 0, st>>>(c->dblocks);
+    k_merge<<<dim3(296, c->nblocks), 256, 0, st>>>(c->dblocks);
+    k_merge_faces<<<dim3(64, c->nblocks, BS_NDIR), 256, 0, st>>>(c->dblocks);
+    BS_CU(cudaGetLastError());
+    return BS_OK;
+}
+
+int bs_owner_residual(bs_ctx *c, void *stream) {
+    if (!c) return fail(BS_EINVAL, "bs_owner_residual: null context");
+    if (int e = set_dev(c)) return e;
+    cudaStream_t st = (cudaStream_t)stream;
+    ++g_launches;
+    k_arm<<<(c->nblocks + 127) / 128, 128, 0, st>>>(c->dstates, nullptr, c->nblocks, PH_OWNRES, 0, 0.0, 0, 0, 0);
+    launch_point<PK_OWNRES>(c, st, 0, 0);
+    BS_CU(cudaGetLastError());
     return BS_OK;
 }
 

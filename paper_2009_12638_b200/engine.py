@@ -254,6 +254,12 @@ class BlockEngine:
         _lib.check(self.lib.bs_halo_pack(self.ctx, plan.shape[0], plan.ctypes.data_as(ctypes.c_void_p),
                                          self.stream))
 
+    def overlap_merge(self) -> None:
+        _lib.check(self.lib.bs_overlap_merge(self.ctx, self.stream))
+
+    def owner_residual(self) -> None:
+        _lib.check(self.lib.bs_owner_residual(self.ctx, self.stream))
+
     def reports(self) -> list:
         _lib.check(self.lib.bs_read_reports(self.ctx, self._reports, self.stream))
         return [self._reports[i] for i in range(self.nblocks)]

@@ -208,8 +208,6 @@ def _validate_device_path(config: OuterConfig) -> None:
     if config.inner.kind not in ("cg", "gmres"):
         raise ConfigurationError(
             f"inner: {config.inner.kind!r} is outside the accelerated path (device kinds: cg, gmres)")
-    if config.overlap != 0:
-        raise ConfigurationError("overlap: the device engine supports overlap 0 (pending)")
     if config.delay.kind != "none":
         raise ConfigurationError("delay: injected delays are a simulation knob; use kind='none'")
 
@@ -250,9 +248,10 @@ def outer_solve(problem: LinearProblem, config: OuterConfig) -> SolveResult:
     t_start = time.perf_counter()
     spec = config.inner
     with torch.cuda.device(dev):
-        eng = BlockEngine(grid.shape, decomp.owned, 0, dev, history_cap=1)
+        overlap = config.overlap
+        eng = BlockEngine(grid.shape, decomp.owned, overlap, dev, history_cap=1)
         eng.load_global("b", b_dev)
-        plan = box_halo_plan(decomp.owned, decomp.block_grid)
+        plan = box_halo_plan(decomp.owned, decomp.block_grid) if overlap == 0 else None
 
         if spec.kind == "gmres":
             # _make_inner_solver (multisplit.py:532-536): one cycle of the configured
@@ -287,9 +286,17 @@ def outer_solve(problem: LinearProblem, config: OuterConfig) -> SolveResult:
                     eng.close()
                     raise SolverBreakdownError(bid, k, f"{spec.kind} reported breakdown")
             per_block.append(its)
-            eng.halo_pack(plan)
-            arm()
-            eng.sweep_resid()
+            if overlap == 0:
+                # halo planes <- neighbours' boundary values; the next INIT sweep is at
+                # once the sweep-k residual and the rhs/r0 of sweep k+1
+                eng.halo_pack(plan)
+                arm()
+                eng.sweep_resid()
+            else:
+                # payload snapshot + 1/m merge, then the owner-canonical residual
+                eng.flush()
+                eng.overlap_merge()
+                eng.owner_residual()
             reps = eng.reports()
             locals_ = [math.sqrt(r.r_owned_sq) / dens[i] for i, r in enumerate(reps)]
             estimate = math.sqrt(sum(v ** 2 for v in locals_))  # comm.py:442-445 order
@@ -312,6 +319,8 @@ def outer_solve(problem: LinearProblem, config: OuterConfig) -> SolveResult:
                 converged = True
                 eng.cancel()
                 break
+            if overlap:
+                arm()
             solve()
             k += 1
         eng.flush()

@@ -180,7 +180,7 @@ def test_cg_config2_full_256_iteration_count():
 
 
 OUTER = ["outer/cfg1_16_fixed", "outer/cfg1_16_literal", "outer/cfg3_16_paper",
-         "outer/cfg3_16_true", "outer/box_12_222"]
+         "outer/cfg3_16_true", "outer/box_12_222", "outer/cfg5_12_o2", "outer/o1_10_211"]
 
 
 @pytest.mark.parametrize("key", OUTER)
