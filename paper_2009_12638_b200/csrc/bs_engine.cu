@@ -1246,6 +1246,113 @@ __global__ void k_halo_pack(const DBlock *__restrict__ blocks, const DState *sta
     }
 }
 
+// ------------------------------------------------------------------ async halo mailboxes
+// One-sided puts for asynchronous block Jacobi (comm.py:367-418 semantics on
+// real hardware): a sender stores its boundary plane (x + pending alpha p)
+// into slot seq % R of the receiver's ring and then publishes seq with a
+// system-scope release; the receiver picks the freshest published slot newer
+// than the one it applied (stale ones are never applied), copies it to its
+// halo plane and re-validates the slot's seq (seqlock) before accepting it.
+
+__device__ __forceinline__ void plane_cell(const DBlock &B, int dir, long long c, int nu, int &i, int &j, int &k) {
+    const int u = (int)(c % nu), v = (int)(c / nu);
+    switch (dir) {  // the block's own boundary plane facing `dir`
+        case 0: i = B.plo[0] + u; j = B.plo[1] + v; k = B.plo[2]; break;
+        case 5: i = B.plo[0] + u; j = B.plo[1] + v; k = B.plo[2] + B.pdim[2] - 1; break;
+        case 1: i = B.plo[0] + u; j = B.plo[1]; k = B.plo[2] + v; break;
+        case 4: i = B.plo[0] + u; j = B.plo[1] + B.pdim[1] - 1; k = B.plo[2] + v; break;
+        case 2: i = B.plo[0]; j = B.plo[1] + u; k = B.plo[2] + v; break;
+        default: i = B.plo[0] + B.pdim[0] - 1; j = B.plo[1] + u; k = B.plo[2] + v; break;
+    }
+}
+
+__host__ __device__ __forceinline__ int plane_nu(const int *pdim, int dir) {
+    return (dir == 2 || dir == 3) ? pdim[1] : pdim[0];
+}
+
+__host__ __device__ __forceinline__ long long plane_len(const int *pdim, int dir) {
+    if (dir == 0 || dir == 5) return (long long)pdim[0] * pdim[1];
+    if (dir == 1 || dir == 4) return (long long)pdim[0] * pdim[2];
+    return (long long)pdim[1] * pdim[2];
+}
+
+__global__ void k_async_post(const DBlock *__restrict__ blocks, const DState *states, int b, int dir, double *ring,
+                             unsigned long long *seqs, int R, unsigned long long seq, unsigned *counter) {
+    const DBlock &B = blocks[b];
+    const DState &S = states[b];
+    const int nu = plane_nu(B.pdim, dir);
+    const long long n = plane_len(B.pdim, dir);
+    double *slot = ring + (long long)(seq % (unsigned long long)R) * n;
+    const double a = S.alpha_pend;
+    const bool pend = S.pend != 0;
+    const double *p = B.p[S.pcur];
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += (long long)gridDim.x * blockDim.x) {
+        int i, j, k;
+        plane_cell(B, dir, c, nu, i, j, k);
+        const long long sx = sidx(B, i, j, k);
+        const double xv = B.x[sx];
+        slot[c] = pend ? add(xv, mul(a, p[sx])) : xv;
+    }
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence_system();  // payload visible system-wide before the seq (release)
+        *((volatile unsigned long long *)&seqs[seq % (unsigned long long)R]) = seq + 1;  // 0 = empty slot
+        *counter = 0u;
+    }
+}
+
+// pick[0] = chosen seq+1 (0: nothing newer), pick[1] = slot
+__global__ void k_async_pick(const unsigned long long *seqs, int R, const unsigned long long *applied,
+                             unsigned long long *pick) {
+    unsigned long long best = 0, slot = 0;
+    for (int s = 0; s < R; ++s) {
+        const unsigned long long v = ((const volatile unsigned long long *)seqs)[s];
+        if (v > best) {
+            best = v;
+            slot = s;
+        }
+    }
+    __threadfence_system();  // acquire: payload reads below follow the seq read
+    pick[0] = best > *applied ? best : 0ull;
+    pick[1] = slot;
+}
+
+__global__ void k_async_copy(const DBlock *__restrict__ blocks, int b, int gdir, const double *ring, long long n,
+                             const unsigned long long *pick, double *stage) {
+    if (pick[0] == 0) return;
+    const double *src = ring + (long long)pick[1] * n;
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += (long long)gridDim.x * blockDim.x)
+        stage[c] = ((const volatile double *)src)[c];
+}
+
+// seqlock check: the slot must still hold the chosen seq after the copy;
+// torn[0] counts rejected (overwritten-while-read) payloads.
+__global__ void k_async_check(const unsigned long long *seqs, unsigned long long *pick, unsigned long long *applied,
+                              int *torn) {
+    if (pick[0] == 0) return;
+    __threadfence_system();
+    if (((const volatile unsigned long long *)seqs)[pick[1]] != pick[0]) {
+        atomicAdd(torn, 1);
+        pick[0] = 0;
+        return;
+    }
+    *applied = pick[0];
+}
+
+__global__ void k_async_apply(const DBlock *__restrict__ blocks, int b, int gdir, long long n,
+                              const unsigned long long *pick, const double *stage) {
+    if (pick[0] == 0) return;
+    double *g = blocks[b].ghost[gdir];
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += (long long)gridDim.x * blockDim.x)
+        g[c] = stage[c];
+}
+
 // ------------------------------------------------------------------ host helpers
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -1303,6 +1410,8 @@ struct bs_ctx {
     int *hpinned = nullptr;  // [0]: n_active, [1..]: active mask staging
     DState *hstates = nullptr;
     Control *hctl = nullptr;
+    unsigned *dpost_counter = nullptr;     // async post completion counter
+    unsigned long long *dpick = nullptr;   // async receive scratch
     // GMRES(m) workspace (bs_gmres_setup)
     int gm = 0;
     GState *dgstates = nullptr;
@@ -1602,6 +1711,9 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
     if (e == cudaSuccess) e = cudaMalloc(&c->dnactive, sizeof(int));
     if (e == cudaSuccess) e = cudaMalloc(&c->dctl, sizeof(Control));
     if (e == cudaSuccess) e = cudaMalloc(&c->dactive, sizeof(int) * nblocks);
+    if (e == cudaSuccess) e = cudaMalloc(&c->dpost_counter, sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMemset(c->dpost_counter, 0, sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMalloc(&c->dpick, 2 * sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaHostAlloc(&c->hpinned, sizeof(int) * (nblocks + 1), cudaHostAllocDefault);
     if (e == cudaSuccess) e = cudaHostAlloc(&c->hstates, sizeof(DState) * nblocks, cudaHostAllocDefault);
     if (e == cudaSuccess) e = cudaHostAlloc(&c->hctl, sizeof(Control), cudaHostAllocDefault);
@@ -1650,6 +1762,8 @@ int bs_ctx_destroy(bs_ctx *c) {
     cudaFree(c->dplan);
     cudaFree(c->dgstates);
     cudaFree(c->dgmaps);
+    cudaFree(c->dpost_counter);
+    cudaFree(c->dpick);
     for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
     if (c->hpinned) cudaFreeHost(c->hpinned);
     if (c->hstates) cudaFreeHost(c->hstates);
@@ -1891,6 +2005,37 @@ int bs_owner_residual(bs_ctx *c, void *stream) {
     ++g_launches;
     k_arm<<<(c->nblocks + 127) / 128, 128, 0, st>>>(c->dstates, nullptr, c->nblocks, PH_OWNRES, 0, 0.0, 0, 0, 0);
     launch_point<PK_OWNRES>(c, st, 0, 0);
+    BS_CU(cudaGetLastError());
+    return BS_OK;
+}
+
+int bs_async_post(bs_ctx *c, int block, int dir, double *ring, uint64_t *seqs, int R, uint64_t seq,
+                  void *stream) {
+    if (!c || block < 0 || block >= c->nblocks || dir < 0 || dir >= BS_NDIR || !ring || !seqs || R < 1)
+        return fail(BS_EINVAL, "bs_async_post: bad arguments");
+    if (int e = set_dev(c)) return e;
+    ++g_launches;
+    k_async_post<<<64, 256, 0, (cudaStream_t)stream>>>(c->dblocks, c->dstates, block, dir, ring,
+                                                       (unsigned long long *)seqs, R, (unsigned long long)seq,
+                                                       c->dpost_counter);
+    BS_CU(cudaGetLastError());
+    return BS_OK;
+}
+
+int bs_async_receive(bs_ctx *c, int block, int ghost_dir, const double *ring, const uint64_t *seqs, int R,
+                     uint64_t *applied, double *stage, int *torn, void *stream) {
+    if (!c || block < 0 || block >= c->nblocks || ghost_dir < 0 || ghost_dir >= BS_NDIR || !ring || !seqs || R < 1 ||
+        !applied || !stage || !torn)
+        return fail(BS_EINVAL, "bs_async_receive: bad arguments");
+    if (!c->hblocks[block].ghost[ghost_dir]) return fail(BS_EINVAL, "bs_async_receive: no ghost plane");
+    if (int e = set_dev(c)) return e;
+    cudaStream_t st = (cudaStream_t)stream;
+    const long long n = plane_len(c->hblocks[block].pdim, ghost_dir);
+    g_launches += 4;
+    k_async_pick<<<1, 1, 0, st>>>((const unsigned long long *)seqs, R, (const unsigned long long *)applied, c->dpick);
+    k_async_copy<<<64, 256, 0, st>>>(c->dblocks, block, ghost_dir, ring, n, c->dpick, stage);
+    k_async_check<<<1, 1, 0, st>>>((const unsigned long long *)seqs, c->dpick, (unsigned long long *)applied, torn);
+    k_async_apply<<<64, 256, 0, st>>>(c->dblocks, block, ghost_dir, n, c->dpick, stage);
     BS_CU(cudaGetLastError());
     return BS_OK;
 }

@@ -99,6 +99,7 @@ class OuterConfig:
     device: str | None = None
     tolerance_basis: str = "rhs"
     batch: int = 4
+    residual_check_every: int = 1
 
     def __post_init__(self):
         if self.mode not in ("sync", "async"):
@@ -120,6 +121,8 @@ class OuterConfig:
             raise ConfigurationError(f"tolerance_basis: unknown basis {self.tolerance_basis!r}")
         if self.batch < 1:
             raise ConfigurationError("batch: must be at least 1")
+        if self.residual_check_every < 1:
+            raise ConfigurationError("residual_check_every: must be at least 1")
 
 
 @dataclass
@@ -203,8 +206,8 @@ def check_termination(estimate: float, tol: float, completed: int, max_outer: in
 
 
 def _validate_device_path(config: OuterConfig) -> None:
-    if config.mode != "sync":
-        raise ConfigurationError("mode: the device engine runs 'sync' (async pending)")
+    if config.mode == "async" and (config.inner.kind != "cg" or config.overlap != 0):
+        raise ConfigurationError("mode: async runs CG inner solves on overlap-0 decompositions")
     if config.inner.kind not in ("cg", "gmres"):
         raise ConfigurationError(
             f"inner: {config.inner.kind!r} is outside the accelerated path (device kinds: cg, gmres)")
@@ -247,6 +250,8 @@ def outer_solve(problem: LinearProblem, config: OuterConfig) -> SolveResult:
 
     t_start = time.perf_counter()
     spec = config.inner
+    if config.mode == "async":
+        return _outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, on_device, t_start)
     with torch.cuda.device(dev):
         overlap = config.overlap
         eng = BlockEngine(grid.shape, decomp.owned, overlap, dev, history_cap=1)
@@ -335,3 +340,28 @@ def outer_solve(problem: LinearProblem, config: OuterConfig) -> SolveResult:
     return SolveResult(solution=solution, trace=ResidualTrace(rows), converged=converged,
                        outer_iterations=len(rows), final_true_residual=final_true,
                        snapshots=snapshots, inner_iterations_per_block=per_block, wall_seconds=wall)
+
+
+def _outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, on_device, t_start):
+    from .async_driver import outer_solve_async
+    from .linalg import residual_norms
+
+    grid = problem.grid
+    sol, records, converged = outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, config.inner)
+    flat = sol.reshape(-1)
+    final_true = residual_norms(problem.matrix, flat, b_dev.reshape(-1))[1]
+    # trace aggregation across blocks (multisplit.py:769-787)
+    outer = max(len(r) for r in records)
+    rows = []
+    for k in range(outer):
+        at_k = [r[k] for r in records if k < len(r)]
+        est = records[0][k][2] if k < len(records[0]) else at_k[0][2]
+        rows.append(TraceRow(k, max(a[1] for a in at_k), est, None, int(sum(a[3] for a in at_k)),
+                             int(max(a[4] for a in at_k))))
+    if rows:
+        rows[-1].true_residual = final_true
+    per_block = [[r[k][3] if k < len(r) else 0 for r in records] for k in range(outer)]
+    solution = flat if on_device else flat.cpu().numpy()
+    return SolveResult(solution=solution, trace=ResidualTrace(rows), converged=converged, outer_iterations=outer,
+                       final_true_residual=final_true, inner_iterations_per_block=per_block,
+                       wall_seconds=time.perf_counter() - t_start)

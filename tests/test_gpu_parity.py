@@ -314,3 +314,30 @@ def test_outer_sync_gmres_matches_oracle():
     for row, ref in zip(res.trace.rows, ro.rows):
         assert row.estimated_residual == pytest.approx(ref.estimated_residual, rel=1e-8)
     assert np.linalg.norm(res.solution - ro.solution) <= 1e-9 * np.linalg.norm(ro.solution)
+
+
+# ------------------------------------------------------------------ async (a9)
+
+
+def test_async_converges_to_the_sync_solution():
+    """Async block Jacobi (config-4 shape: z-slabs, CG fixed 10 its, residual
+    checked every 5 sweeps, confirmed stop).  Nondeterministic by design
+    (SURVEY §0 item 7): compare the converged result only — true residual
+    below tol and distance to a tight solve within 10x the sync oracle's."""
+    n = 24
+    b = O.seeded_rhs(n ** 3, 0)
+    prob = bs.LinearProblem(bs.StencilOperator(n, n, n), b, bs.Grid3D(n, n, n))
+    tol = 1e-8
+    cfg = bs.OuterConfig(block_grid=(1, 1, 4), inner=bs.InnerSolverSpec("cg", 10), mode="async", tol=tol,
+                         max_outer=3000, residual_check_every=5)
+    res = bs.outer_solve(prob, cfg)
+    assert res.converged
+    assert res.final_true_residual < tol
+    a = O.laplace_csr(n, n, n)
+    tight, _ = O.cg(lambda v: O.csr_spmv(a, v), b, np.zeros(n ** 3), 5000, 1e-13)
+    ro = O.outer_solve_sync((n, n, n), b, (1, 1, 4), 0, dict(kind="cg", max_iterations=10), tol=tol)
+    sync_err = np.linalg.norm(ro.solution - tight) / np.linalg.norm(tight)
+    async_err = np.linalg.norm(res.solution - tight) / np.linalg.norm(tight)
+    assert async_err <= 10 * sync_err
+    assert res.outer_iterations >= 10
+    assert all(row.inner_iterations > 0 for row in res.trace.rows)
