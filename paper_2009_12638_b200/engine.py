@@ -176,6 +176,38 @@ class BlockEngine:
             (x0, y0, z0), (x1, y1, z1) = bb.padded.lo, bb.padded.hi
             bb.view3(getattr(bb, name)).copy_(g3[z0:z1, y0:y1, x0:x1])
 
+    def load_host(self, name: str, g3: np.ndarray) -> None:
+        """Scatter a global (nz, ny, nx) host array into every block's padded box."""
+        for bb in self.blocks:
+            (x0, y0, z0), (x1, y1, z1) = bb.padded.lo, bb.padded.hi
+            src = torch.from_numpy(np.ascontiguousarray(g3[z0:z1, y0:y1, x0:x1])).to(self.device)
+            bb.view3(getattr(bb, name)).copy_(src)
+
+    # -- halo planes across processes (distributed.py) --------------------
+    @property
+    def comm_device(self):
+        return self.device
+
+    def plane_len(self, block: int, direction: int) -> int:
+        px, py, pz = self.blocks[block].dims
+        return {0: px * py, 5: px * py, 1: px * pz, 4: px * pz}.get(direction, py * pz)
+
+    def new_plane(self, n: int) -> "torch.Tensor":
+        return torch.zeros(n, dtype=torch.float64, device=self.device)
+
+    def ghost(self, block: int, direction: int) -> "torch.Tensor":
+        return self.blocks[block].ghost[direction]
+
+    def post_plane(self, block: int, direction: int, buf: "torch.Tensor") -> None:
+        """Block's own boundary plane facing `direction` (x + pending alpha p) -> buf."""
+        if not hasattr(self, "_seq1"):
+            self._seq1 = torch.zeros(1, dtype=torch.int64, device=self.device)
+        _lib.check(self.lib.bs_async_post(self.ctx, block, direction, buf.data_ptr(), self._seq1.data_ptr(), 1, 0,
+                                          self.stream))
+
+    def synchronize(self) -> None:
+        torch.cuda.current_stream(self.device).synchronize()
+
     def gather_owned(self, out3: "torch.Tensor", name: str = "x") -> None:
         """Write every block's owned values of ``name`` into a global (nz, ny, nx) tensor."""
         for bb in self.blocks:

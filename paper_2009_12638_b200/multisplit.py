@@ -30,10 +30,11 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .engine import BlockEngine, box_halo_plan, launch_bound, require_cuda, torch
-from .errors import ConfigurationError, SolverBreakdownError
+from .engine import BlockEngine, box_halo_plan, require_cuda, torch
+from .errors import ConfigurationError
 from .inner_solvers import InnerSolverSpec
 from .problems import LinearProblem, decompose
+from .sync_driver import run_sync
 
 __all__ = [
     "OuterConfig",
@@ -257,83 +258,27 @@ def outer_solve(problem: LinearProblem, config: OuterConfig) -> SolveResult:
         eng = BlockEngine(grid.shape, decomp.owned, overlap, dev, history_cap=1)
         eng.load_global("b", b_dev)
         plan = box_halo_plan(decomp.owned, decomp.block_grid) if overlap == 0 else None
+        snapshots = []
 
-        if spec.kind == "gmres":
-            # _make_inner_solver (multisplit.py:532-536): one cycle of the configured
-            # length unless a restart is given; gmres_solve caps it at n (162)
-            restart = spec.restart if spec.restart is not None else spec.max_iterations
-            restart = min(restart, min(bb.padded.size for bb in eng.blocks))
-            eng.gmres_setup(restart)
-
-            def arm():
-                eng.gmres_begin(spec.max_iterations, spec.tolerance, config.tolerance_basis)
-
-            def solve():
-                eng.gmres_run(max_cycles=spec.max_iterations + 2)
-        else:
-            def arm():
-                eng.cg_begin(spec.max_iterations, spec.tolerance, config.tolerance_basis)
-
-            def solve():
-                eng.run(batch=config.batch, max_launches=launch_bound(spec.max_iterations, config.batch))
-
-        arm()
-        solve()  # sweep 0: rhs = b (zero halos), x0 = 0
-        rows, per_block, snapshots = [], [], []
-        converged = False
-        k = 0
-        final_true = math.nan
-        while True:
-            reps = eng.reports()
-            its = [int(r.iterations_used) for r in reps]
-            for bid, r in enumerate(reps):
-                if int(r.stop_reason) == 3:
-                    eng.close()
-                    raise SolverBreakdownError(bid, k, f"{spec.kind} reported breakdown")
-            per_block.append(its)
-            if overlap == 0:
-                # halo planes <- neighbours' boundary values; the next INIT sweep is at
-                # once the sweep-k residual and the rhs/r0 of sweep k+1
-                eng.halo_pack(plan)
-                arm()
-                eng.sweep_resid()
-            else:
-                # payload snapshot + 1/m merge, then the owner-canonical residual
-                eng.flush()
-                eng.overlap_merge()
-                eng.owner_residual()
-            reps = eng.reports()
-            locals_ = [math.sqrt(r.r_owned_sq) / dens[i] for i, r in enumerate(reps)]
-            estimate = math.sqrt(sum(v ** 2 for v in locals_))  # comm.py:442-445 order
-            true_res = math.sqrt(sum(float(r.rglob_owned_sq) for r in reps)) / bnorm if bnorm else math.inf
-            want_true = config.residual_check_mode == "true" or k % config.true_residual_interval == 0
-            now = float(k) if config.execution == "replay" else time.perf_counter() - t_start
-            rows.append(TraceRow(k, now, estimate, true_res if want_true else None, int(sum(its)), 0))
+        def capture(k):
             if config.capture_iterates:
                 snap = torch.empty(nz, ny, nx, dtype=torch.float64, device=dev)
                 eng.flush()
                 eng.gather_owned(snap)
                 snapshots.append((k, snap.reshape(-1).cpu().numpy()))
-            final_true = true_res
-            decision = check_termination(estimate, config.tol, k + 1, config.max_outer, "sync")
-            if decision == "stop":
-                converged = estimate < config.tol
-                eng.cancel()
-                break
-            if config.residual_check_mode == "true" and true_res < config.tol:
-                converged = True
-                eng.cancel()
-                break
-            if overlap:
-                arm()
-            solve()
-            k += 1
-        eng.flush()
-        sol = torch.empty(nz, ny, nx, dtype=torch.float64, device=dev)
-        eng.gather_owned(sol)
-        torch.cuda.synchronize(dev)
-        eng.close()
+
+        try:
+            trace, per_block, converged, final_true = run_sync(
+                eng, config, dens, bnorm, decomp.num_blocks, list(range(decomp.num_blocks)),
+                lambda: eng.halo_pack(plan), lambda table: table, t_start, on_sweep=capture)
+            eng.flush()
+            sol = torch.empty(nz, ny, nx, dtype=torch.float64, device=dev)
+            eng.gather_owned(sol)
+            torch.cuda.synchronize(dev)
+        finally:
+            eng.close()
     wall = time.perf_counter() - t_start
+    rows = [TraceRow(k, t, est, tr, inner, 0) for k, t, est, tr, inner in trace]
     if rows and rows[-1].true_residual is None:
         rows[-1].true_residual = final_true
     solution = sol.reshape(-1) if on_device else sol.reshape(-1).cpu().numpy()

@@ -1,0 +1,114 @@
+"""The synchronous outer sweep (multisplit.py:544-707, replay semantics) over a
+set of engine blocks — all blocks of the problem (one GPU) or this rank's
+share of them (one process per GPU, see ``distributed.py``).
+
+Schedule of sweep k (every block at once, device-side):
+
+  1. inner solve (fused CG sweeps or GMRES(m) Arnoldi passes);
+  2. overlap 0: halo exchange — neighbours' boundary planes (x + pending
+     alpha p) land in this block's halo planes (comm.py:332-365, merge with
+     m = 1), locally by ``k_halo_pack`` or across ranks by P2P; then one
+     residual sweep that is at once the sweep-k local residual
+     (multisplit.py:372-396), the true residual on owned rows (404-406) and
+     the rhs/r0 assembly of sweep k+1 (333-338).
+     overlap > 0: flush, snapshot + 1/m merge, owner-canonical residual;
+  3. per-block scalars are combined across blocks (and ranks) into one array
+     ordered by block id; every rank evaluates the same estimate exactly as
+     comm.py:442-445 does and takes the same decision (409-426).
+"""
+
+from __future__ import annotations
+
+import math
+import time
+
+import numpy as np
+
+from .engine import launch_bound
+from .errors import SolverBreakdownError
+
+
+def make_inner(eng, spec, config):
+    """(arm, solve) callables for the configured inner solver."""
+    if spec.kind == "gmres":
+        # _make_inner_solver (multisplit.py:532-536): one cycle of the configured
+        # length unless a restart is given; gmres_solve caps it at n (162)
+        restart = spec.restart if spec.restart is not None else spec.max_iterations
+        restart = min(restart, min(bb.padded.size for bb in eng.blocks))
+        eng.gmres_setup(restart)
+
+        def arm():
+            eng.gmres_begin(spec.max_iterations, spec.tolerance, config.tolerance_basis)
+
+        def solve():
+            eng.gmres_run(max_cycles=spec.max_iterations + 2)
+    else:
+        def arm():
+            eng.cg_begin(spec.max_iterations, spec.tolerance, config.tolerance_basis)
+
+        def solve():
+            eng.run(batch=config.batch, max_launches=launch_bound(spec.max_iterations, config.batch))
+    return arm, solve
+
+
+def run_sync(eng, config, dens, bnorm, nblocks, local_ids, exchange, allreduce_rows, t_start,
+             on_sweep=None):
+    """Run sweeps until the reference's termination rule fires.
+
+    ``exchange()`` performs the overlap-0 halo exchange; ``allreduce_rows(a)``
+    sums an (nblocks, 4) array whose rows only the owning rank fills (exact:
+    every entry is nonzero on one rank).  Returns (rows, per_block, converged,
+    final_true) with rows = (k, time, estimate, true_or_None, inner_total).
+    """
+    spec = config.inner
+    overlap = eng.overlap
+    arm, solve = make_inner(eng, spec, config)
+    arm()
+    solve()  # sweep 0: rhs = b (zero halos), x0 = 0
+    rows, per_block = [], []
+    converged = False
+    final_true = math.nan
+    k = 0
+    while True:
+        its_reps = eng.reports()
+        if overlap == 0:
+            exchange()
+            arm()
+            eng.sweep_resid()
+        else:
+            eng.flush()
+            eng.overlap_merge()
+            eng.owner_residual()
+        reps = eng.reports()
+        table = np.zeros((nblocks, 4))
+        for li, gid in enumerate(local_ids):
+            table[gid] = (its_reps[li].iterations_used, 1.0 if int(its_reps[li].stop_reason) == 3 else 0.0,
+                          reps[li].r_owned_sq, reps[li].rglob_owned_sq)
+        table = allreduce_rows(table)
+        broken = np.nonzero(table[:, 1])[0]
+        if broken.size:
+            raise SolverBreakdownError(int(broken[0]), k, f"{spec.kind} reported breakdown")
+        its = [int(v) for v in table[:, 0]]
+        per_block.append(its)
+        locals_ = [math.sqrt(table[g, 2]) / dens[g] for g in range(nblocks)]
+        estimate = math.sqrt(sum(v ** 2 for v in locals_))  # comm.py:442-445 order
+        true_res = math.sqrt(sum(float(table[g, 3]) for g in range(nblocks))) / bnorm if bnorm else math.inf
+        want_true = config.residual_check_mode == "true" or k % config.true_residual_interval == 0
+        now = float(k) if config.execution == "replay" else time.perf_counter() - t_start
+        rows.append((k, now, estimate, true_res if want_true else None, int(sum(its))))
+        if on_sweep is not None:
+            on_sweep(k)
+        final_true = true_res
+        if estimate < config.tol or k + 1 >= config.max_outer:  # check_termination (409-426)
+            converged = estimate < config.tol
+            eng.cancel()
+            break
+        if config.residual_check_mode == "true" and true_res < config.tol:  # 685-686
+            converged = True
+            eng.cancel()
+            break
+        if overlap:
+            arm()
+        solve()
+        k += 1
+    return rows, per_block, converged, final_true

@@ -341,3 +341,55 @@ def test_async_converges_to_the_sync_solution():
     assert async_err <= 10 * sync_err
     assert res.outer_iterations >= 10
     assert all(row.inner_iterations > 0 for row in res.trace.rows)
+
+
+# ------------------------------------------------------------------ multi-rank plumbing (e)
+
+
+def test_post_plane_matches_device_halo_pack():
+    """The cross-rank send buffer (bs_async_post) carries exactly what the
+    same-GPU pack (bs_halo_pack) stores in the neighbour's halo plane."""
+    t = torch()
+    n = 20
+    b = O.seeded_rhs(n ** 3, 1)
+    dec = bs.decompose(bs.Grid3D(n, n, n), (2, 1, 2), 0)
+    eng = BlockEngine((n, n, n), dec.owned, 0, "cuda")
+    eng.load_host("b", b.reshape(n, n, n))
+    eng.cg_begin(7, 0.0)
+    eng.run()
+    from paper_2009_12638_b200.engine import box_halo_plan
+    plan = box_halo_plan(dec.owned, dec.block_grid)
+    eng.halo_pack(plan)
+    for dst, d, src in plan.tolist():
+        buf = eng.new_plane(eng.plane_len(src, 5 - d))
+        eng.post_plane(src, 5 - d, buf)
+        t.cuda.synchronize()
+        assert t.equal(buf, eng.ghost(dst, d))
+    eng.close()
+
+
+def test_distributed_driver_single_rank_nccl_equals_outer_solve():
+    import socket
+
+    t = torch()
+    from paper_2009_12638_b200.distributed import outer_solve_distributed
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    t.distributed.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        n = 24
+        b = O.seeded_rhs(n ** 3, 0)
+        prob = bs.LinearProblem(bs.StencilOperator(n, n, n), b, bs.Grid3D(n, n, n))
+        cfg = bs.OuterConfig(block_grid=(1, 1, 4), inner=bs.InnerSolverSpec("cg", 20, 1e-2), tol=1e-8,
+                             tolerance_basis="initial")
+        rd = outer_solve_distributed(prob, cfg)
+        rl = bs.outer_solve(prob, cfg)
+        assert rd.outer_iterations == rl.outer_iterations
+        assert rd.inner_iterations_per_block == rl.inner_iterations_per_block
+        assert [r.estimated_residual for r in rd.trace.rows] == [r.estimated_residual for r in rl.trace.rows]
+        assert np.array_equal(rd.solution, rl.solution)
+    finally:
+        t.distributed.destroy_process_group()
