@@ -294,7 +294,8 @@ class BlockEngine:
 
     def reports(self) -> list:
         _lib.check(self.lib.bs_read_reports(self.ctx, self._reports, self.stream))
-        return [self._reports[i] for i in range(self.nblocks)]
+        # copies: the next read reuses the staging array
+        return [_lib.BlockReport.from_buffer_copy(self._reports[i]) for i in range(self.nblocks)]
 
 
 def launch_bound(max_iterations: int, batch: int) -> int:
