@@ -79,6 +79,9 @@ constexpr int NQ = 4;                  // partial sums per CTA
 #define BS_NSTAGE_A 12   // ring depth of sweeps staging one haloed operand
 #endif
 constexpr int PITCH_ALIGN = 4;         // doubles
+#ifndef BS_MINBLOCKS
+#define BS_MINBLOCKS 3   // resident CTAs per SM the sweep kernels are compiled for
+#endif
 
 constexpr int SEG_H = ((SC * 8 + 127) / 128) * 128;  // staged haloed box, 128B aligned
 constexpr int SEG_O = NT * 8;                         // bare tile
@@ -478,11 +481,19 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
     if (lane == 0) mbar_arrive(&empty[0]);
 
     const bool px_box = lx > 0, py_box = ly > 0;
+    // output pointers hoisted into registers: stores through them cannot alias
+    // the block descriptor, so the compiler need not re-load it every plane
+    double *__restrict__ out_r = B.r;
+    double *__restrict__ out_x = B.x;
+    double *__restrict__ out_w = B.W;
+    double *__restrict__ out_p = C.pout;
+    double *__restrict__ out_y = C.yout;
+    int s = 1 % NS, sn = 2 % NS;   // stage of plane q and q+1
+    uint32_t par_n = 2 / NS;        // completion parity of stage sn
     for (int q = 1; q <= nplanes - 2; ++q) {
-        const int s = q % NS, sn = (q + 1) % NS;
         const int lz = lz0 - 1 + q;
         const unsigned char *st = smem + s * STB;
-        mbar_wait(&full[sn], (uint32_t)(((q + 1) / NS) & 1));
+        mbar_wait(&full[sn], par_n & 1u);
         const double u_next = uval(smem + sn * STB, own, 0, 0, lz + 1);
         const bool here = BOX ? col_in : (col_in && in_region(B, gi, gj, B.plo[2] + lz));
         if (here) {
@@ -502,18 +513,18 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
             const double au = stencil7(u_prev, ym, xm, u_cur, xp, yp, u_next, pz, py, px);
             const double *cst = reinterpret_cast<const double *>(st + COFF);
             if (OP == OP_APPLY) {
-                C.yout[sx] = au;
+                out_y[sx] = au;
             } else if (OP == OP_GSPMV) {  // w = A v_j ; h_0j = v_0 . w (inner_solvers.py:187-190)
-                B.W[sx] = au;
+                out_w[sx] = au;
                 const double v0 = first ? u_cur : cst[tid];
                 acc[0] = add(acc[0], mul(v0, au));
             } else if (OP == OP_S2) {
                 const double rnv = sub(cst[tid], mul(alpha, au));
-                B.r[sx] = rnv;
+                out_r[sx] = rnv;
                 acc[0] = add(acc[0], mul(rnv, rnv));
             } else if (OP == OP_S1) {
-                C.pout[sx] = u_cur;
-                if (pend) B.x[sx] = add(cst[tid], mul(alpha_pend, reinterpret_cast<const double *>(st + SEG_H)[own]));
+                out_p[sx] = u_cur;
+                if (pend) out_x[sx] = add(cst[tid], mul(alpha_pend, reinterpret_cast<const double *>(st + SEG_H)[own]));
                 acc[0] = add(acc[0], mul(u_cur, au));
             } else {  // OP_RESID: r = (b - C*halo) - A_ii u
                 const double bv = cst[tid];
@@ -548,7 +559,7 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
                     rg_au = stencil7(v[0], v[1], v[2], u_cur, v[3], v[4], v[5], pg[0], pg[1], pg[2]);
                 }
                 const double rv = sub(rhs, au);
-                B.r[sx] = rv;
+                out_r[sx] = rv;
                 acc[0] = add(acc[0], mul(rhs, rhs));
                 const double r2 = mul(rv, rv);
                 acc[1] = add(acc[1], r2);
@@ -564,6 +575,11 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
         u_cur = u_next;
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
+        s = sn;
+        if (++sn == NS) {
+            sn = 0;
+            ++par_n;
+        }
     }
 }
 
@@ -900,7 +916,7 @@ __device__ void finish(const KParams &P, int b, int ph, bool served, double (&ac
 
 // One sweep over every block whose phase this kernel serves.
 template <int OPK, bool BOX>
-__global__ void __launch_bounds__(NTHR, 3) k_sweep(const KParams P) {
+__global__ void __launch_bounds__(NTHR, BS_MINBLOCKS) k_sweep(const KParams P) {
     extern __shared__ __align__(1024) unsigned char smem[];
     const int b = P.cta_block[blockIdx.x];
     const DBlock &B = P.blocks[b];
