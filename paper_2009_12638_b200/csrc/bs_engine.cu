@@ -1292,6 +1292,13 @@ __host__ __device__ __forceinline__ long long plane_len(const int *pdim, int dir
     return (long long)pdim[1] * pdim[2];
 }
 
+// Seqlock writer side: retire the slot before its payload is overwritten, so
+// a reader that picked the slot's previous seq fails its re-validation.
+__global__ void k_async_retire(unsigned long long *seqs, int R, unsigned long long seq) {
+    *((volatile unsigned long long *)&seqs[seq % (unsigned long long)R]) = 0ull;
+    __threadfence_system();
+}
+
 __global__ void k_async_post(const DBlock *__restrict__ blocks, const DState *states, int b, int dir, double *ring,
                              unsigned long long *seqs, int R, unsigned long long seq, unsigned *counter) {
     const DBlock &B = blocks[b];
@@ -2030,7 +2037,8 @@ int bs_async_post(bs_ctx *c, int block, int dir, double *ring, uint64_t *seqs, i
     if (!c || block < 0 || block >= c->nblocks || dir < 0 || dir >= BS_NDIR || !ring || !seqs || R < 1)
         return fail(BS_EINVAL, "bs_async_post: bad arguments");
     if (int e = set_dev(c)) return e;
-    ++g_launches;
+    g_launches += 2;
+    k_async_retire<<<1, 1, 0, (cudaStream_t)stream>>>((unsigned long long *)seqs, R, (unsigned long long)seq);
     k_async_post<<<64, 256, 0, (cudaStream_t)stream>>>(c->dblocks, c->dstates, block, dir, ring,
                                                        (unsigned long long *)seqs, R, (unsigned long long)seq,
                                                        c->dpost_counter);

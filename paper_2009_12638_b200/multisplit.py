@@ -292,7 +292,8 @@ def _outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, on_devi
     from .linalg import residual_norms
 
     grid = problem.grid
-    sol, records, converged = outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, config.inner)
+    sol, records, converged, lapped = outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev,
+                                                       config.inner)
     flat = sol.reshape(-1)
     final_true = residual_norms(problem.matrix, flat, b_dev.reshape(-1))[1]
     # trace aggregation across blocks (multisplit.py:769-787)
@@ -309,4 +310,5 @@ def _outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, on_devi
     solution = flat if on_device else flat.cpu().numpy()
     return SolveResult(solution=solution, trace=ResidualTrace(rows), converged=converged, outer_iterations=outer,
                        final_true_residual=final_true, inner_iterations_per_block=per_block,
-                       wall_seconds=time.perf_counter() - t_start)
+                       wall_seconds=time.perf_counter() - t_start,
+                       comm_events=[("lapped_reads", lapped)])
