@@ -263,6 +263,13 @@ __device__ __forceinline__ double stencil7(double zm, double ym, double xm, doub
     return add(t3, add(add(-xp, -yp), -zp));
 }
 
+// Interior row (all seven terms present): the reduceat order without any
+// presence logic.  Callers take this path only when it is warp-uniform.
+__device__ __forceinline__ double stencil7_interior(double zm, double ym, double xm, double c, double xp, double yp,
+                                                    double zp) {
+    return add(-zm, add(add(add(add(add(-ym, -xm), mul(6.0, c)), -xp), -yp), -zp));
+}
+
 // ------------------------------------------------------------------ TMA / mbarrier
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -481,6 +488,9 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
     if (lane == 0) mbar_arrive(&empty[0]);
 
     const bool px_box = lx > 0, py_box = ly > 0;
+    // warp-uniform fast path: every lane of this warp has its x-1 and y-1
+    // neighbours in the box (only the tile column at x = 0 / row at y = 0 differ)
+    const bool warp_xy_interior = BOX && __all_sync(0xffffffffu, px_box && py_box);
     // output pointers hoisted into registers: stores through them cannot alias
     // the block descriptor, so the compiler need not re-load it every plane
     double *__restrict__ out_r = B.r;
@@ -499,18 +509,23 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
         if (here) {
             const double xm = uval(st, own - 1, -1, 0, lz), xp = uval(st, own + 1, 1, 0, lz);
             const double ym = uval(st, own - SX, 0, -1, lz), yp = uval(st, own + SX, 0, 1, lz);
-            bool pz, py, px;
-            if (BOX) {
-                pz = lz > 0;
-                py = py_box;
-                px = px_box;
+            double au;
+            if (BOX && warp_xy_interior && lz > 0) {
+                au = stencil7_interior(u_prev, ym, xm, u_cur, xp, yp, u_next);
             } else {
-                const int gk = B.plo[2] + lz;
-                pz = in_region(B, gi, gj, gk - 1);
-                py = in_region(B, gi, gj - 1, gk);
-                px = in_region(B, gi - 1, gj, gk);
+                bool pz, py, px;
+                if (BOX) {
+                    pz = lz > 0;
+                    py = py_box;
+                    px = px_box;
+                } else {
+                    const int gk = B.plo[2] + lz;
+                    pz = in_region(B, gi, gj, gk - 1);
+                    py = in_region(B, gi, gj - 1, gk);
+                    px = in_region(B, gi - 1, gj, gk);
+                }
+                au = stencil7(u_prev, ym, xm, u_cur, xp, yp, u_next, pz, py, px);
             }
-            const double au = stencil7(u_prev, ym, xm, u_cur, xp, yp, u_next, pz, py, px);
             const double *cst = reinterpret_cast<const double *>(st + COFF);
             if (OP == OP_APPLY) {
                 out_y[sx] = au;
