@@ -62,9 +62,13 @@ int fail(int code, const std::string &msg) {
             return fail(BS_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
-constexpr int TX = 32;                 // tile width  (one consumer lane per column)
-constexpr int TY = 8;                  // tile height (one consumer warp per row)
+#ifndef BS_TX
+#define BS_TX 32
+#endif
+constexpr int TX = BS_TX;              // tile width (x, contiguous)
+constexpr int TY = 256 / TX;           // tile height: 256 consumer threads, one column each
 constexpr int NT = TX * TY;            // consumer threads
+constexpr int NCW = NT / 32;           // consumer warps
 constexpr int NTHR = NT + 32;          // + one TMA producer warp
 constexpr int HY = TY + 2;
 // TMA boxes must start on a 16-byte boundary in the innermost dimension, so
@@ -393,10 +397,10 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 
 // Process one tile (TX x TY columns, planes [lz0, lz1) of the padded box).
 //
-// Warp roles: warps 0..TY-1 consume (lane = x, warp = y of the tile), warp TY
+// Warp roles: warps 0..NCW-1 consume (thread = one column of the tile), warp NCW
 // produces: its lane 0 streams plane q = 0..nplanes-1 (lz = lz0-1+q) into
 // stage q % NS with TMA, after every consumer warp released that stage's
-// previous plane (empty mbarrier, count TY).  Consumers never block on each
+// previous plane (empty mbarrier, count NCW).  Consumers never block on each
 // other — only on `full` — so there is no CTA-wide barrier per plane.
 //
 // BOX (overlap 0, region == padded box): TMA zero-fill supplies the absent
@@ -430,14 +434,14 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], TY);
+            mbar_init(&empty[s], NCW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncthreads();
 
-    if (warp == TY) {  // ---------------- TMA producer warp
+    if (warp == NCW) {  // ---------------- TMA producer warp
         if (lane == 0) {
             for (int q = 0; q < nplanes; ++q) {
                 const int s = q % NS;
@@ -457,7 +461,7 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
     }
 
     // ---------------- consumers
-    const int tx = lane, ty = warp;
+    const int tx = tid % TX, ty = tid / TX;
     const int lx = lx0 + tx, ly = ly0 + ty;
     const bool col_in = lx < pdx && ly < pdy;
     const int gi = B.plo[0] + lx, gj = B.plo[1] + ly;
