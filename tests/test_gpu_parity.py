@@ -197,14 +197,18 @@ def test_outer_sync_matches_reference(key):
     res = bs.outer_solve(prob, cfg)
     assert res.converged == M["converged"]
     assert res.outer_iterations == M["outer_iterations"]
+    # per-sweep residuals: 1e-9 relative plus an absolute floor of 5e-12 — the
+    # reference algorithm itself moves its box_12_222 estimates by 8.3e-13
+    # absolute (1.5e-6 relative) when only its dot products are reassociated
+    # (measured with the oracle)
     for row, ref in zip(res.trace.rows, M["trace"]):
         assert row.outer_iteration == ref[0] and row.time == ref[1]
         assert row.inner_iterations == ref[4], f"sweep {ref[0]}"
-        assert row.estimated_residual == pytest.approx(ref[2], rel=1e-9)
+        assert row.estimated_residual == pytest.approx(ref[2], rel=1e-9, abs=5e-12)
         if ref[3] is None:
             assert row.true_residual is None
         else:
-            assert row.true_residual == pytest.approx(ref[3], rel=1e-9)
+            assert row.true_residual == pytest.approx(ref[3], rel=1e-9, abs=5e-12)
         assert row.max_halo_staleness == ref[5]
     sol = A[key + "/solution"]
     assert np.linalg.norm(res.solution - sol) <= 1e-10 * np.linalg.norm(sol)
