@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--cpu-its", type=int, default=6, help="CG iterations in the CPU sample")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--workload", default="config2", choices=["config2", "config3", "config4", "config5"],
+                    help="config2 (default, the bench line); config3/4/5 = outer block-Jacobi solves (supplemental)")
     return ap.parse_args()
 
 
@@ -342,10 +344,98 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
+OUTER_WORKLOADS = {
+    # BASELINE.json configs[2..4]; inner tolerances in the r0-relative basis (the
+    # literal rhs-relative reading stalls on the reference)
+    "config3": dict(block_grid=(1, 1, 8), inner=("cg", 100, 1e-3), mode="sync", tol=1e-8, overlap=0,
+                    faces=None, basis="initial", every=1),
+    "config4": dict(block_grid=(1, 1, 8), inner=("cg", 20, 0.0), mode="async", tol=1e-8, overlap=0,
+                    faces=None, basis="rhs", every=10),
+    "config5": dict(block_grid=(2, 2, 2), inner=("gmres", 30, 1e-3), mode="sync", tol=1e-8, overlap=2,
+                    faces={"z_lo": 1.0}, basis="initial", every=1),
+}
+
+
+def run_outer_workload(args):
+    """Supplemental: time-to-solution of the outer block-Jacobi configs on this
+    box (1 GPU: all blocks on one device; torchrun N>1: config3 sharded)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2009_12638_b200 as bs
+
+    w = OUTER_WORKLOADS[args.workload]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n = args.n
+    N = n ** 3
+    grid = bs.Grid3D(n, n, n, bs.DirichletBoundary(w["faces"] or {}))
+    if w["faces"]:
+        prob = bs.build_laplace_3d(grid)
+    else:
+        prob = bs.LinearProblem(bs.StencilOperator(n, n, n), np.random.default_rng(0).uniform(-1.0, 1.0, N), grid)
+    kind, its, itol = w["inner"]
+    cfg = bs.OuterConfig(block_grid=w["block_grid"], overlap=w["overlap"], inner=bs.InnerSolverSpec(kind, its, itol),
+                         mode=w["mode"], tol=w["tol"], max_outer=100000, tolerance_basis=w["basis"],
+                         residual_check_every=w["every"], execution="threads" if w["mode"] == "async" else "replay")
+    from paper_2009_12638_b200.distributed import outer_solve_distributed
+
+    def solve():
+        if world > 1:
+            return outer_solve_distributed(prob, cfg)
+        return bs.outer_solve(prob, cfg)
+
+    for _ in range(args.warmup):
+        solve()
+    times, results = [], []
+    for _ in range(args.steps):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        res = solve()
+        torch.cuda.synchronize(dev)
+        times.append(time.perf_counter() - t0)
+        results.append(res)
+    t = torch.tensor([sum(times) / len(times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tts = float(t.item())
+    res = results[-1]
+    total_its = int(sum(sum(row) for row in res.inner_iterations_per_block))
+    nb = int(np.prod(w["block_grid"]))
+    pts_its = N * total_its / nb if w["overlap"] == 0 else None
+    if w["overlap"] == 0:
+        # SURVEY §8(d): sum over sweeps and blocks of N_b (64 its_b + 64)
+        alg = sum((N / nb) * (64 * i + 64) for row in res.inner_iterations_per_block for i in row)
+    else:
+        alg = None
+    hbm = peaks()[0]
+    if rank == 0:
+        line = {"metric": METRIC + " (supplemental: " + args.workload + ")", "workload": args.workload,
+                "grid": [n, n, n], "n_gpus": world, "config": {k: (list(v) if isinstance(v, tuple) else v)
+                                                             for k, v in w.items()},
+                "time_to_solution_s": tts, "outer_sweeps": res.outer_iterations, "converged": res.converged,
+                "final_true_residual": res.final_true_residual, "inner_iterations_total": total_its,
+                "stencil_gpts_per_s": (pts_its / tts / 1e9) if pts_its else None,
+                "hbm_fraction": (alg / tts / 1e9 / (hbm * world)) if alg else None,
+                "dtype": "f64", "data": "synthetic" if not w["faces"] else "Dirichlet z_lo=1"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload != "config2":
+        run_outer_workload(args)
     else:
         run_b200(args)
 
