@@ -196,3 +196,10 @@ def test_outer_sync_matches_reference_trace(key):
     assert res.final_true_residual == pytest.approx(M["final_true_residual"], rel=1e-10)
     sol = A[key + "/solution"]
     assert np.linalg.norm(res.solution - sol) <= 1e-12 * np.linalg.norm(sol)
+
+
+def test_threaded_csr_bit_identical():
+    A = arrays()
+    a = lap((16, 16, 16))
+    x = A["spmv/16x16x16/x"]
+    assert np.array_equal(O.ThreadedCSR(a, 3)(x), A["spmv/16x16x16/y"])
