@@ -203,6 +203,12 @@ int bs_async_post(bs_ctx *ctx, int block, int dir, double *ring, uint64_t *seqs,
 int bs_async_receive(bs_ctx *ctx, int block, int ghost_dir, const double *ring, const uint64_t *seqs, int R,
                      uint64_t *applied, double *stage, int *torn, void *stream);
 
+/* the seeded rhs generated on the device, bit-identical
+ * to numpy's default_rng(seed).uniform(low, high, n) — PCG64 state/increment
+ * as numpy reports them after seeding (bit_generator.state). */
+int bs_uniform_pcg64(double *out, int64_t n, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                     uint64_t inc_lo, double low, double high, void *stream);
+
 /* Number of kernels this library has launched (process lifetime). */
 unsigned long long bs_launch_count(void);
 

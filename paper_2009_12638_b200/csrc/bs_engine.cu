@@ -1477,6 +1477,45 @@ __global__ void k_async_apply(const DBlock *__restrict__ blocks, int b, int gdir
         g[c] = stage[c];
 }
 
+// ------------------------------------------------------------------ seeded rhs on the device
+// numpy's Generator(PCG64).uniform(low, high, n) reproduced bit for bit: PCG64
+// = 128-bit LCG (state = state * M + inc) with XSL-RR output of the new state;
+// a double is (raw >> 11) * 2^-53 and the sample low + (high - low) * u.  Each
+// thread jumps ahead to its chunk (O(log n) LCG power) and steps sequentially.
+
+__device__ __forceinline__ unsigned long long pcg_xsl_rr(unsigned __int128 x) {
+    const unsigned rot = (unsigned)(x >> 122);
+    const unsigned long long v = (unsigned long long)(x >> 64) ^ (unsigned long long)x;
+    return (v >> rot) | (v << ((64u - rot) & 63u));
+}
+
+__global__ void k_pcg64_uniform(double *out, long long n, unsigned long long s_hi, unsigned long long s_lo,
+                                unsigned long long i_hi, unsigned long long i_lo, double low, double range,
+                                int chunk) {
+    const unsigned __int128 M = ((unsigned __int128)0x2360ed051fc65da4ull << 64) | 0x4385df649fccf645ull;
+    const unsigned __int128 inc = ((unsigned __int128)i_hi << 64) | i_lo;
+    unsigned __int128 st = ((unsigned __int128)s_hi << 64) | s_lo;
+    const long long start = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * chunk;
+    if (start >= n) return;
+    // jump ahead `start` steps: (A, C) <- composition of (M, inc) applied start times
+    unsigned __int128 acc_mult = 1, acc_plus = 0, cur_mult = M, cur_plus = inc;
+    for (unsigned long long d = (unsigned long long)start; d; d >>= 1) {
+        if (d & 1) {
+            acc_mult *= cur_mult;
+            acc_plus = acc_plus * cur_mult + cur_plus;
+        }
+        cur_plus = (cur_mult + 1) * cur_plus;
+        cur_mult *= cur_mult;
+    }
+    st = acc_mult * st + acc_plus;
+    const long long end = min(n, start + chunk);
+    for (long long i = start; i < end; ++i) {
+        st = st * M + inc;
+        const double u = (double)(pcg_xsl_rr(st) >> 11) * (1.0 / 9007199254740992.0);
+        out[i] = __dadd_rn(low, __dmul_rn(range, u));
+    }
+}
+
 // ------------------------------------------------------------------ host helpers
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -2161,6 +2200,19 @@ int bs_async_receive(bs_ctx *c, int block, int ghost_dir, const double *ring, co
     k_async_copy<<<64, 256, 0, st>>>(c->dblocks, block, ghost_dir, ring, n, c->dpick, stage);
     k_async_check<<<1, 1, 0, st>>>((const unsigned long long *)seqs, c->dpick, (unsigned long long *)applied, torn);
     k_async_apply<<<64, 256, 0, st>>>(c->dblocks, block, ghost_dir, n, c->dpick, stage);
+    BS_CU(cudaGetLastError());
+    return BS_OK;
+}
+
+int bs_uniform_pcg64(double *out, int64_t n, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                     uint64_t inc_lo, double low, double high, void *stream) {
+    if (!out || n < 0) return fail(BS_EINVAL, "bs_uniform_pcg64: bad arguments");
+    if (n == 0) return BS_OK;
+    const int chunk = 256;
+    const long long threads = (n + chunk - 1) / chunk;
+    ++g_launches;
+    k_pcg64_uniform<<<(unsigned)((threads + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+        out, n, state_hi, state_lo, inc_hi, inc_lo, low, high - low, chunk);
     BS_CU(cudaGetLastError());
     return BS_OK;
 }

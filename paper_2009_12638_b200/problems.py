@@ -169,9 +169,29 @@ def build_laplace_3d(grid: Grid3D) -> LinearProblem:
     return LinearProblem(StencilOperator(nx, ny, nz), rhs.ravel(), grid)
 
 
-def seeded_rhs(n: int, seed: int = 0) -> np.ndarray:
-    """Seeded rhs convention of SURVEY §8(d): uniform [-1, 1], x-fastest."""
-    return np.random.default_rng(seed).uniform(-1.0, 1.0, n)
+def seeded_rhs(n: int, seed: int = 0, device=None):
+    """Seeded rhs convention of SURVEY §8(d): uniform [-1, 1], x-fastest.
+
+    With ``device`` the values are generated on the GPU (bit-identical to
+    numpy's PCG64 stream; no host array, no upload)."""
+    if device is None:
+        return np.random.default_rng(seed).uniform(-1.0, 1.0, n)
+    import ctypes
+
+    from . import _lib
+    from .engine import require_cuda, torch
+
+    dev = require_cuda(device)
+    st = np.random.default_rng(seed).bit_generator.state["state"]
+    s, inc = int(st["state"]), int(st["inc"])
+    out = torch.empty(n, dtype=torch.float64, device=dev)
+    lib = _lib.load()
+    m64 = (1 << 64) - 1
+    with torch.cuda.device(dev):
+        stream = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+        _lib.check(lib.bs_uniform_pcg64(out.data_ptr(), n, s >> 64, s & m64, inc >> 64, inc & m64, -1.0, 1.0,
+                                        stream))
+    return out
 
 
 def _split_ranges(n: int, g: int) -> list:

@@ -397,3 +397,9 @@ def test_distributed_driver_single_rank_nccl_equals_outer_solve():
         assert np.array_equal(rd.solution, rl.solution)
     finally:
         t.distributed.destroy_process_group()
+
+
+def test_device_seeded_rhs_bit_identical_to_numpy():
+    for n, seed in ((1, 0), (1000, 3), (256 ** 3, 0)):
+        d = bs.seeded_rhs(n, seed, device="cuda").cpu().numpy()
+        assert np.array_equal(d, O.seeded_rhs(n, seed))
