@@ -1601,8 +1601,11 @@ int upload_active(bs_ctx *c, const int32_t *active, cudaStream_t st, const int *
         *dptr = nullptr;
         return BS_OK;
     }
+    // the pinned staging slot is reused by the next call: finish this copy first
+    BS_CU(cudaStreamSynchronize(st));
     std::memcpy(c->hpinned + 1, active, sizeof(int) * c->nblocks);
     BS_CU(cudaMemcpyAsync(c->dactive, c->hpinned + 1, sizeof(int) * c->nblocks, cudaMemcpyHostToDevice, st));
+    BS_CU(cudaStreamSynchronize(st));
     *dptr = c->dactive;
     return BS_OK;
 }
