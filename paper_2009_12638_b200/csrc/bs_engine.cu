@@ -602,85 +602,7 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
             ++par_n;
         }
     };
-    // Interior fast path, two planes per step: both stencil chains are
-    // independent, so they interleave (ILP 2); all shared loads are issued
-    // before any global store.  Per-point arithmetic and the per-thread
-    // accumulation order are exactly those of the one-plane step.
-    constexpr bool PAIRABLE = BOX && (OP == OP_S1 || OP == OP_S2 || OP == OP_GSPMV || OP == OP_APPLY);
     int q = 1;
-    if (PAIRABLE && warp_xy_interior) {
-        if (lz0 == 0 && q <= nplanes - 2) single_step(q++);  // pz absent on the first plane
-        for (; q + 1 <= nplanes - 2; q += 2) {
-            const int s2 = sn + 1 == NS ? 0 : sn + 1;
-            const uint32_t par2 = par_n + (sn + 1 == NS ? 1u : 0u);
-            mbar_wait(&full[sn], par_n & 1u);
-            mbar_wait(&full[s2], par2 & 1u);
-            const unsigned char *sa = smem + s * STB, *sb = smem + sn * STB, *sc = smem + s2 * STB;
-            const double u1 = val(sb, own), u2 = val(sc, own);
-            const double axm = val(sa, own - 1), axp = val(sa, own + 1);
-            const double aym = val(sa, own - SX), ayp = val(sa, own + SX);
-            const double bxm = val(sb, own - 1), bxp = val(sb, own + 1);
-            const double bym = val(sb, own - SX), byp = val(sb, own + SX);
-            const double *ca = reinterpret_cast<const double *>(sa + COFF);
-            const double *cb = reinterpret_cast<const double *>(sb + COFF);
-            double ea = 0.0, eb = 0.0, fa = 0.0, fb = 0.0;
-            if (OP == OP_S2 || (OP == OP_GSPMV && !first) || (OP == OP_S1 && pend)) {
-                ea = ca[tid];
-                eb = cb[tid];
-            }
-            if (OP == OP_S1 && pend) {
-                fa = reinterpret_cast<const double *>(sa + SEG_H)[own];
-                fb = reinterpret_cast<const double *>(sb + SEG_H)[own];
-            }
-            const double au0 = stencil7_interior(u_prev, aym, axm, u_cur, axp, ayp, u1);
-            const double au1 = stencil7_interior(u_cur, bym, bxm, u1, bxp, byp, u2);
-            const long long sx1 = sx + plane;
-            if (OP == OP_APPLY) {
-                if (col_in) {
-                    out_y[sx] = au0;
-                    out_y[sx1] = au1;
-                }
-            } else if (OP == OP_GSPMV) {
-                const double v0a = first ? u_cur : ea, v0b = first ? u1 : eb;
-                if (col_in) {
-                    out_w[sx] = au0;
-                    out_w[sx1] = au1;
-                    acc[0] = add(acc[0], mul(v0a, au0));
-                    acc[0] = add(acc[0], mul(v0b, au1));
-                }
-            } else if (OP == OP_S2) {
-                const double ra = sub(ea, mul(alpha, au0)), rb = sub(eb, mul(alpha, au1));
-                if (col_in) {
-                    out_r[sx] = ra;
-                    out_r[sx1] = rb;
-                    acc[0] = add(acc[0], mul(ra, ra));
-                    acc[0] = add(acc[0], mul(rb, rb));
-                }
-            } else {  // OP_S1
-                if (col_in) {
-                    out_p[sx] = u_cur;
-                    out_p[sx1] = u1;
-                    if (pend) {
-                        out_x[sx] = add(ea, mul(alpha_pend, fa));
-                        out_x[sx1] = add(eb, mul(alpha_pend, fb));
-                    }
-                    acc[0] = add(acc[0], mul(u_cur, au0));
-                    acc[0] = add(acc[0], mul(u1, au1));
-                }
-            }
-            sx += 2 * plane;
-            u_prev = u1;
-            u_cur = u2;
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&empty[s]);
-                mbar_arrive(&empty[sn]);
-            }
-            s = s2;
-            sn = s2 + 1 == NS ? 0 : s2 + 1;
-            par_n = par2 + (s2 + 1 == NS ? 1u : 0u);
-        }
-    }
     for (; q <= nplanes - 2; ++q) single_step(q);
 }
 
