@@ -143,6 +143,8 @@ struct DBlock {
     int overlap;
     int cta_begin, cta_end;  // CTA range in sweep launches
     int tiles_x, tiles_y, tiles_z, cz;
+    int pcta_begin, pcta_end;  // CTA range in pointwise (GMRES) launches:
+    int ptiles_z, pcz;         // same column tiles, short z-chunks (more CTAs)
     double *x, *r, *p[2];
     const double *b;
     double *ghost[BS_NDIR];
@@ -185,6 +187,8 @@ struct KParams {
     const int *cta_block;
     int nblocks;
     int nctas;
+    const int *pcta_block;  // pointwise-launch CTA table
+    int npctas;
     double *partials;
     unsigned *blk_counter;
     unsigned *launch_counter;
@@ -863,9 +867,10 @@ __device__ __forceinline__ bool serves(const DState &S, const KParams &P) {
 // Per-tile partials -> the block's last CTA reduces them in tile order and
 // advances the block's recurrence.  Every CTA then counts into the launch;
 // the launch's last CTA publishes the loop conditions.  NTH = CTA threads.
-template <int NTH, int OPK>
+template <int NTH, int OPK, bool POINT = false>
 __device__ void finish(const KParams &P, int b, int ph, bool served, double (&acc)[NQ], int nq,
                        unsigned char *smem) {
+    const int nctas = POINT ? P.npctas : P.nctas;
     const int tid = threadIdx.x;
     double *red = reinterpret_cast<double *>(smem);
     double *scratch = red + NQ * (NTH / 32);
@@ -875,18 +880,19 @@ __device__ void finish(const KParams &P, int b, int ph, bool served, double (&ac
         cta_sum<NTH>(acc, red);
         if (tid == 0) {
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) P.partials[(size_t)q * P.nctas + blockIdx.x] = acc[q];
+            for (int q = 0; q < NQ; ++q) P.partials[(size_t)q * nctas + blockIdx.x] = acc[q];
             __threadfence();
             const unsigned prev = atomicAdd(&P.blk_counter[b], 1u);
-            *flag = (prev == (unsigned)(B.cta_end - B.cta_begin) - 1u);
+            const int span = POINT ? B.pcta_end - B.pcta_begin : B.cta_end - B.cta_begin;
+            *flag = (prev == (unsigned)span - 1u);
         }
         __syncthreads();
         if (*flag) {  // last tile of block b
             __threadfence();
+            const int c0 = POINT ? B.pcta_begin : B.cta_begin, c1 = POINT ? B.pcta_end : B.cta_end;
             double q[NQ];
             for (int i = 0; i < NQ; ++i)
-                q[i] = i < nq ? range_sum<NTH>(P.partials + (size_t)i * P.nctas, B.cta_begin, B.cta_end, scratch)
-                              : 0.0;
+                q[i] = i < nq ? range_sum<NTH>(P.partials + (size_t)i * nctas, c0, c1, scratch) : 0.0;
             if (tid == 0) {
                 DState Sn = P.states[b];
                 transition(B, Sn, P.gstates ? P.gstates + b : nullptr, ph, q);
@@ -900,7 +906,7 @@ __device__ void finish(const KParams &P, int b, int ph, bool served, double (&ac
     if (tid == 0) {
         __threadfence();
         const unsigned prev = atomicAdd(P.launch_counter, 1u);
-        *flag = (prev == (unsigned)P.nctas - 1u);
+        *flag = (prev == (unsigned)nctas - 1u);
     }
     __syncthreads();
     if (!*flag || tid != 0) return;
@@ -990,7 +996,7 @@ __global__ void __launch_bounds__(NTHR, BS_MINBLOCKS) k_sweep(const KParams P) {
 template <int PKK, bool BOX>
 __global__ void __launch_bounds__(NT) k_point(const KParams P) {
     extern __shared__ __align__(1024) unsigned char smem[];
-    const int b = P.cta_block[blockIdx.x];
+    const int b = P.pcta_block[blockIdx.x];
     const DBlock &B = P.blocks[b];
     const DState S = P.states[b];
     const int ph = S.phase;
@@ -999,13 +1005,13 @@ __global__ void __launch_bounds__(NT) k_point(const KParams P) {
     if (served) {
         const GState &G = P.gstates[b];
         const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
-        int t = blockIdx.x - B.cta_begin;
+        int t = blockIdx.x - B.pcta_begin;
         const int ix = t % B.tiles_x;
         t /= B.tiles_x;
         const int iy = t % B.tiles_y;
         const int iz = t / B.tiles_y;
         const int lx = ix * TX + tx, ly = iy * TY + ty;
-        const int lz0 = iz * B.cz, lz1 = min(lz0 + B.cz, B.pdim[2]);
+        const int lz0 = iz * B.pcz, lz1 = min(lz0 + B.pcz, B.pdim[2]);
         const bool col_in = lx < B.pdim[0] && ly < B.pdim[1];
         const int gi = B.plo[0] + lx, gj = B.plo[1] + ly;
         const long long plane = (long long)B.pitch * B.pdim[1];
@@ -1092,7 +1098,7 @@ __global__ void __launch_bounds__(NT) k_point(const KParams P) {
             }
         }
     }
-    finish<NT, -1>(P, b, ph, served, acc, PKK == PK_OWNRES ? NQ : 1, smem);
+    finish<NT, -1, true>(P, b, ph, served, acc, PKK == PK_OWNRES ? NQ : 1, smem);
 }
 
 // ---- overlapping merge (multisplit.py:341-369), overlap > 0.  Inputs are the
@@ -1484,6 +1490,8 @@ struct bs_ctx {
     DState *dstates = nullptr;
     CUtensorMap *dtmaps = nullptr;
     int *dcta_block = nullptr;
+    int *dpcta_block = nullptr;
+    int npctas = 0;
     double *dpartials = nullptr;
     unsigned *dblk_counter = nullptr;
     unsigned *dlaunch_counter = nullptr;
@@ -1541,6 +1549,8 @@ KParams make_params(bs_ctx *c, bool graph, cudaGraphConditionalHandle hl = 0,
     P.cta_block = c->dcta_block;
     P.nblocks = c->nblocks;
     P.nctas = c->nctas;
+    P.pcta_block = c->dpcta_block;
+    P.npctas = c->npctas;
     P.partials = c->dpartials;
     P.blk_counter = c->dblk_counter;
     P.launch_counter = c->dlaunch_counter;
@@ -1563,9 +1573,9 @@ void launch_point(bs_ctx *c, cudaStream_t st, int j, int i) {
     P.launch_i = i;
     constexpr int smem = (NQ * (NT / 32) + 256 + 8) * 8;
     if (c->box)
-        k_point<PKK, true><<<c->nctas, NT, smem, st>>>(P);
+        k_point<PKK, true><<<c->npctas, NT, smem, st>>>(P);
     else
-        k_point<PKK, false><<<c->nctas, NT, smem, st>>>(P);
+        k_point<PKK, false><<<c->npctas, NT, smem, st>>>(P);
     ++g_launches;
 }
 
@@ -1767,6 +1777,20 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
         }
         c->hblocks.push_back(B);
     }
+    // pointwise table: same column tiles, 16-plane z-chunks (streaming kernels
+    // want many CTAs in flight; each CTA still owns a fixed tile, so per-block
+    // reductions stay independent of the co-resident blocks)
+    std::vector<int> pcta_block;
+    for (int b = 0; b < nblocks; ++b) {
+        DBlock &B = c->hblocks[b];
+        B.pcz = std::min(16, B.pdim[2]);
+        B.ptiles_z = (B.pdim[2] + B.pcz - 1) / B.pcz;
+        B.pcta_begin = (int)pcta_block.size();
+        const long long ntile = (long long)B.tiles_x * B.tiles_y * B.ptiles_z;
+        for (long long t = 0; t < ntile; ++t) pcta_block.push_back(b);
+        B.pcta_end = (int)pcta_block.size();
+    }
+    c->npctas = (int)pcta_block.size();
     // neighbour lists (problems.py:343-349): extended regions within one stencil
     // step, i.e. L1 gap between owned boxes <= 2o+1; ascending block ids
     for (int a = 0; a < nblocks; ++a) {
@@ -1793,7 +1817,10 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
     if (e == cudaSuccess) e = cudaMalloc(&c->dstates, sizeof(DState) * nblocks);
     if (e == cudaSuccess) e = cudaMalloc(&c->dtmaps, sizeof(CUtensorMap) * maps.size());
     if (e == cudaSuccess) e = cudaMalloc(&c->dcta_block, sizeof(int) * c->nctas);
-    if (e == cudaSuccess) e = cudaMalloc(&c->dpartials, sizeof(double) * NQ * c->nctas);
+    if (e == cudaSuccess) e = cudaMalloc(&c->dpartials, sizeof(double) * NQ * std::max(c->nctas, c->npctas));
+    if (e == cudaSuccess) e = cudaMalloc(&c->dpcta_block, sizeof(int) * c->npctas);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(c->dpcta_block, pcta_block.data(), sizeof(int) * c->npctas, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&c->dblk_counter, sizeof(unsigned) * nblocks);
     if (e == cudaSuccess) e = cudaMalloc(&c->dlaunch_counter, sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMalloc(&c->dnactive, sizeof(int));
@@ -1841,6 +1868,7 @@ int bs_ctx_destroy(bs_ctx *c) {
     cudaFree(c->dstates);
     cudaFree(c->dtmaps);
     cudaFree(c->dcta_block);
+    cudaFree(c->dpcta_block);
     cudaFree(c->dpartials);
     cudaFree(c->dblk_counter);
     cudaFree(c->dlaunch_counter);
