@@ -118,6 +118,7 @@ enum Pk : int { PK_NORM = 0, PK_MGS = 1, PK_FINAL = 2, PK_FORM = 3, PK_OWNRES = 
 
 constexpr int MAXM = 64;    // largest supported GMRES restart length
 constexpr int MAXNBR = 32;  // neighbour list capacity per block (overlapping merge)
+constexpr int PCHUNK = 4096; // doubles per CTA in pointwise passes
 enum GFlag : int { GF_NONE = 0, GF_HAPPY = 1, GF_CHECK = 2, GF_CYCLE = 3 };
 
 // Stage layout per op: [A haloed][B haloed, if the op has one][C bare tile].
@@ -143,8 +144,8 @@ struct DBlock {
     int overlap;
     int cta_begin, cta_end;  // CTA range in sweep launches
     int tiles_x, tiles_y, tiles_z, cz;
-    int pcta_begin, pcta_end;  // CTA range in pointwise (GMRES) launches:
-    int ptiles_z, pcz;         // same column tiles, short z-chunks (more CTAs)
+    int pcta_begin, pcta_end;  // CTA range in pointwise (GMRES) launches: fixed
+                               // PCHUNK-element chunks of the pitched box
     double *x, *r, *p[2];
     const double *b;
     double *ghost[BS_NDIR];
@@ -1003,61 +1004,72 @@ __global__ void __launch_bounds__(NT) k_point(const KParams P) {
     const bool served = serves<-1, PKK>(S, P);
     double acc[NQ] = {0.0, 0.0, 0.0, 0.0};
     if (served) {
+        // flat, contiguous chunk of the block's pitched padded box: each thread
+        // takes element pairs (16-byte loads) at a fixed stride, so the CTA
+        // streams PCHUNK consecutive doubles.  Cells outside the region (and
+        // the row padding) hold exact zeros in r, W and V, so MGS / FINAL /
+        // NORM need no mask; FORM and OWNRES test the region explicitly.
         const GState &G = P.gstates[b];
-        const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
-        int t = blockIdx.x - B.pcta_begin;
-        const int ix = t % B.tiles_x;
-        t /= B.tiles_x;
-        const int iy = t % B.tiles_y;
-        const int iz = t / B.tiles_y;
-        const int lx = ix * TX + tx, ly = iy * TY + ty;
-        const int lz0 = iz * B.pcz, lz1 = min(lz0 + B.pcz, B.pdim[2]);
-        const bool col_in = lx < B.pdim[0] && ly < B.pdim[1];
-        const int gi = B.plo[0] + lx, gj = B.plo[1] + ly;
-        const long long plane = (long long)B.pitch * B.pdim[1];
-        long long sx = (long long)lx + (long long)B.pitch * ((long long)ly + (long long)B.pdim[1] * lz0);
+        const int tid = threadIdx.x;
+        const long long n = (long long)B.pitch * B.pdim[1] * B.pdim[2];
+        const long long base = (long long)(blockIdx.x - B.pcta_begin) * PCHUNK;
         const int j = S.gj, i = S.gi;
         const long long vs = B.vstride;
-        double *W = B.W;
-        const double *V = B.V;
-        if (col_in) {
-            if (PKK == PK_NORM) {  // v_j = src / nrm (inner_solvers.py:164, 237)
-                const double *src = j == 0 ? B.r : W;
-                double *vj = B.V + j * vs;
-                const double nrm = S.gnrm;
-                for (int lz = lz0; lz < lz1; ++lz, sx += plane)
-                    if (BOX || in_region(B, gi, gj, B.plo[2] + lz)) vj[sx] = __ddiv_rn(src[sx], nrm);
-            } else if (PKK == PK_MGS) {  // w -= h_{i-1,j} v_{i-1} ; h_ij = v_i . w (189-193)
-                const double h = G.H[(i - 1) * MAXM + j];
-                const double *va = V + (i - 1) * vs, *vb = V + i * vs;
+        double *__restrict__ W = B.W;
+        const double *__restrict__ V = B.V;
+        if (PKK == PK_NORM) {  // v_j = src / nrm (inner_solvers.py:164, 237)
+            const double2 *src = reinterpret_cast<const double2 *>(j == 0 ? B.r : W);
+            double2 *vj = reinterpret_cast<double2 *>(B.V + j * vs);
+            const double nrm = S.gnrm;
 #pragma unroll 4
-                for (int lz = lz0; lz < lz1; ++lz) {
-                    const long long q = sx + (long long)(lz - lz0) * plane;
-                    if (BOX || in_region(B, gi, gj, B.plo[2] + lz)) {
-                        const double w = sub(W[q], mul(h, va[q]));
-                        W[q] = w;
-                        acc[0] = add(acc[0], mul(vb[q], w));
-                    }
-                }
-            } else if (PKK == PK_FINAL) {  // w -= h_jj v_j ; ||w||^2 (193-195)
-                const double h = G.H[j * MAXM + j];
-                const double *vj = V + j * vs;
+            for (int it = 0; it < PCHUNK / (2 * NT); ++it) {
+                const long long e = base + 2LL * (it * NT + tid);
+                if (e >= n) break;
+                const double2 v = src[e / 2];
+                vj[e / 2] = make_double2(__ddiv_rn(v.x, nrm), __ddiv_rn(v.y, nrm));
+            }
+        } else if (PKK == PK_MGS || PKK == PK_FINAL) {
+            // MGS:   w -= h_{i-1,j} v_{i-1} ; h_ij = v_i . w   (inner_solvers.py:189-193)
+            // FINAL: w -= h_jj v_j ; ||w||^2                    (193-195)
+            const double h = PKK == PK_MGS ? G.H[(i - 1) * MAXM + j] : G.H[j * MAXM + j];
+            const double2 *va = reinterpret_cast<const double2 *>(V + (PKK == PK_MGS ? i - 1 : j) * vs);
+            const double2 *vb = reinterpret_cast<const double2 *>(V + i * vs);
+            double2 *w2 = reinterpret_cast<double2 *>(W);
 #pragma unroll 4
-                for (int lz = lz0; lz < lz1; ++lz) {
-                    const long long q = sx + (long long)(lz - lz0) * plane;
-                    if (BOX || in_region(B, gi, gj, B.plo[2] + lz)) {
-                        const double w = sub(W[q], mul(h, vj[q]));
-                        W[q] = w;
-                        acc[0] = add(acc[0], mul(w, w));
-                    }
+            for (int it = 0; it < PCHUNK / (2 * NT); ++it) {
+                const long long e = base + 2LL * (it * NT + tid);
+                if (e >= n) break;
+                const double2 w = w2[e / 2], a = va[e / 2];
+                const double w0 = sub(w.x, mul(h, a.x)), w1 = sub(w.y, mul(h, a.y));
+                w2[e / 2] = make_double2(w0, w1);
+                if (PKK == PK_MGS) {
+                    const double2 c = vb[e / 2];
+                    acc[0] = add(acc[0], mul(c.x, w0));
+                    acc[0] = add(acc[0], mul(c.y, w1));
+                } else {
+                    acc[0] = add(acc[0], mul(w0, w0));
+                    acc[0] = add(acc[0], mul(w1, w1));
                 }
-            } else if (PKK == PK_OWNRES) {
-                // Local residual with owner-canonical values (multisplit.py:372-396): on
-                // owned rows every stencil neighbour is a region point (o >= 1), so this
-                // is b - A x_gathered, x_gathered[p] = owner's post-solve value
-                // (snapshot in each block's r).  acc[2] = acc[3] = ||r_owned||^2.
-                for (int lz = lz0; lz < lz1; ++lz, sx += plane) {
-                    const int gk = B.plo[2] + lz;
+            }
+        } else {
+            const int pitch = B.pitch, pdx = B.pdim[0], pdy = B.pdim[1];
+            for (int it = 0; it < PCHUNK / NT; ++it) {
+                const long long e = base + (long long)it * NT + tid;
+                if (e >= n) break;
+                const int lx = (int)(e % pitch);
+                if (lx >= pdx) continue;
+                const long long t2 = e / pitch;
+                const int gi = B.plo[0] + lx, gj = B.plo[1] + (int)(t2 % pdy), gk = B.plo[2] + (int)(t2 / pdy);
+                if (PKK == PK_FORM) {  // x = x + V[:j+1]^T y (inner_solvers.py:173-175)
+                    if (!BOX && !in_region(B, gi, gj, gk)) continue;
+                    double acc_t = mul(V[e], G.y[0]);
+                    for (int k = 1; k <= j; ++k) acc_t = add(acc_t, mul(V[k * vs + e], G.y[k]));
+                    B.x[e] = add(B.x[e], acc_t);
+                } else {  // PK_OWNRES
+                    // Local residual with owner-canonical values (multisplit.py:372-396):
+                    // on owned rows every stencil neighbour is a region point (o >= 1),
+                    // so this is b - A x_gathered with x_gathered = each owner's
+                    // post-solve value (the snapshot in its r).  acc[2] = acc[3].
                     if (!in_owned(B, gi, gj, gk)) continue;
                     const int ni[6] = {gi, gi, gi - 1, gi + 1, gi, gi};
                     const int nj[6] = {gj, gj - 1, gj, gj, gj + 1, gj};
@@ -1081,19 +1093,11 @@ __global__ void __launch_bounds__(NT) k_point(const KParams P) {
                             }
                         }
                     }
-                    const double ag = stencil7(v[0], v[1], v[2], B.r[sx], v[3], v[4], v[5], pg[0], pg[1], pg[2]);
-                    const double rg = sub(B.b[sx], ag);
+                    const double ag = stencil7(v[0], v[1], v[2], B.r[e], v[3], v[4], v[5], pg[0], pg[1], pg[2]);
+                    const double rg = sub(B.b[e], ag);
                     const double r2 = mul(rg, rg);
                     acc[2] = add(acc[2], r2);
                     acc[3] = add(acc[3], r2);
-                }
-            } else {  // PK_FORM: x = x + V[:j+1]^T y (inner_solvers.py:173-175)
-                for (int lz = lz0; lz < lz1; ++lz, sx += plane) {
-                    if (BOX || in_region(B, gi, gj, B.plo[2] + lz)) {
-                        double acc_t = mul(V[sx], G.y[0]);
-                        for (int k = 1; k <= j; ++k) acc_t = add(acc_t, mul(V[k * vs + sx], G.y[k]));
-                        B.x[sx] = add(B.x[sx], acc_t);
-                    }
                 }
             }
         }
@@ -1106,11 +1110,19 @@ __global__ void __launch_bounds__(NT) k_point(const KParams P) {
 // written into x (shared points; coupled halo cells inside the padded box) and
 // the face planes (coupled cells just outside it).
 
+// r := x on region cells, 0 elsewhere (non-region cells of x hold halo values;
+// r, W and V must stay zero off the region for the unmasked pointwise passes)
 __global__ void k_snapshot(const DBlock *__restrict__ blocks) {
     const DBlock &B = blocks[blockIdx.y];
     const long long n = (long long)B.pitch * B.pdim[1] * B.pdim[2];
-    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += (long long)gridDim.x * blockDim.x)
-        B.r[c] = B.x[c];
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < n;
+         c += (long long)gridDim.x * blockDim.x) {
+        const int lx = (int)(c % B.pitch);
+        const long long t = c / B.pitch;
+        const bool in = lx < B.pdim[0] && in_region(B, B.plo[0] + lx, B.plo[1] + (int)(t % B.pdim[1]),
+                                                    B.plo[2] + (int)(t / B.pdim[1]));
+        B.r[c] = in ? B.x[c] : 0.0;
+    }
 }
 
 // (own? + sum over covering neighbours in ascending id order) / cover count
@@ -1777,17 +1789,16 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
         }
         c->hblocks.push_back(B);
     }
-    // pointwise table: same column tiles, 16-plane z-chunks (streaming kernels
-    // want many CTAs in flight; each CTA still owns a fixed tile, so per-block
-    // reductions stay independent of the co-resident blocks)
+    // pointwise table: fixed contiguous chunks of each block (streaming kernels
+    // want many CTAs and long contiguous runs; the chunk -> CTA map is a
+    // function of the block alone, so per-block reductions stay independent of
+    // the co-resident blocks)
     std::vector<int> pcta_block;
     for (int b = 0; b < nblocks; ++b) {
         DBlock &B = c->hblocks[b];
-        B.pcz = std::min(16, B.pdim[2]);
-        B.ptiles_z = (B.pdim[2] + B.pcz - 1) / B.pcz;
+        const long long n = (long long)B.pitch * B.pdim[1] * B.pdim[2];
         B.pcta_begin = (int)pcta_block.size();
-        const long long ntile = (long long)B.tiles_x * B.tiles_y * B.ptiles_z;
-        for (long long t = 0; t < ntile; ++t) pcta_block.push_back(b);
+        for (long long t = 0; t < (n + PCHUNK - 1) / PCHUNK; ++t) pcta_block.push_back(b);
         B.pcta_end = (int)pcta_block.size();
     }
     c->npctas = (int)pcta_block.size();
