@@ -1,0 +1,110 @@
+"""Host-side API parity with the reference (CPU): validation messages, error
+types, decomposition geometry vs the oracle, trace CSV round trip, combiner."""
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_2009_12638_b200 as bs
+from oracle import blocksolve_oracle as O
+
+
+def test_spec_validation():
+    # inner_solvers.py:49-57
+    with pytest.raises(ValueError):
+        bs.InnerSolverSpec("sor", 10)
+    with pytest.raises(ValueError):
+        bs.InnerSolverSpec("cg", 0)
+    with pytest.raises(ValueError):
+        bs.InnerSolverSpec("cg", 10, tolerance=-1.0)
+    with pytest.raises(ValueError):
+        bs.InnerSolverSpec("gmres", 10, restart=0)
+
+
+@pytest.mark.parametrize("kwargs,field", [
+    (dict(mode="warp"), "mode"), (dict(tol=0.0), "tol"), (dict(max_outer=0), "max_outer"),
+    (dict(residual_check_mode="x"), "residual_mode"), (dict(execution="gpu"), "exec"),
+    (dict(execution="threads", residual_check_mode="true"), "exec"), (dict(true_residual_interval=0), "true_res_every"),
+    (dict(tolerance_basis="r0"), "tolerance_basis"), (dict(residual_check_every=0), "residual_check_every"),
+])
+def test_outer_config_validation_names_the_field(kwargs, field):
+    # multisplit.py:83-103: ConfigurationError (a ValueError) naming the field
+    with pytest.raises(bs.ConfigurationError, match=field):
+        bs.OuterConfig(**kwargs)
+
+
+def test_errors_taxonomy():
+    assert issubclass(bs.ConfigurationError, ValueError)
+    assert issubclass(bs.ProtocolError, RuntimeError)
+    e = bs.SolverBreakdownError(3, 7, "cg reported breakdown")
+    assert e.block_id == 3 and e.outer_iteration == 7 and "block 3" in str(e)
+
+
+def test_boundary_and_grid_validation():
+    with pytest.raises(bs.ConfigurationError, match="boundary"):
+        bs.DirichletBoundary({"w_lo": 1.0})
+    with pytest.raises(bs.ConfigurationError, match="nx"):
+        bs.Grid3D(0, 1, 1)
+
+
+@pytest.mark.parametrize("shape,bg,ov", [((8, 8, 8), (2, 2, 2), 2), ((9, 7, 6), (2, 1, 3), 1), ((13, 11, 9), (2, 3, 2), 1),
+                                         ((16, 16, 16), (1, 1, 4), 0), ((6, 6, 6), (3, 2, 1), 0)])
+def test_analytic_decomposition_equals_oracle_masks(shape, bg, ov):
+    """problems.py:287-359 via full-grid masks (oracle) == analytic geometry."""
+    dec = bs.decompose(bs.Grid3D(*shape), bg, ov)
+    boxes, wss, nbrs, cover = O.build_workspaces(shape, np.zeros(np.prod(shape)), bg, ov)
+    assert [(b.lo, b.hi) for b in dec.owned] == [tuple(map(tuple, b)) for b in boxes]
+    assert dec.neighbors == nbrs
+    for blk in range(dec.num_blocks):
+        assert np.array_equal(dec.extended_indices(blk), wss[blk].ext)
+        assert np.array_equal(dec.owned_indices(blk), wss[blk].owned_global)
+
+
+def test_decompose_preconditions():
+    with pytest.raises(bs.ConfigurationError, match="gx"):
+        bs.decompose(bs.Grid3D(4, 4, 4), (5, 1, 1))
+    with pytest.raises(bs.ConfigurationError, match="overlap"):
+        bs.decompose(bs.Grid3D(4, 4, 4), (2, 1, 1), 2)
+    with pytest.raises(bs.ConfigurationError, match="overlap"):
+        bs.decompose(bs.Grid3D(4, 4, 4), (1, 1, 1), -1)
+
+
+def test_build_laplace_rhs_bitwise_vs_oracle():
+    faces = {"x_lo": 1.0, "y_hi": 0.5, "z_lo": 2.0, "x_hi": -0.25}
+    p = bs.build_laplace_3d(bs.Grid3D(5, 4, 3, bs.DirichletBoundary(faces)))
+    assert np.array_equal(p.rhs, O.dirichlet_rhs(5, 4, 3, faces))
+    assert p.matrix.nnz == O.laplace_csr(5, 4, 3).values.shape[0]
+
+
+def test_combiner_and_termination():
+    # multisplit.py:399-426
+    assert bs.combined_residual([3.0, 4.0]) == 5.0 and bs.combined_residual([]) == 0.0
+    assert bs.check_termination(5e-7, 1e-6, 10, 100, "sync") == "stop"
+    assert bs.check_termination(1.0, 1e-6, 100, 100, "async") == "stop"
+    assert bs.check_termination(5e-7, 1e-6, 10, 100, "async") == "confirm"
+    assert bs.check_termination(1e-3, 1e-6, 10, 100, "sync") == "continue"
+
+
+def test_trace_csv_round_trip(tmp_path):
+    rows = [bs.TraceRow(0, 0.0, 0.5, 0.25, 10, 0), bs.TraceRow(1, 1.0, 1e-7, None, 8, 2)]
+    tr = bs.ResidualTrace(rows)
+    path = tmp_path / "t.csv"
+    tr.write_csv(path)
+    assert path.read_text().splitlines()[0] == bs.TRACE_HEADER
+    assert bs.ResidualTrace.read_csv(path) == tr
+    bad = tmp_path / "bad.csv"
+    bad.write_text("time,residual\n0,1\n")
+    with pytest.raises(ValueError, match="bad.csv"):
+        bs.ResidualTrace.read_csv(bad)
+
+
+def test_no_cpu_fallback():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(bs.DeviceError):
+        bs.spmv(bs.StencilOperator(4, 4, 4), np.ones(64))
+    with pytest.raises(bs.DeviceError):
+        bs.cg_solve(bs.StencilOperator(4, 4, 4), np.ones(64), np.zeros(64), bs.InnerSolverSpec("cg", 5))
