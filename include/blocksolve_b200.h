@@ -203,6 +203,16 @@ int bs_async_post(bs_ctx *ctx, int block, int dir, double *ring, uint64_t *seqs,
 int bs_async_receive(bs_ctx *ctx, int block, int ghost_dir, const double *ring, const uint64_t *seqs, int R,
                      uint64_t *applied, double *stage, int *torn, void *stream);
 
+/* Peer memory for one-sided halo puts across processes (one process per GPU,
+ * NVLink): export a device pointer as a 64-byte CUDA IPC handle of its
+ * allocation plus the offset inside it; open it in another process (peer
+ * access enabled lazily) to get a pointer that bs_async_post / the halo puts
+ * can store into directly.  bs_ipc_close takes the base returned by
+ * bs_ipc_open minus the offset. */
+int bs_ipc_export(const void *ptr, unsigned char *handle_out /* 64 bytes */, uint64_t *offset_out);
+int bs_ipc_open(const unsigned char *handle /* 64 bytes */, uint64_t offset, void **ptr_out);
+int bs_ipc_close(void *base);
+
 /* the seeded rhs generated on the device, bit-identical
  * to numpy's default_rng(seed).uniform(low, high, n) — PCG64 state/increment
  * as numpy reports them after seeding (bit_generator.state). */

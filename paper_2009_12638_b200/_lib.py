@@ -76,6 +76,9 @@ _SIGS = {
     "bs_read_reports": ([_P, ctypes.POINTER(BlockReport), _P], _I),
     "bs_launch_count": ([], ctypes.c_ulonglong),
     "bs_overlap_merge": ([_P, _P], _I),
+    "bs_ipc_export": ([_P, _P, ctypes.POINTER(ctypes.c_uint64)], _I),
+    "bs_ipc_open": ([_P, ctypes.c_uint64, ctypes.POINTER(_P)], _I),
+    "bs_ipc_close": ([_P], _I),
     "bs_uniform_pcg64": ([_P, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                           ctypes.c_double, ctypes.c_double, _P], _I),
     "bs_async_post": ([_P, _I, _I, _P, _P, _I, ctypes.c_uint64, _P], _I),

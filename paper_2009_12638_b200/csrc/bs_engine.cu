@@ -2181,6 +2181,42 @@ int bs_uniform_pcg64(double *out, int64_t n, uint64_t state_hi, uint64_t state_l
     return BS_OK;
 }
 
+int bs_ipc_export(const void *ptr, unsigned char *handle_out, uint64_t *offset_out) {
+    if (!ptr || !handle_out || !offset_out) return fail(BS_EINVAL, "bs_ipc_export: bad arguments");
+    static PFN_cuMemGetAddressRange_v3020 range_fn = nullptr;
+    if (!range_fn) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+            return fail(BS_ECUDA, "cuMemGetAddressRange unavailable from the driver");
+        range_fn = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn);
+    }
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range_fn(&base, &size, (CUdeviceptr)ptr) != CUDA_SUCCESS) return fail(BS_ECUDA, "bs_ipc_export: not a device allocation");
+    cudaIpcMemHandle_t h;
+    BS_CU(cudaIpcGetMemHandle(&h, (void *)base));
+    std::memcpy(handle_out, &h, sizeof(h));
+    *offset_out = (uint64_t)((CUdeviceptr)ptr - base);
+    return BS_OK;
+}
+
+int bs_ipc_open(const unsigned char *handle, uint64_t offset, void **ptr_out) {
+    if (!handle || !ptr_out) return fail(BS_EINVAL, "bs_ipc_open: bad arguments");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    void *base = nullptr;
+    BS_CU(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    *ptr_out = (unsigned char *)base + offset;
+    return BS_OK;
+}
+
+int bs_ipc_close(void *base) {
+    if (!base) return BS_OK;
+    BS_CU(cudaIpcCloseMemHandle(base));
+    return BS_OK;
+}
+
 int bs_flush(bs_ctx *c, void *stream) {
     if (!c) return fail(BS_EINVAL, "bs_flush: null context");
     if (int e = set_dev(c)) return e;

@@ -55,12 +55,25 @@ def rank_of_block(nblocks: int, world: int) -> list:
 
 
 class HaloExchange:
-    """Routing of the overlap-0 halo plan across ranks."""
+    """Routing of the overlap-0 halo plan across ranks.
 
-    def __init__(self, eng, plan: np.ndarray, local_ids: list, owner: list, rank: int, group=None):
+    transport "nccl": the boundary plane is packed into a send buffer and moved
+    by one batched NCCL isend/irecv into the neighbour's halo plane.
+    transport "p2p": every rank exports its halo planes as CUDA IPC handles
+    once; each sweep the sender's pack kernel stores its boundary plane
+    straight into the peer's halo plane over NVLink (one-sided put, no
+    staging copy), bracketed by two host barriers (nobody reads a halo plane
+    while it is overwritten; every put landed before the next residual sweep).
+    """
+
+    def __init__(self, eng, plan: np.ndarray, local_ids: list, owner: list, rank: int, group=None,
+                 transport: str = "nccl"):
+        if transport not in ("nccl", "p2p"):
+            raise ConfigurationError(f"transport: unknown halo transport {transport!r}")
         self.eng = eng
         self.group = group
         self.rank = rank
+        self.transport = transport
         loc = {g: i for i, g in enumerate(local_ids)}
         self.local_plan = np.asarray([(loc[d], dr, loc[s]) for d, dr, s in plan.tolist()
                                       if owner[d] == rank and owner[s] == rank], dtype=np.int32).reshape(-1, 3)
@@ -71,20 +84,67 @@ class HaloExchange:
             elif owner[s] == rank and owner[d] != rank:
                 li = loc[s]
                 ghost_len = eng.plane_len(li, 5 - dr)
-                buf = eng.new_plane(ghost_len)
-                self.ops.append(("send", owner[d], li, 5 - dr, buf))
+                buf = eng.new_plane(ghost_len) if transport == "nccl" else None
+                self.ops.append(("send", owner[d], li, 5 - dr, buf, (d, dr)))
+        self.ops = [op if len(op) == 6 else op + (None,) for op in self.ops]
+        self._opened = []
+        if transport == "p2p":
+            self._open_peer_planes(plan, owner, local_ids)
+
+    def _open_peer_planes(self, plan, owner, local_ids):
+        import ctypes
+
+        lib = _lib.load()
+        loc = {g: i for i, g in enumerate(local_ids)}
+        mine = {}
+        for d, dr, s in plan.tolist():
+            if owner[d] == self.rank and owner[s] != self.rank:
+                handle = (ctypes.c_ubyte * 64)()
+                off = ctypes.c_uint64(0)
+                _lib.check(lib.bs_ipc_export(ctypes.c_void_p(self.eng.ghost(loc[d], dr).data_ptr()), handle,
+                                             ctypes.byref(off)))
+                mine[(d, dr)] = (bytes(handle), off.value)
+        gathered = [None] * torch.distributed.get_world_size(self.group)
+        torch.distributed.all_gather_object(gathered, mine, group=self.group)
+        table = {k: v for part in gathered for k, v in part.items()}
+        ops = []
+        for kind, peer, li, dr, buf, key in self.ops:
+            if kind == "send":
+                handle, off = table[key]
+                ptr = ctypes.c_void_p()
+                _lib.check(lib.bs_ipc_open((ctypes.c_ubyte * 64).from_buffer_copy(handle), off, ctypes.byref(ptr)))
+                self._opened.append(ptr.value - off)
+                buf = ptr.value  # the peer's halo plane itself
+            ops.append((kind, peer, li, dr, buf, key))
+        self.ops = ops
+
+    def close(self) -> None:
+        if self._opened:
+            lib = _lib.load()
+            for base in self._opened:
+                lib.bs_ipc_close(base)
+            self._opened = []
 
     def __call__(self) -> None:
         if self.local_plan.size:
             self.eng.halo_pack(self.local_plan)
         if not self.ops:
             return
-        for kind, peer, li, dr, buf in self.ops:
+        if self.transport == "p2p":
+            self.eng.synchronize()
+            torch.distributed.barrier(group=self.group)  # every rank is done reading its halo planes
+            for kind, peer, li, dr, ptr, key in self.ops:
+                if kind == "send":
+                    self.eng.post_plane_ptr(li, dr, ptr)
+            self.eng.synchronize()
+            torch.distributed.barrier(group=self.group)  # every put has landed
+            return
+        for kind, peer, li, dr, buf, key in self.ops:
             if kind == "send":
                 self.eng.post_plane(li, dr, buf)
         self.eng.synchronize()
         p2p = []
-        for kind, peer, li, dr, buf in self.ops:
+        for kind, peer, li, dr, buf, key in self.ops:
             if kind == "send":
                 p2p.append(torch.distributed.P2POp(torch.distributed.isend, buf, peer, self.group))
             else:
@@ -101,7 +161,7 @@ def _default_factory(grid_shape, owned, overlap, local_ids):
 
 
 def outer_solve_distributed(problem: LinearProblem, config: OuterConfig, group=None,
-                            engine_factory=None) -> SolveResult:
+                            engine_factory=None, transport: str = "nccl") -> SolveResult:
     """Sharded synchronous two-stage solve; every rank returns the same result
     (solution gathered on every rank)."""
     dist = torch.distributed
@@ -129,10 +189,13 @@ def outer_solve_distributed(problem: LinearProblem, config: OuterConfig, group=N
     factory = engine_factory or _default_factory
     eng = factory(grid.shape, [decomp.owned[g] for g in local_ids], config.overlap, local_ids)
     eng.load_host("b", b3)
-    exchange = HaloExchange(eng, box_halo_plan(decomp.owned, decomp.block_grid), local_ids, owner, rank, group)
+    exchange = HaloExchange(eng, box_halo_plan(decomp.owned, decomp.block_grid), local_ids, owner, rank, group,
+                            transport)
+    host_comm = dist.get_backend(group) == "gloo"
+    comm_dev = torch.device("cpu") if host_comm else eng.comm_device
 
     def allreduce_rows(table: np.ndarray) -> np.ndarray:
-        t = torch.from_numpy(table).to(eng.comm_device)
+        t = torch.from_numpy(table).to(comm_dev)
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
         return t.cpu().numpy()
 
@@ -143,8 +206,10 @@ def outer_solve_distributed(problem: LinearProblem, config: OuterConfig, group=N
         eng.flush()
         sol = torch.zeros(nz, ny, nx, dtype=torch.float64, device=eng.comm_device)
         eng.gather_owned(sol)
+        sol = sol.to(comm_dev)
         dist.all_reduce(sol, op=dist.ReduceOp.SUM, group=group)  # disjoint owned boxes: exact
     finally:
+        exchange.close()
         eng.close()
     rows = [TraceRow(k, t, est, tr, inner, 0) for k, t, est, tr, inner in trace]
     if rows and rows[-1].true_residual is None:

@@ -205,6 +205,14 @@ class BlockEngine:
         _lib.check(self.lib.bs_async_post(self.ctx, block, direction, buf.data_ptr(), self._seq1.data_ptr(), 1, 0,
                                           self.stream))
 
+    def post_plane_ptr(self, block: int, direction: int, dst_ptr: int) -> None:
+        """Block's boundary plane facing `direction` stored at a raw (possibly
+        peer-mapped) device address."""
+        if not hasattr(self, "_seq1"):
+            self._seq1 = torch.zeros(1, dtype=torch.int64, device=self.device)
+        _lib.check(self.lib.bs_async_post(self.ctx, block, direction, ctypes.c_void_p(dst_ptr),
+                                          self._seq1.data_ptr(), 1, 0, self.stream))
+
     def synchronize(self) -> None:
         torch.cuda.current_stream(self.device).synchronize()
 

@@ -134,5 +134,8 @@ class FakeEngine:
     def post_plane(self, block, direction, buf):
         buf.copy_(torch.from_numpy(self.blocks[block].plane(direction)))
 
+    def post_plane_ptr(self, block, direction, ptr):
+        raise NotImplementedError("the CPU stand-in has no device pointers")
+
     def synchronize(self):
         pass

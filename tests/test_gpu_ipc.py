@@ -1,0 +1,71 @@
+"""One-sided NVLink-style halo puts across processes (transport="p2p"): two
+ranks, each with its own CUDA context and engine, exchange halo planes by
+storing straight into the peer's IPC-mapped halo plane.  Both ranks share
+the single GPU of this build (host barriers only — no kernel waits on
+another rank), and the result must equal the single-process solve bit for bit."""
+
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+
+from oracle import blocksolve_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out_dir):
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    os.environ["LOCAL_RANK"] = "0"
+    import torch
+
+    import paper_2009_12638_b200 as bs
+    from paper_2009_12638_b200.distributed import outer_solve_distributed
+
+    torch.cuda.set_device(0)
+    torch.distributed.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                                         world_size=world)
+    n = 32
+    b = O.seeded_rhs(n ** 3, 0)
+    prob = bs.LinearProblem(bs.StencilOperator(n, n, n), b, bs.Grid3D(n, n, n))
+    cfg = bs.OuterConfig(block_grid=(1, 1, 4), inner=bs.InnerSolverSpec("cg", 50, 1e-3), tol=1e-8,
+                         tolerance_basis="initial")
+    res = outer_solve_distributed(prob, cfg, transport="p2p")
+    np.savez(os.path.join(out_dir, f"ipc_{rank}.npz"), solution=res.solution,
+             counts=np.asarray(res.inner_iterations_per_block),
+             est=np.asarray([r.estimated_residual for r in res.trace.rows]))
+    torch.distributed.destroy_process_group()
+
+
+@pytest.mark.timeout(600)
+def test_p2p_ipc_halo_puts_two_processes_equal_single_process():
+    import torch.multiprocessing as mp
+
+    import paper_2009_12638_b200 as bs
+
+    with tempfile.TemporaryDirectory() as tmp:
+        mp.spawn(_worker, args=(2, _port(), tmp), nprocs=2, join=True)
+        n = 32
+        b = O.seeded_rhs(n ** 3, 0)
+        prob = bs.LinearProblem(bs.StencilOperator(n, n, n), b, bs.Grid3D(n, n, n))
+        cfg = bs.OuterConfig(block_grid=(1, 1, 4), inner=bs.InnerSolverSpec("cg", 50, 1e-3), tol=1e-8,
+                             tolerance_basis="initial")
+        ref = bs.outer_solve(prob, cfg)
+        for rank in (0, 1):
+            got = np.load(os.path.join(tmp, f"ipc_{rank}.npz"))
+            assert np.array_equal(got["counts"], np.asarray(ref.inner_iterations_per_block))
+            assert np.array_equal(got["est"], np.asarray([r.estimated_residual for r in ref.trace.rows]))
+            assert np.array_equal(got["solution"], ref.solution)
