@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--cpu-its", type=int, default=6, help="CG iterations in the CPU sample")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
+                    help="cross-GPU halo transport of the sharded outer workloads")
     ap.add_argument("--workload", default="config2", choices=["config2", "config3", "config4", "config5"],
                     help="config2 (default, the bench line); config3/4/5 = outer block-Jacobi solves (supplemental)")
     return ap.parse_args()
@@ -392,7 +394,7 @@ def run_outer_workload(args):
 
     def solve():
         if world > 1:
-            return outer_solve_distributed(prob, cfg)
+            return outer_solve_distributed(prob, cfg, transport=args.transport)
         return bs.outer_solve(prob, cfg)
 
     for _ in range(args.warmup):
