@@ -114,6 +114,17 @@ int bs_stencil_apply(bs_ctx *ctx, int block, const double *x, double *y, void *s
 int bs_cg_begin(bs_ctx *ctx, int max_iterations, double tolerance, int basis,
                 const int32_t *active, void *stream);
 
+/* a2': arm point-Jacobi sweeps x <- D^-1 (b - (A - D) x) on the active blocks
+ * (inner_solvers.py:75-99; same rhs assembly and warm start as bs_cg_begin).
+ * One fused sweep per iteration k reads x_k once (haloed), reports
+ * ||rhs - A x_k|| / ||rhs|| and writes x_{k+1}; stops at the first x_k that
+ * meets the tolerance (k = iterations used), on a non-finite residual
+ * (breakdown) or at k = max_iterations.  bs_run drives the solve; the iterate
+ * is home in x after bs_flush (halo packs and residual sweeps read it where it
+ * is without a flush). */
+int bs_jacobi_begin(bs_ctx *ctx, int max_iterations, double tolerance, int basis,
+                    const int32_t *active, void *stream);
+
 /* a3: restarted GMRES(m) workspace.  Per block: V = m Krylov vectors in the
  * block's pitched layout, V[j] = V + j*vstride; W = the Arnoldi work vector.
  * m <= 64.  (inner_solvers.py:149-251; V is fp64[(m+1) x n] there.) */
@@ -141,7 +152,7 @@ int bs_gmres_run(bs_ctx *ctx, int max_cycles, void *stream, int64_t *kernels_out
 /* Run armed solves to completion with device-side stopping.  Default: one
  * CUDA-graph launch whose WHILE node iterates {CG sweep 1, CG sweep 2,
  * IF(any block verifying) residual sweep} until no block is active — no host
- * round trip per iteration.  With timing enabled (bs_timing) the same kernels
+ * round trip per iteration (after bs_jacobi_begin: WHILE { Jacobi sweep }).  With timing enabled (bs_timing) the same kernels
  * are launched from the host in batches of `batch` cycles with CUDA events
  * around each.  max_launches > 0 bounds the sweeps (runaway guard; exceeding
  * it stops the solves and returns BS_ESTATE).  Blocking.  *sweeps_out

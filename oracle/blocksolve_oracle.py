@@ -143,6 +143,25 @@ def csr_spmv(a: CSR, x: np.ndarray) -> np.ndarray:
     return out
 
 
+def csr_diagonal(a: CSR) -> np.ndarray:
+    """Stored diagonal entries, 0 where absent (linalg.py:134-142)."""
+    d = np.zeros(min(a.num_rows, a.num_cols))
+    rows = np.repeat(np.arange(a.num_rows), np.diff(a.row_offsets))
+    hit = (rows == a.col_indices) & (rows < d.shape[0])
+    d[rows[hit]] = a.values[hit]
+    return d
+
+
+def csr_without_diagonal(a: CSR) -> CSR:
+    """Copy with the diagonal entries dropped, order kept (linalg.py:144-159)."""
+    rows = np.repeat(np.arange(a.num_rows, dtype=np.int64), np.diff(a.row_offsets))
+    keep = rows != a.col_indices
+    counts = np.bincount(rows[keep], minlength=a.num_rows)
+    offsets = np.zeros(a.num_rows + 1, dtype=np.int64)
+    np.cumsum(counts, out=offsets[1:])
+    return CSR(a.num_rows, a.num_cols, offsets, a.col_indices[keep].copy(), a.values[keep].copy())
+
+
 class ThreadedCSR:
     """Row-partitioned ``csr_spmv`` on a thread pool (numpy releases the GIL in
     its gather, multiply and reduceat loops).  Rows are independent, so the
@@ -238,6 +257,32 @@ def stencil_apply(u3: np.ndarray, region: np.ndarray | None = None) -> np.ndarra
     return np.where(region, y, 0.0)
 
 
+def offdiag_apply(u3: np.ndarray, region: np.ndarray | None = None) -> np.ndarray:
+    """(A - D) u matrix-free on ``region``: ``csr_spmv`` of
+    ``csr_without_diagonal`` bit for bit.  Present terms
+    [-u(z-1), -u(y-1), -u(x-1), -u(x+1), -u(y+1), -u(z+1)] as
+    ``t_first + seq(t_rest)``; unlike the full row no term is always present,
+    so the upper neighbours can lead, and a row without neighbours is 0."""
+    if region is None:
+        region = np.ones(u3.shape, dtype=bool)
+    u = np.where(region, u3, 0.0)
+    t = [-_shift(u, 0, -1, 0.0), -_shift(u, 1, -1, 0.0), -_shift(u, 2, -1, 0.0),
+         -_shift(u, 2, 1, 0.0), -_shift(u, 1, 1, 0.0), -_shift(u, 0, 1, 0.0)]
+    pres = [_shift(region, 0, -1, False), _shift(region, 1, -1, False), _shift(region, 2, -1, False),
+            _shift(region, 2, 1, False), _shift(region, 1, 1, False), _shift(region, 0, 1, False)]
+
+    def chain(first: int) -> np.ndarray:
+        s = t[first]
+        for q in range(first + 1, 6):
+            s = s + t[q]
+        return s
+
+    y = np.zeros_like(u)
+    for lead in range(5, -1, -1):  # the first present term leads
+        y = np.where(pres[lead], t[lead] + chain(lead + 1) if lead < 5 else t[5], y)
+    return np.where(region, y, 0.0)
+
+
 # --------------------------------------------------------------------------
 # inner solvers  (inner_solvers.py)
 # --------------------------------------------------------------------------
@@ -309,6 +354,35 @@ def cg(apply: Callable, b, x0, max_iterations: int, tolerance: float = 0.0,
         p = r + beta * p
         rr = rr_new
     return x, Report(it, rel, "max_iterations", history)
+
+
+def jacobi(apply: Callable, apply_off: Callable, diag: np.ndarray, b, x0, max_iterations: int,
+           tolerance: float = 0.0, basis: str = "rhs"):
+    """Point Jacobi, restating ``jacobi_solve`` (inner_solvers.py:75-99):
+    x <- (b - (A - D) x) / d, relative residual after every update, stop at
+    the first iterate meeting ``tolerance`` (or non-finite: breakdown).
+    ``basis="initial"`` scales the tolerance by the initial relative residual
+    (the wrapper of SURVEY §8(c))."""
+    b = np.asarray(b, dtype=np.float64)
+    x = np.array(x0, dtype=np.float64, copy=True)
+    d = np.asarray(diag, dtype=np.float64)
+    if np.any(d == 0.0):
+        return x, Report(0, np.inf, "breakdown")
+    scale = _scale(b)
+    rel = float(np.linalg.norm(b - apply(x))) / scale
+    tol = tolerance if basis == "rhs" else tolerance * rel
+    if rel <= tol:
+        return x, Report(0, rel, "tolerance_met")
+    history = []
+    for it in range(1, max_iterations + 1):
+        x = (b - apply_off(x)) / d
+        rel = float(np.linalg.norm(b - apply(x))) / scale
+        history.append(rel)
+        if not np.isfinite(rel):
+            return x, Report(it, rel, "breakdown", history)
+        if rel <= tol:
+            return x, Report(it, rel, "tolerance_met", history)
+    return x, Report(max_iterations, rel, "max_iterations", history)
 
 
 def _back_substitute(u: np.ndarray, rhs: np.ndarray) -> np.ndarray:
@@ -627,7 +701,7 @@ def outer_solve_sync(shape, b: np.ndarray, block_grid, overlap: int, inner: dict
                      capture_iterates: bool = False) -> OracleResult:
     """Synchronous two-stage solve (multisplit.py:544-797, replay execution).
 
-    ``inner`` = dict(kind="cg"|"gmres", max_iterations, tolerance, restart,
+    ``inner`` = dict(kind="jacobi"|"cg"|"gmres", max_iterations, tolerance, restart,
     basis="rhs"|"initial").  Sync exchanges deliver every neighbor's
     iteration-k payload, so the schedule is plain block Jacobi and the
     result does not depend on worker order.
@@ -663,6 +737,9 @@ def outer_solve_sync(shape, b: np.ndarray, block_grid, overlap: int, inner: dict
             ap = (lambda v, m=ws.a_ii: csr_spmv(m, v))
             if kind == "cg":
                 x_new, rep = cg(ap, rhs, xs[blk], max_its, itol, basis)
+            elif kind == "jacobi":
+                off = (lambda v, m=csr_without_diagonal(ws.a_ii): csr_spmv(m, v))
+                x_new, rep = jacobi(ap, off, csr_diagonal(ws.a_ii), rhs, xs[blk], max_its, itol, basis)
             else:
                 x_new, rep = gmres(ap, rhs, xs[blk], max_its, itol, restart, basis)
             if rep.stop_reason == "breakdown":

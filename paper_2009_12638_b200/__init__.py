@@ -8,7 +8,7 @@ for that path; every numerical step runs in the hand-written CUDA kernels of
 
 from .errors import (ConfigurationError, DeviceError, ProtocolError, SolverBreakdownError,
                      ZeroRhsError)
-from .inner_solvers import InnerSolveReport, InnerSolverSpec, cg_solve, gmres_solve, solve
+from .inner_solvers import InnerSolveReport, InnerSolverSpec, cg_solve, gmres_solve, jacobi_solve, solve
 from .linalg import residual_norms, spmv
 from .multisplit import (TRACE_HEADER, DelayModel, OuterConfig, ResidualTrace, SolveResult,
                          TraceRow, check_termination, combined_residual, outer_solve)
@@ -22,6 +22,6 @@ __all__ = [
     "FACES", "Grid3D", "InnerSolveReport", "InnerSolverSpec", "LinearProblem", "OuterConfig",
     "ProtocolError", "ResidualTrace", "SolveResult", "SolverBreakdownError", "StencilOperator",
     "TRACE_HEADER", "TraceRow", "ZeroRhsError", "build_laplace_3d", "cg_solve",
-    "check_termination", "combined_residual", "decompose", "gmres_solve", "outer_solve",
+    "check_termination", "combined_residual", "decompose", "gmres_solve", "jacobi_solve", "outer_solve",
     "residual_norms", "seeded_rhs", "solve", "spmv",
 ]

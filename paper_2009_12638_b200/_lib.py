@@ -67,6 +67,7 @@ _SIGS = {
     "bs_block_pitch": ([_P, _I], _I),
     "bs_stencil_apply": ([_P, _I, _P, _P, _P], _I),
     "bs_cg_begin": ([_P, _I, ctypes.c_double, _I, _P, _P], _I),
+    "bs_jacobi_begin": ([_P, _I, ctypes.c_double, _I, _P, _P], _I),
     "bs_sweep_resid": ([_P, _P], _I),
     "bs_cancel": ([_P, _P, _P], _I),
     "bs_run": ([_P, _I, _I, _P, ctypes.POINTER(ctypes.c_int64)], _I),

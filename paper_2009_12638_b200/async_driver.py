@@ -117,7 +117,8 @@ def outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, spec):
                         _lib.check(lib.bs_async_receive(eng.ctx, 0, mb.ghost_dir, mb.ring.data_ptr(),
                                                         mb.seqs.data_ptr(), mb.R, mb.applied.data_ptr(),
                                                         mb.stage.data_ptr(), mb.torn.data_ptr(), st))
-                    eng.cg_begin(spec.max_iterations, spec.tolerance, config.tolerance_basis)
+                    begin = eng.cg_begin if spec.kind == "cg" else eng.jacobi_begin
+                    begin(spec.max_iterations, spec.tolerance, config.tolerance_basis)
                     eng.run(batch=config.batch, max_launches=launch_bound(spec.max_iterations, config.batch))
                     rep = eng.reports()[0]
                     if int(rep.stop_reason) == 3:

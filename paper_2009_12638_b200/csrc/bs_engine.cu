@@ -107,11 +107,12 @@ enum Phase : int {
     PH_G_FORM = 11,   // x += V y
     PH_G_RESID = 12,  // true residual of the formed iterate ; restart or stop
     PH_OWNRES = 13,   // residual of the gathered (owner) iterate on owned rows
+    PH_JAC = 14,      // point-Jacobi sweep: rel of x_k and x_{k+1} = (rhs - offd x_k) / 6
 };
 
-enum Kind : int { KIND_CG = 0, KIND_GMRES = 1 };
+enum Kind : int { KIND_CG = 0, KIND_GMRES = 1, KIND_JACOBI = 2 };
 
-enum Op : int { OP_RESID = 0, OP_S1 = 1, OP_S2 = 2, OP_APPLY = 3, OP_GSPMV = 4 };
+enum Op : int { OP_RESID = 0, OP_S1 = 1, OP_S2 = 2, OP_APPLY = 3, OP_GSPMV = 4, OP_JAC = 5 };
 
 // pointwise (non-stencil) GMRES passes
 enum Pk : int { PK_NORM = 0, PK_MGS = 1, PK_FINAL = 2, PK_FORM = 3, PK_OWNRES = 4 };
@@ -162,7 +163,8 @@ struct DState {
     int phase, stop, it, first, pend, pcur, max_its, basis;
     double tol, tol_eff, scale, rel, rr, alpha, beta, alpha_pend;
     double q[NQ];
-    int kind, gj, gi, gflag, gm, gpad;
+    int kind, gj, gi, gflag, gm;
+    int xin;  // where the block's iterate lives: 0 = x, 1 = p[0] (Jacobi ping-pong)
     double cycle_start, gnrm;
 };
 
@@ -277,6 +279,22 @@ __device__ __forceinline__ double stencil7(double zm, double ym, double xm, doub
 __device__ __forceinline__ double stencil7_interior(double zm, double ym, double xm, double c, double xp, double yp,
                                                     double zp) {
     return add(-zm, add(add(add(add(add(-ym, -xm), mul(6.0, c)), -xp), -yp), -zp));
+}
+
+// One row of the operator without its diagonal (linalg.py:144-159) under the
+// same reduceat rule: present terms [-zm, -ym, -xm, -xp, -yp, -zp], the first
+// present one plus the left-to-right sum of those after it (absent ones are
+// exact zeros there).  Without any lower neighbour the upper flags decide
+// which term leads; a row with no neighbour at all is an empty segment (0).
+__device__ __forceinline__ double offdiag6(double zm, double ym, double xm, double xp, double yp, double zp, bool pz,
+                                           bool py, bool px, bool qx, bool qy, bool qz) {
+    if (pz) return add(-zm, add(add(add(add(-ym, -xm), -xp), -yp), -zp));
+    if (py) return add(-ym, add(add(add(-xm, -xp), -yp), -zp));
+    if (px) return add(-xm, add(add(-xp, -yp), -zp));
+    if (qx) return add(-xp, add(-yp, -zp));
+    if (qy) return add(-yp, -zp);
+    if (qz) return -zp;
+    return 0.0;
 }
 
 // ------------------------------------------------------------------ TMA / mbarrier
@@ -520,9 +538,10 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
         if (here) {
             const double xm = uval(st, own - 1, -1, 0, lz), xp = uval(st, own + 1, 1, 0, lz);
             const double ym = uval(st, own - SX, 0, -1, lz), yp = uval(st, own + SX, 0, 1, lz);
-            double au;
+            double au, od = 0.0;
             if (BOX && warp_xy_interior && lz > 0) {
                 au = stencil7_interior(u_prev, ym, xm, u_cur, xp, yp, u_next);
+                if (OP == OP_JAC) od = offdiag6(u_prev, ym, xm, xp, yp, u_next, true, true, true, true, true, true);
             } else {
                 bool pz, py, px;
                 if (BOX) {
@@ -536,6 +555,20 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
                     px = in_region(B, gi - 1, gj, gk);
                 }
                 au = stencil7(u_prev, ym, xm, u_cur, xp, yp, u_next, pz, py, px);
+                if (OP == OP_JAC) {
+                    bool qz, qy, qx;
+                    if (BOX) {
+                        qz = lz < pdz - 1;
+                        qy = ly < pdy - 1;
+                        qx = lx < pdx - 1;
+                    } else {
+                        const int gk = B.plo[2] + lz;
+                        qz = in_region(B, gi, gj, gk + 1);
+                        qy = in_region(B, gi, gj + 1, gk);
+                        qx = in_region(B, gi + 1, gj, gk);
+                    }
+                    od = offdiag6(u_prev, ym, xm, xp, yp, u_next, pz, py, px, qx, qy, qz);
+                }
             }
             const double *cst = reinterpret_cast<const double *>(st + COFF);
             if (OP == OP_APPLY) {
@@ -552,7 +585,7 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
                 out_p[sx] = u_cur;
                 if (pend) out_x[sx] = add(cst[tid], mul(alpha_pend, reinterpret_cast<const double *>(st + SEG_H)[own]));
                 acc[0] = add(acc[0], mul(u_cur, au));
-            } else {  // OP_RESID: r = (b - C*halo) - A_ii u
+            } else {  // OP_RESID: r = (b - C*halo) - A_ii u ; OP_JAC: also the Jacobi update
                 const double bv = cst[tid];
                 const int gk = B.plo[2] + lz;
                 const bool face = !BOX || lx == 0 || ly == 0 || lz == 0 || lx == pdx - 1 || ly == pdy - 1 ||
@@ -582,17 +615,24 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
                     }
                     if (cnt) rhs = sub(bv, cnt == 1 ? firstc : add(firstc, rest));
                     // global operator row (residual_norms on the gathered iterate)
-                    rg_au = stencil7(v[0], v[1], v[2], u_cur, v[3], v[4], v[5], pg[0], pg[1], pg[2]);
+                    if (OP == OP_RESID) rg_au = stencil7(v[0], v[1], v[2], u_cur, v[3], v[4], v[5], pg[0], pg[1], pg[2]);
                 }
                 const double rv = sub(rhs, au);
-                out_r[sx] = rv;
-                acc[0] = add(acc[0], mul(rhs, rhs));
-                const double r2 = mul(rv, rv);
-                acc[1] = add(acc[1], r2);
-                if (BOX || in_owned(B, gi, gj, gk)) {
-                    acc[2] = add(acc[2], r2);
-                    const double rg = sub(bv, rg_au);
-                    acc[3] = add(acc[3], mul(rg, rg));
+                if (OP == OP_JAC) {
+                    // x_{k+1} = (rhs - offd x_k) / d (inner_solvers.py:88) ; ||rhs - A x_k||
+                    out_p[sx] = __ddiv_rn(sub(rhs, od), 6.0);
+                    acc[0] = add(acc[0], mul(rhs, rhs));
+                    acc[1] = add(acc[1], mul(rv, rv));
+                } else {
+                    out_r[sx] = rv;
+                    acc[0] = add(acc[0], mul(rhs, rhs));
+                    const double r2 = mul(rv, rv);
+                    acc[1] = add(acc[1], r2);
+                    if (BOX || in_owned(B, gi, gj, gk)) {
+                        acc[2] = add(acc[2], r2);
+                        const double rg = sub(bv, rg_au);
+                        acc[3] = add(acc[3], mul(rg, rg));
+                    }
                 }
             }
         }
@@ -843,7 +883,54 @@ __device__ __noinline__ void cg_transition(const DBlock &B, DState &S, int ph, c
     }
 }
 
+// ---- point Jacobi (inner_solvers.py:75-99).  Sweep k reads x_k from
+// buf[xin] (x or p[0]), reports ||rhs - A x_k|| and writes x_{k+1} into the
+// other buffer; the solve stops at the first k whose x_k passes a test, so the
+// answer is buf[xin] and k the iteration count.
+__device__ __noinline__ void jacobi_transition(const DBlock &B, DState &S, int ph, const double *q) {
+    const double rel_in = [&] {
+        if (S.it == 0) {
+            const double bn = sqrt(q[0]);
+            S.scale = bn > 0.0 ? bn : 1.0;  // inner_solvers.py:70-72
+        }
+        return sqrt(q[1]) / S.scale;
+    }();
+    if (ph == PH_INIT) {  // residual sweep of the outer driver doubles as the initial check
+        for (int i = 0; i < NQ; ++i) S.q[i] = q[i];
+        S.rel = rel_in;
+        S.tol_eff = S.basis == BS_BASIS_INITIAL ? S.tol * rel_in : S.tol;
+        S.xin = 0;
+        if (rel_in <= S.tol_eff) {  // inner_solvers.py:85-87
+            S.stop = BS_STOP_TOLERANCE_MET;
+            S.phase = PH_DONE;
+        } else {
+            S.phase = PH_JAC;
+        }
+        return;
+    }
+    // PH_JAC, sweep k = S.it
+    const int k = S.it;
+    if (k == 0) S.tol_eff = S.basis == BS_BASIS_INITIAL ? S.tol * rel_in : S.tol;
+    S.rel = rel_in;
+    if (k > 0 && k - 1 < B.hist_cap) B.hist[k - 1] = rel_in;
+    int stop = BS_STOP_NONE;
+    if (k > 0 && !isfinite(rel_in)) stop = BS_STOP_BREAKDOWN;           // inner_solvers.py:93-94
+    else if (rel_in <= S.tol_eff) stop = BS_STOP_TOLERANCE_MET;        // 85-87, 95-96
+    else if (k >= S.max_its) stop = BS_STOP_MAX_ITERATIONS;             // 97
+    if (stop != BS_STOP_NONE) {
+        S.stop = stop;
+        S.phase = PH_DONE;  // x_k stays in buf[xin]
+    } else {
+        S.xin ^= 1;  // x_{k+1} was written to the other buffer
+        S.it = k + 1;
+    }
+}
+
 __device__ void transition(const DBlock &B, DState &S, GState *G, int ph, const double *q) {
+    if (ph == PH_JAC || (ph == PH_INIT && S.kind == KIND_JACOBI)) {
+        jacobi_transition(B, S, ph, q);
+        return;
+    }
     const bool gm = (ph >= PH_G_NORM && ph <= PH_G_RESID) || (ph == PH_INIT && S.kind == KIND_GMRES);
     if (gm) gmres_transition(B, S, *G, ph, q);
     else cg_transition(B, S, ph, q);
@@ -857,6 +944,7 @@ __device__ __forceinline__ bool serves(const DState &S, const KParams &P) {
     if (OPK == OP_S2) return ph == PH_S2;
     if (OPK == OP_RESID) return ph == PH_INIT || ph == PH_VERIFY || ph == PH_RESID || ph == PH_G_RESID;
     if (OPK == OP_GSPMV) return ph == PH_G_SPMV && S.gj == P.launch_j;
+    if (OPK == OP_JAC) return ph == PH_JAC;
     if (PKK == PK_NORM) return ph == PH_G_NORM && S.gj == P.launch_j;
     if (PKK == PK_MGS) return ph == PH_G_MGS && S.gj == P.launch_j && S.gi == P.launch_i;
     if (PKK == PK_FINAL) return ph == PH_G_FINAL && S.gj == P.launch_j;
@@ -918,7 +1006,7 @@ __device__ void finish(const KParams &P, int b, int ph, bool served, double (&ac
         if (p2 != PH_DONE && p2 != PH_IDLE) ++active;
         if (p2 == PH_VERIFY || p2 == PH_INIT || p2 == PH_RESID) ++verify;
     }
-    if (OPK == OP_S2) {
+    if (OPK == OP_S2 || OPK == OP_JAC) {
         Control &ctl = *P.ctl;
         ctl.cycles += 1;
         if (ctl.max_cycles > 0 && ctl.cycles > ctl.max_cycles && active) {
@@ -968,9 +1056,14 @@ __global__ void __launch_bounds__(NTHR, BS_MINBLOCKS) k_sweep(const KParams P) {
         C.pout = B.p[S.pcur ^ 1];
         const CUtensorMap *tm_p = tm + (S.pcur ? TM_P1H : TM_P0H);
         if (OPK == OP_RESID) {
-            C.map_a = tm + TM_XH;
+            C.map_a = tm + (S.xin ? TM_P0H : TM_XH);
             C.map_b = C.pend ? tm_p : nullptr;
             C.map_c = tm + TM_BO;
+        } else if (OPK == OP_JAC) {  // x_k haloed from buf[xin], b bare; x_{k+1} -> other buffer
+            C.map_a = tm + (S.xin ? TM_P0H : TM_XH);
+            C.map_b = nullptr;
+            C.map_c = tm + TM_BO;
+            C.pout = S.xin ? B.x : B.p[0];
         } else if (OPK == OP_S1) {
             C.map_a = tm + TM_RH;
             C.map_b = (!C.first || C.pend) ? tm_p : nullptr;
@@ -989,7 +1082,7 @@ __global__ void __launch_bounds__(NTHR, BS_MINBLOCKS) k_sweep(const KParams P) {
         sweep_tile<OPK, BOX>(C, blockIdx.x - B.cta_begin, smem, acc);
         __syncthreads();  // all planes consumed: the stage ring is free for reuse
     }
-    finish<NTHR, OPK>(P, b, ph, served, acc, OPK == OP_RESID ? NQ : 1, smem);
+    finish<NTHR, OPK>(P, b, ph, served, acc, OPK == OP_RESID ? NQ : (OPK == OP_JAC ? 2 : 1), smem);
 }
 
 // Pointwise GMRES passes over a block's region, tile by tile (same CTA table
@@ -1241,10 +1334,11 @@ __global__ void k_flush(const DBlock *__restrict__ blocks, const DState *states)
     const int b = blockIdx.y;
     const DBlock &B = blocks[b];
     const DState &S = states[b];
-    if (!S.pend) return;
+    if (!S.pend && !S.xin) return;
     const long long n = (long long)B.pdim[0] * B.pdim[1] * B.pdim[2];
     const double a = S.alpha_pend;
-    const double *p = B.p[S.pcur];
+    const bool jac = S.xin != 0;  // Jacobi iterate left in p[0]: copy it home
+    const double *p = B.p[jac ? 0 : S.pcur];
     for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < n;
          c += (long long)gridDim.x * blockDim.x) {
         const int i = B.plo[0] + (int)(c % B.pdim[0]);
@@ -1253,14 +1347,17 @@ __global__ void k_flush(const DBlock *__restrict__ blocks, const DState *states)
         const int k = B.plo[2] + (int)(t / B.pdim[1]);
         if (B.overlap == 0 || in_region(B, i, j, k)) {
             const long long s = sidx(B, i, j, k);
-            B.x[s] = add(B.x[s], mul(a, p[s]));
+            B.x[s] = jac ? p[s] : add(B.x[s], mul(a, p[s]));
         }
     }
 }
 
 __global__ void k_clear_pend(DState *states, int nblocks) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b < nblocks) states[b].pend = 0;
+    if (b < nblocks) {
+        states[b].pend = 0;
+        states[b].xin = 0;
+    }
 }
 
 // Sync halo pack: ghost[dir] of dst <- current (flushed-on-the-fly) x of src.
@@ -1285,6 +1382,7 @@ __global__ void k_halo_pack(const DBlock *__restrict__ blocks, const DState *sta
     const double a = SS.alpha_pend;
     const bool pend = SS.pend != 0;
     const double *p = S.p[SS.pcur];
+    const double *xsrc = SS.xin ? S.p[0] : S.x;
     for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < n;
          c += (long long)gridDim.x * blockDim.x) {
         const int u = (int)(c % nu), v = (int)(c / nu);
@@ -1298,7 +1396,7 @@ __global__ void k_halo_pack(const DBlock *__restrict__ blocks, const DState *sta
             default: i = D.plo[0] + D.pdim[0]; j = D.plo[1] + u; k = D.plo[2] + v; break;
         }
         const long long s = sidx(S, i, j, k);
-        const double xv = S.x[s];
+        const double xv = xsrc[s];
         D.ghost[dir][c] = pend ? add(xv, mul(a, p[s])) : xv;
     }
 }
@@ -1350,11 +1448,12 @@ __global__ void k_async_post(const DBlock *__restrict__ blocks, const DState *st
     const double a = S.alpha_pend;
     const bool pend = S.pend != 0;
     const double *p = B.p[S.pcur];
+    const double *xsrc = S.xin ? B.p[0] : B.x;
     for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += (long long)gridDim.x * blockDim.x) {
         int i, j, k;
         plane_cell(B, dir, c, nu, i, j, k);
         const long long sx = sidx(B, i, j, k);
-        const double xv = B.x[sx];
+        const double xv = xsrc[sx];
         slot[c] = pend ? add(xv, mul(a, p[sx])) : xv;
     }
     __shared__ bool last;
@@ -1524,6 +1623,11 @@ struct bs_ctx {
     // device-side solve loop: RESID ; WHILE(any active) { S1 ; S2 ; IF(any verify) RESID }
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t graph_exec = nullptr;
+    // point-Jacobi loop: RESID (serves INIT) ; WHILE(any active) { JAC }
+    cudaGraph_t jgraph = nullptr;
+    cudaGraphExec_t jgraph_exec = nullptr;
+    int run_kind = KIND_CG;    // solve armed last: bs_run drives its loop
+    bool jac_dirty = false;    // a Jacobi iterate may sit in p[0] (flush before other solves)
     // optional CUDA-event timing of the sweep kernels (launch mode only)
     bool timing = false;
     std::vector<cudaEvent_t> ev;
@@ -1693,6 +1797,40 @@ int build_graph(bs_ctx *c) {
     return BS_OK;
 }
 
+// Graph: RESID (serves INIT) -> WHILE(active) { JAC }
+int build_jacobi_graph(bs_ctx *c) {
+    if (c->jgraph_exec) return BS_OK;
+    cudaGraph_t g;
+    BS_CU(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h_loop;
+    BS_CU(cudaGraphConditionalHandleCreate(&h_loop, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNode_t n_init;
+    if (int e = add_sweep_node<OP_RESID>(c, g, &n_init, nullptr, 0, h_loop, 0)) return e;
+    cudaGraphNodeParams wp = {};
+    wp.type = cudaGraphNodeTypeConditional;
+    wp.conditional.handle = h_loop;
+    wp.conditional.type = cudaGraphCondTypeWhile;
+    wp.conditional.size = 1;
+    cudaGraphNode_t n_while;
+    BS_CU(cudaGraphAddNode(&n_while, g, &n_init, 1, &wp));
+    cudaGraph_t body = wp.conditional.phGraph_out[0];
+    cudaGraphNode_t n_j;
+    if (int e = add_sweep_node<OP_JAC>(c, body, &n_j, nullptr, 0, h_loop, 0)) return e;
+    cudaGraphExec_t ex;
+    BS_CU(cudaGraphInstantiate(&ex, g, 0));
+    c->jgraph = g;
+    c->jgraph_exec = ex;
+    return BS_OK;
+}
+
+// x := x + alpha_pend p / the Jacobi iterate, for every block with one pending
+void launch_flush(bs_ctx *c, cudaStream_t st) {
+    g_launches += 2;
+    k_flush<<<dim3(592, c->nblocks), 256, 0, st>>>(c->dblocks, c->dstates);
+    k_clear_pend<<<(c->nblocks + 127) / 128, 128, 0, st>>>(c->dstates, c->nblocks);
+    c->jac_dirty = false;
+}
+
 }  // namespace
 
 // ====================================================================== C ABI
@@ -1857,7 +1995,8 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
     {
         const void *fns[] = {sweep_fn<OP_RESID>(true),    sweep_fn<OP_RESID>(false), sweep_fn<OP_S1>(true),
                              sweep_fn<OP_S1>(false),      sweep_fn<OP_S2>(true),     sweep_fn<OP_S2>(false),
-                             sweep_fn<OP_GSPMV>(true),    sweep_fn<OP_GSPMV>(false), (const void *)k_apply<true>,
+                             sweep_fn<OP_GSPMV>(true),    sweep_fn<OP_GSPMV>(false), sweep_fn<OP_JAC>(true),
+                             sweep_fn<OP_JAC>(false),     (const void *)k_apply<true>,
                              (const void *)k_apply<false>};
         for (const void *f : fns)
             if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
@@ -1875,6 +2014,8 @@ int bs_ctx_destroy(bs_ctx *c) {
     cudaSetDevice(c->device);
     if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
     if (c->graph) cudaGraphDestroy(c->graph);
+    if (c->jgraph_exec) cudaGraphExecDestroy(c->jgraph_exec);
+    if (c->jgraph) cudaGraphDestroy(c->jgraph);
     cudaFree(c->dblocks);
     cudaFree(c->dstates);
     cudaFree(c->dtmaps);
@@ -1950,10 +2091,32 @@ int bs_cg_begin(bs_ctx *c, int max_iterations, double tolerance, int basis, cons
     cudaStream_t st = (cudaStream_t)stream;
     const int *dact = nullptr;
     if (int e = upload_active(c, active, st, &dact)) return e;
+    if (c->jac_dirty) launch_flush(c, st);
     ++g_launches;
     k_arm<<<(c->nblocks + 127) / 128, 128, 0, st>>>(c->dstates, dact, c->nblocks, PH_INIT, max_iterations,
                                                    tolerance, basis, KIND_CG, 0);
     BS_CU(cudaGetLastError());
+    c->run_kind = KIND_CG;
+    return BS_OK;
+}
+
+int bs_jacobi_begin(bs_ctx *c, int max_iterations, double tolerance, int basis, const int32_t *active,
+                    void *stream) {
+    if (!c) return fail(BS_EINVAL, "bs_jacobi_begin: null context");
+    if (max_iterations < 1) return fail(BS_EINVAL, "max_iterations must be at least 1");
+    if (!(tolerance >= 0.0)) return fail(BS_EINVAL, "tolerance must be non-negative");
+    if (basis != BS_BASIS_RHS && basis != BS_BASIS_INITIAL) return fail(BS_EINVAL, "unknown tolerance basis");
+    if (int e = set_dev(c)) return e;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int *dact = nullptr;
+    if (int e = upload_active(c, active, st, &dact)) return e;
+    launch_flush(c, st);  // sweep 0 reads x itself: apply any pending CG update / Jacobi copy
+    ++g_launches;
+    k_arm<<<(c->nblocks + 127) / 128, 128, 0, st>>>(c->dstates, dact, c->nblocks, PH_INIT, max_iterations,
+                                                   tolerance, basis, KIND_JACOBI, 0);
+    BS_CU(cudaGetLastError());
+    c->run_kind = KIND_JACOBI;
+    c->jac_dirty = true;
     return BS_OK;
 }
 
@@ -1990,11 +2153,47 @@ int bs_residual(bs_ctx *c, const int32_t *active, void *stream) {
     return BS_OK;
 }
 
+namespace {
+// Jacobi solves: graph mode (one launch) or launch mode (timing), sweep count out
+int run_jacobi(bs_ctx *c, int batch, int max_launches, cudaStream_t st, int64_t *sweeps_out) {
+    if (!c->timing) {
+        if (int e = build_jacobi_graph(c)) return e;
+        ++g_launches;
+        k_reset_control<<<1, 1, 0, st>>>(c->dctl, max_launches > 0 ? max_launches : 0);
+        BS_CU(cudaGraphLaunch(c->jgraph_exec, st));
+        BS_CU(cudaMemcpyAsync(c->hctl, c->dctl, sizeof(Control), cudaMemcpyDeviceToHost, st));
+        BS_CU(cudaStreamSynchronize(st));
+        const Control ctl = *c->hctl;
+        g_launches += (long long)ctl.resid_runs + ctl.cycles;
+        if (sweeps_out) *sweeps_out = (long long)ctl.resid_runs + ctl.cycles;
+        if (ctl.stalled) return fail(BS_ESTATE, "bs_run: solves still active after max_launches sweeps");
+        return BS_OK;
+    }
+    int64_t launched = 1;
+    launch_sweep<OP_RESID>(c, st, -1);
+    for (;;) {
+        BS_CU(cudaMemcpyAsync(c->hpinned, c->dnactive, sizeof(int), cudaMemcpyDeviceToHost, st));
+        BS_CU(cudaStreamSynchronize(st));
+        if (c->hpinned[0] == 0) break;
+        if (max_launches > 0 && launched >= max_launches) {
+            if (sweeps_out) *sweeps_out = launched;
+            return fail(BS_ESTATE, "bs_run: solves still active after max_launches sweeps");
+        }
+        for (int i = 0; i < batch; ++i) launch_sweep<OP_JAC>(c, st, -1);
+        launched += batch;
+        BS_CU(cudaGetLastError());
+    }
+    if (sweeps_out) *sweeps_out = launched;
+    return BS_OK;
+}
+}  // namespace
+
 int bs_run(bs_ctx *c, int batch, int max_launches, void *stream, int64_t *sweeps_out) {
     if (!c) return fail(BS_EINVAL, "bs_run: null context");
     if (batch < 1) batch = 1;
     if (int e = set_dev(c)) return e;
     cudaStream_t st = (cudaStream_t)stream;
+    if (c->run_kind == KIND_JACOBI) return run_jacobi(c, batch, max_launches, st, sweeps_out);
     if (!c->timing) {
         // device-side loop: one graph launch runs the solves to completion
         if (int e = build_graph(c)) return e;
@@ -2075,6 +2274,7 @@ int bs_gmres_begin(bs_ctx *c, int max_iterations, double tolerance, int basis, c
     cudaStream_t st = (cudaStream_t)stream;
     const int *dact = nullptr;
     if (int e = upload_active(c, active, st, &dact)) return e;
+    if (c->jac_dirty) launch_flush(c, st);
     ++g_launches;
     k_arm<<<(c->nblocks + 127) / 128, 128, 0, st>>>(c->dstates, dact, c->nblocks, PH_INIT, max_iterations,
                                                    tolerance, basis, KIND_GMRES, c->gm);
@@ -2221,9 +2421,7 @@ int bs_flush(bs_ctx *c, void *stream) {
     if (!c) return fail(BS_EINVAL, "bs_flush: null context");
     if (int e = set_dev(c)) return e;
     cudaStream_t st = (cudaStream_t)stream;
-    g_launches += 2;
-    k_flush<<<dim3(592, c->nblocks), 256, 0, st>>>(c->dblocks, c->dstates);
-    k_clear_pend<<<(c->nblocks + 127) / 128, 128, 0, st>>>(c->dstates, c->nblocks);
+    launch_flush(c, st);
     BS_CU(cudaGetLastError());
     return BS_OK;
 }

@@ -240,6 +240,11 @@ class BlockEngine:
         _lib.check(self.lib.bs_cg_begin(self.ctx, int(max_iterations), float(tolerance),
                                         _lib.BASIS[basis], m[0] if m else None, self.stream))
 
+    def jacobi_begin(self, max_iterations: int, tolerance: float, basis: str = "rhs", active=None) -> None:
+        m = self._mask(active)
+        _lib.check(self.lib.bs_jacobi_begin(self.ctx, int(max_iterations), float(tolerance),
+                                            _lib.BASIS[basis], m[0] if m else None, self.stream))
+
     def sweep_resid(self) -> None:
         _lib.check(self.lib.bs_sweep_resid(self.ctx, self.stream))
 

@@ -29,12 +29,13 @@ __all__ = [
     "InnerSolveReport",
     "cg_solve",
     "gmres_solve",
+    "jacobi_solve",
     "solve",
     "SOLVER_KINDS",
 ]
 
 SOLVER_KINDS = ("jacobi", "cg", "gmres", "direct")
-DEVICE_KINDS = ("cg", "gmres")
+DEVICE_KINDS = ("jacobi", "cg", "gmres")
 DEFAULT_RESTART = 30
 
 
@@ -81,6 +82,20 @@ def cg_solve(a: StencilOperator, b, x0, spec: InnerSolverSpec, tolerance_basis: 
     host tensor in -> host tensor out (written into ``out`` when given, e.g.
     a pinned buffer, so the device->host copy runs at full PCIe speed).
     """
+    return _fused_solve("cg", a, b, x0, spec, tolerance_basis, batch, out)
+
+
+def jacobi_solve(a: StencilOperator, b, x0, spec: InnerSolverSpec, tolerance_basis: str = "rhs",
+                 batch: int = 8, out=None):
+    """Point-Jacobi sweeps x <- D^-1 (b - (A - D) x) on the GPU
+    (inner_solvers.py:75-99): one fused sweep per iteration reads x_k once,
+    yields ||b - A x_k|| / ||b|| and writes x_{k+1}; the first x_k meeting the
+    tolerance is returned with k iterations, as in the reference.  Same
+    argument / return conventions as ``cg_solve``."""
+    return _fused_solve("jacobi", a, b, x0, spec, tolerance_basis, batch, out)
+
+
+def _fused_solve(kind, a, b, x0, spec, tolerance_basis, batch, out):
     _check_basis(tolerance_basis)
     n = a.num_rows
     is_tensor = torch is not None and isinstance(b, torch.Tensor)
@@ -92,7 +107,8 @@ def cg_solve(a: StencilOperator, b, x0, spec: InnerSolverSpec, tolerance_basis: 
     with torch.cuda.device(eng.device):
         bb.put("b", bd)
         bb.put("x", xd)
-        eng.cg_begin(spec.max_iterations, spec.tolerance, tolerance_basis)
+        begin = eng.cg_begin if kind == "cg" else eng.jacobi_begin
+        begin(spec.max_iterations, spec.tolerance, tolerance_basis)
         eng.run(batch=batch, max_launches=launch_bound(spec.max_iterations, batch))
         eng.flush()
         rep = eng.reports()[0]
@@ -157,6 +173,8 @@ def solve(a: StencilOperator, b, x0, spec: InnerSolverSpec, tolerance_basis: str
     """Dispatch on ``spec.kind`` (inner_solvers.py:264-276)."""
     if spec.kind == "cg":
         return cg_solve(a, b, x0, spec, tolerance_basis)
+    if spec.kind == "jacobi":
+        return jacobi_solve(a, b, x0, spec, tolerance_basis)
     if spec.kind == "gmres":
         return gmres_solve(a, b, x0, spec, tolerance_basis)
     raise ConfigurationError(

@@ -207,11 +207,11 @@ def check_termination(estimate: float, tol: float, completed: int, max_outer: in
 
 
 def _validate_device_path(config: OuterConfig) -> None:
-    if config.mode == "async" and (config.inner.kind != "cg" or config.overlap != 0):
-        raise ConfigurationError("mode: async runs CG inner solves on overlap-0 decompositions")
-    if config.inner.kind not in ("cg", "gmres"):
+    if config.mode == "async" and (config.inner.kind not in ("cg", "jacobi") or config.overlap != 0):
+        raise ConfigurationError("mode: async runs CG or Jacobi inner solves on overlap-0 decompositions")
+    if config.inner.kind not in ("jacobi", "cg", "gmres"):
         raise ConfigurationError(
-            f"inner: {config.inner.kind!r} is outside the accelerated path (device kinds: cg, gmres)")
+            f"inner: {config.inner.kind!r} is outside the accelerated path (device kinds: jacobi, cg, gmres)")
     if config.delay.kind != "none":
         raise ConfigurationError("delay: injected delays are a simulation knob; use kind='none'")
 

@@ -4,7 +4,7 @@ share of them (one process per GPU, see ``distributed.py``).
 
 Schedule of sweep k (every block at once, device-side):
 
-  1. inner solve (fused CG sweeps or GMRES(m) Arnoldi passes);
+  1. inner solve (fused CG or point-Jacobi sweeps, or GMRES(m) Arnoldi passes);
   2. overlap 0: halo exchange — neighbours' boundary planes (x + pending
      alpha p) land in this block's halo planes (comm.py:332-365, merge with
      m = 1), locally by ``k_halo_pack`` or across ranks by P2P; then one
@@ -42,9 +42,11 @@ def make_inner(eng, spec, config):
 
         def solve():
             eng.gmres_run(max_cycles=spec.max_iterations + 2)
-    else:
+    else:  # fused stencil-sweep solvers: CG (two sweeps per iteration) or point Jacobi (one)
+        begin = eng.cg_begin if spec.kind == "cg" else eng.jacobi_begin
+
         def arm():
-            eng.cg_begin(spec.max_iterations, spec.tolerance, config.tolerance_basis)
+            begin(spec.max_iterations, spec.tolerance, config.tolerance_basis)
 
         def solve():
             eng.run(batch=config.batch, max_launches=launch_bound(spec.max_iterations, config.batch))

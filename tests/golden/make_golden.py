@@ -32,6 +32,7 @@ from blocksolve import (  # noqa: E402  (reference, read-only)
     cg_solve,
     decompose,
     gmres_solve,
+    jacobi_solve,
     outer_solve,
     spmv,
 )
@@ -136,6 +137,24 @@ def main():
                              InnerSolverSpec("gmres", its, tol, restart))
         add_report(f"gmres/{n}_{its}_{restart}", x, rep)
 
+    # -- point Jacobi (inner_solvers.py:75-99)
+    pr = problem(10, 10, 10, {"x_lo": 1.0, "z_hi": 0.5})
+    x, rep = jacobi_solve(pr.matrix, pr.rhs, np.zeros(1000), InnerSolverSpec("jacobi", 400, 1e-3))
+    add_report("jacobi/10_tol", x, rep)
+    pr = problem(9, 6, 4, rhs=seeded(216, 2))
+    x0 = wide_x(rng, 216)
+    arrays["jacobi/9x6x4_maxit/x0"] = x0
+    x, rep = jacobi_solve(pr.matrix, pr.rhs, x0, InnerSolverSpec("jacobi", 25, 0.0))
+    add_report("jacobi/9x6x4_maxit", x, rep)
+    for shape in ((7, 1, 3), (1, 1, 5), (1, 1, 1)):  # rows whose leading neighbour is an upper one
+        n = shape[0] * shape[1] * shape[2]
+        pr = problem(*shape, rhs=seeded(n, 4))
+        x, rep = jacobi_solve(pr.matrix, pr.rhs, np.zeros(n), InnerSolverSpec("jacobi", 12, 0.0))
+        add_report("jacobi/%dx%dx%d" % shape, x, rep)
+    pr = problem(4, 4, 4, rhs=np.zeros(64))
+    x, rep = jacobi_solve(pr.matrix, pr.rhs, np.zeros(64), InnerSolverSpec("jacobi", 5, 0.0))
+    add_report("jacobi/zero_rhs", x, rep)
+
     # -- outer sync traces (multisplit.py:742-797)
     cases = {
         # config-1 shape at reduced size: z_lo=1, 2 z-slabs, CG(50) fixed its
@@ -158,6 +177,11 @@ def main():
                                  inner=("gmres", 10, 0.0), tol=1e-8, mode="paper"),
         "outer/o1_10_211": dict(n=10, seed=5, bg=(2, 1, 1), ov=1,
                                 inner=("cg", 6, 0.0), tol=1e-7, mode="true"),
+        # point-Jacobi inner solves: slabs (box path) and an overlapping split
+        "outer/jac_10_112": dict(n=10, seed=6, bg=(1, 1, 2), ov=0,
+                                 inner=("jacobi", 20, 0.0), tol=1e-6, mode="paper"),
+        "outer/jac_8_221_o1": dict(n=8, faces={"z_lo": 1.0}, bg=(2, 2, 1), ov=1,
+                                   inner=("jacobi", 15, 0.0), tol=1e-6, mode="true"),
     }
     for key, c in cases.items():
         n = c["n"]

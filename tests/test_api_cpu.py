@@ -108,3 +108,15 @@ def test_no_cpu_fallback():
         bs.spmv(bs.StencilOperator(4, 4, 4), np.ones(64))
     with pytest.raises(bs.DeviceError):
         bs.cg_solve(bs.StencilOperator(4, 4, 4), np.ones(64), np.zeros(64), bs.InnerSolverSpec("cg", 5))
+    with pytest.raises(bs.DeviceError):
+        bs.jacobi_solve(bs.StencilOperator(4, 4, 4), np.ones(64), np.zeros(64), bs.InnerSolverSpec("jacobi", 5))
+
+
+def test_solver_kind_routing():
+    """Device kinds: jacobi, cg, gmres; 'direct' is a reference-only dense solve."""
+    from paper_2009_12638_b200.inner_solvers import DEVICE_KINDS, SOLVER_KINDS
+
+    assert DEVICE_KINDS == ("jacobi", "cg", "gmres")
+    assert set(DEVICE_KINDS) < set(SOLVER_KINDS)
+    with pytest.raises(bs.ConfigurationError, match="outside the accelerated path"):
+        bs.solve(bs.StencilOperator(2, 2, 2), np.ones(8), np.zeros(8), bs.InnerSolverSpec("direct", 1))

@@ -176,11 +176,85 @@ def test_cg_config2_full_256_iteration_count():
     assert rel <= 1e-8
 
 
+# ------------------------------------------------------------------ point Jacobi (a2')
+
+
+def _jacobi_case(key):
+    A = arrays()
+    if key == "jacobi/10_tol":
+        return (10, 10, 10), O.dirichlet_rhs(10, 10, 10, {"x_lo": 1.0, "z_hi": 0.5}), np.zeros(1000), 400, 1e-3
+    if key == "jacobi/9x6x4_maxit":
+        return (9, 6, 4), O.seeded_rhs(216, 2), A[key + "/x0"], 25, 0.0
+    if key == "jacobi/zero_rhs":
+        return (4, 4, 4), np.zeros(64), np.zeros(64), 5, 0.0
+    shape = tuple(int(v) for v in key.split("/")[1].split("x"))
+    n = shape[0] * shape[1] * shape[2]
+    return shape, O.seeded_rhs(n, 4), np.zeros(n), 12, 0.0
+
+
+@pytest.mark.parametrize("key", ["jacobi/10_tol", "jacobi/9x6x4_maxit", "jacobi/7x1x3", "jacobi/1x1x5",
+                                 "jacobi/1x1x1", "jacobi/zero_rhs"])
+def test_jacobi_matches_reference(key):
+    """The Jacobi update is elementwise over the reduceat off-diagonal row:
+    iterates are bit-identical to the reference's; residual norms use the
+    device's fixed-order reduction (tolerance)."""
+    A, M = arrays(), meta()[key]
+    shape, b, x0, its, tol = _jacobi_case(key)
+    x, rep = bs.jacobi_solve(bs.StencilOperator(*shape), b, x0, bs.InnerSolverSpec("jacobi", its, tol))
+    assert rep.iterations_used == M["iterations_used"]
+    assert rep.stop_reason == M["stop_reason"]
+    assert np.array_equal(x, A[key + "/x"])
+    assert np.allclose(rep.residual_history, M["residual_history"], rtol=1e-12, atol=1e-300)
+    if M["residual_history"]:
+        assert rep.final_relative_residual == pytest.approx(M["final_relative_residual"], rel=1e-12)
+
+
+def test_jacobi_at_scale_bit_identical_and_basis():
+    """64^3 (odd-sized tiles, many CTAs): 150 capped sweeps bit-identical to the
+    oracle; the r0-relative basis stops where the oracle does."""
+    n = 64
+    b = O.seeded_rhs(n ** 3, 1)
+    op = bs.StencilOperator(n, n, n)
+    ap = lambda v: O.stencil_apply(v.reshape(n, n, n)).ravel()
+    ao = lambda v: O.offdiag_apply(v.reshape(n, n, n)).ravel()
+    d = np.full(n ** 3, 6.0)
+    xo, ro = O.jacobi(ap, ao, d, b, np.zeros(n ** 3), 150, 0.0)
+    x, rep = bs.jacobi_solve(op, b, np.zeros(n ** 3), bs.InnerSolverSpec("jacobi", 150, 0.0))
+    assert (rep.iterations_used, rep.stop_reason) == (150, "max_iterations")
+    assert np.array_equal(x, xo)
+    assert np.allclose(rep.residual_history, ro.residual_history, rtol=1e-11)
+    x0 = np.random.default_rng(3).uniform(-1, 1, n ** 3)
+    xo, ro = O.jacobi(ap, ao, d, b, x0, 500, 0.5, basis="initial")
+    x, rep = bs.jacobi_solve(op, b, x0, bs.InnerSolverSpec("jacobi", 500, 0.5), tolerance_basis="initial")
+    assert rep.iterations_used == ro.iterations_used and rep.stop_reason == ro.stop_reason == "tolerance_met"
+    assert np.array_equal(x, xo)
+    # determinism and engine reuse across solver kinds (the Jacobi iterate is
+    # flushed home before a CG solve starts on the same engine)
+    x2, _ = bs.jacobi_solve(op, b, x0, bs.InnerSolverSpec("jacobi", 500, 0.5), tolerance_basis="initial")
+    assert np.array_equal(x, x2)
+    xc, rc = bs.cg_solve(op, b, np.zeros(n ** 3), bs.InnerSolverSpec("cg", 2000, 1e-8))
+    assert rc.stop_reason == "tolerance_met"
+    x3, r3 = bs.jacobi_solve(op, b, xc, bs.InnerSolverSpec("jacobi", 7, 0.0))
+    xo3, ro3 = O.jacobi(ap, ao, d, b, xc, 7, 0.0)
+    assert np.array_equal(x3, xo3)
+
+
+def test_async_jacobi_inner_converges():
+    n = 16
+    b = O.seeded_rhs(n ** 3, 0)
+    prob = bs.LinearProblem(bs.StencilOperator(n, n, n), b, bs.Grid3D(n, n, n))
+    cfg = bs.OuterConfig(block_grid=(1, 1, 2), inner=bs.InnerSolverSpec("jacobi", 20), mode="async", tol=1e-6,
+                         max_outer=20000, residual_check_every=5)
+    res = bs.outer_solve(prob, cfg)
+    assert res.converged and res.final_true_residual < 1e-6
+
+
 # ------------------------------------------------------------------ outer sync
 
 
 OUTER = ["outer/cfg1_16_fixed", "outer/cfg1_16_literal", "outer/cfg3_16_paper",
-         "outer/cfg3_16_true", "outer/box_12_222", "outer/cfg5_12_o2", "outer/o1_10_211"]
+         "outer/cfg3_16_true", "outer/box_12_222", "outer/cfg5_12_o2", "outer/o1_10_211",
+         "outer/jac_10_112", "outer/jac_8_221_o1"]
 
 
 @pytest.mark.parametrize("key", OUTER)

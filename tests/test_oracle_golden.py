@@ -164,11 +164,90 @@ def test_cg_known_answers():
     assert rep.stop_reason == "breakdown"
 
 
+# ---------------------------------------------------------------- point Jacobi
+
+
+def _jacobi_case(key):
+    """(shape, b, x0, max_its, tol) of a golden Jacobi case (make_golden.py)."""
+    A = arrays()
+    if key == "jacobi/10_tol":
+        return (10, 10, 10), O.dirichlet_rhs(10, 10, 10, {"x_lo": 1.0, "z_hi": 0.5}), np.zeros(1000), 400, 1e-3
+    if key == "jacobi/9x6x4_maxit":
+        return (9, 6, 4), O.seeded_rhs(216, 2), A[key + "/x0"], 25, 0.0
+    if key == "jacobi/zero_rhs":
+        return (4, 4, 4), np.zeros(64), np.zeros(64), 5, 0.0
+    shape = tuple(int(v) for v in key.split("/")[1].split("x"))
+    n = shape[0] * shape[1] * shape[2]
+    return shape, O.seeded_rhs(n, 4), np.zeros(n), 12, 0.0
+
+
+JACOBI = ["jacobi/10_tol", "jacobi/9x6x4_maxit", "jacobi/7x1x3", "jacobi/1x1x5", "jacobi/1x1x1",
+          "jacobi/zero_rhs"]
+
+
+@pytest.mark.parametrize("key", JACOBI)
+@pytest.mark.parametrize("form", ["csr", "matrix_free"])
+def test_jacobi_matches_reference(key, form):
+    A, M = arrays(), meta()[key]
+    shape, b, x0, its, tol = _jacobi_case(key)
+    a = lap(shape)
+    if form == "csr":
+        off = O.csr_without_diagonal(a)
+        ap, ao, d = (lambda v: O.csr_spmv(a, v)), (lambda v: O.csr_spmv(off, v)), O.csr_diagonal(a)
+    else:
+        nx, ny, nz = shape
+        ap = lambda v: O.stencil_apply(v.reshape(nz, ny, nx)).ravel()
+        ao = lambda v: O.offdiag_apply(v.reshape(nz, ny, nx)).ravel()
+        d = np.full(a.num_rows, 6.0)
+    x, rep = O.jacobi(ap, ao, d, b, x0, its, tol)
+    assert rep.iterations_used == M["iterations_used"]
+    assert rep.stop_reason == M["stop_reason"]
+    assert np.array_equal(x, A[key + "/x"])  # the update is elementwise: bit-exact
+    assert np.allclose(rep.residual_history, M["residual_history"], rtol=1e-13, atol=0)
+
+
+@pytest.mark.parametrize("shape", [(6, 5, 4), (16, 16, 16), (7, 1, 3)])
+def test_offdiag_matrix_free_bit_equal(shape):
+    A = arrays()
+    x = A["spmv/%dx%dx%d/x" % shape]
+    a = lap(shape)
+    off = O.csr_without_diagonal(a)
+    assert off.values.shape[0] == a.values.shape[0] - a.num_rows
+    assert np.array_equal(O.csr_diagonal(a), np.full(a.num_rows, 6.0))
+    nx, ny, nz = shape
+    y = O.offdiag_apply(x.reshape(nz, ny, nx)).ravel()
+    assert np.array_equal(y, O.csr_spmv(off, x))
+    # the full row = offdiag + the diagonal's place in the chain: cross-check the
+    # region form on an L1 ball (rows whose leading term is an upper neighbour)
+    reg = O.region_mask((nx, ny, nz), O.owned_boxes((nx, ny, nz), (2, 1, 1))[0], 1)
+    u = x.reshape(nz, ny, nx)
+    rows = np.flatnonzero(reg.ravel())
+    sub = O.csr_without_diagonal(_principal(a, rows))
+    assert np.array_equal(O.offdiag_apply(u, reg).ravel()[rows], O.csr_spmv(sub, x[rows]))
+
+
+def _principal(a, rows):
+    """Principal submatrix of CSR `a` on sorted `rows` (entries kept in order)."""
+    pos = -np.ones(a.num_cols, dtype=np.int64)
+    pos[rows] = np.arange(rows.shape[0])
+    offs, cols, vals = [0], [], []
+    for r in rows:
+        s, e = a.row_offsets[r], a.row_offsets[r + 1]
+        c = pos[a.col_indices[s:e]]
+        keep = c >= 0
+        cols.append(c[keep])
+        vals.append(a.values[s:e][keep])
+        offs.append(offs[-1] + int(keep.sum()))
+    return O.CSR(rows.shape[0], rows.shape[0], np.asarray(offs, dtype=np.int64), np.concatenate(cols),
+                 np.concatenate(vals))
+
+
 # ---------------------------------------------------------------- outer sync
 
 
 OUTER = ["outer/cfg1_16_fixed", "outer/cfg1_16_literal", "outer/cfg3_16_paper",
-         "outer/cfg3_16_true", "outer/box_12_222", "outer/cfg5_12_o2", "outer/o1_10_211"]
+         "outer/cfg3_16_true", "outer/box_12_222", "outer/cfg5_12_o2", "outer/o1_10_211",
+         "outer/jac_10_112", "outer/jac_8_221_o1"]
 
 
 @pytest.mark.parametrize("key", OUTER)
