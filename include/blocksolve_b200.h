@@ -230,6 +230,14 @@ int bs_ipc_close(void *base);
 int bs_uniform_pcg64(double *out, int64_t n, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
                      uint64_t inc_lo, double low, double high, void *stream);
 
+/* Power-iteration vector helpers (linalg.py:243-276).
+ * bs_vec_nrm2: work[0] = ||x||_2 (device memory, work >= BS_VEC_WORK doubles),
+ * fixed reduction order — bitwise repeatable.  bs_vec_scale: y = x / denom
+ * elementwise (y may alias x). */
+#define BS_VEC_WORK 512
+int bs_vec_nrm2(const double *x, int64_t n, double *work, void *stream);
+int bs_vec_scale(const double *x, int64_t n, double denom, double *y, void *stream);
+
 /* Number of kernels this library has launched (process lifetime). */
 unsigned long long bs_launch_count(void);
 

@@ -817,3 +817,69 @@ def outer_solve_sync(shape, b: np.ndarray, block_grid, overlap: int, inner: dict
 def seeded_rhs(n: int, seed: int = 0) -> np.ndarray:
     """SURVEY §8(d) convention: default_rng(seed).uniform(-1, 1, n), x-fastest."""
     return np.random.default_rng(seed).uniform(-1.0, 1.0, n)
+
+
+# --------------------------------------------------------------------------
+# spectral diagnostics  (linalg.py:234-276, multisplit.py:800-830)
+# --------------------------------------------------------------------------
+
+
+@dataclass
+class Spectral:
+    """Mirror of ``SpectralEstimate`` (linalg.py:234-240)."""
+
+    radius: float
+    iterations_used: int
+    converged: bool
+
+
+def power_iteration(apply_map: Callable, dim: int, tol: float = 1e-10, max_iterations: int = 5000,
+                    seed: int = 0) -> Spectral:
+    """Power method restating ``power_iteration`` (linalg.py:243-276)."""
+    if dim < 1:
+        raise ValueError("dim must be at least 1")
+    if tol <= 0:
+        raise ValueError("tol must be positive")
+    x = 1.0 + np.random.default_rng(seed).random(dim)
+    x /= np.linalg.norm(x)
+    previous = np.inf
+    estimate = 0.0
+    for it in range(1, max_iterations + 1):
+        y = np.asarray(apply_map(x), dtype=np.float64)
+        estimate = float(np.linalg.norm(y))
+        if estimate == 0.0:
+            return Spectral(0.0, it, True)
+        if abs(estimate - previous) < tol:
+            return Spectral(estimate, it, True)
+        previous = estimate
+        x = y / estimate
+    return Spectral(estimate, max_iterations, False)
+
+
+def iteration_operator(shape, block_grid, overlap: int):
+    """The exact-inner-solve outer iteration z -> M^-1 N z on stacked extended
+    vectors, restating ``iteration_operator`` (multisplit.py:800-830) with
+    dense block solves (small grids only)."""
+    n = shape[0] * shape[1] * shape[2]
+    _, wss, _, _ = build_workspaces(shape, np.zeros(n), block_grid, overlap)
+    dense = [ws.a_ii.to_dense() for ws in wss]
+    offsets = np.concatenate(([0], np.cumsum([ws.ext.shape[0] for ws in wss])))
+
+    def apply(z):
+        parts = [z[offsets[i]:offsets[i + 1]] for i in range(len(wss))]
+        out = np.empty_like(z)
+        for i, ws in enumerate(wss):
+            if ws.halo_cols.size:
+                acc = np.zeros(ws.halo_cols.shape[0])
+                for q in ws.neighbors:
+                    payload = parts[q][wss[q].send_idx[i]]
+                    sel, slots = ws.recv_halo[q]
+                    if sel.size:
+                        acc[slots] += payload[sel]
+                rhs = -csr_spmv(ws.coupling, acc / ws.m_halo)
+            else:
+                rhs = np.zeros(ws.ext.shape[0])
+            out[offsets[i]:offsets[i + 1]] = np.linalg.solve(dense[i], rhs)
+        return out
+
+    return apply, int(offsets[-1])

@@ -6,6 +6,7 @@ for that path; every numerical step runs in the hand-written CUDA kernels of
 ``csrc/bs_engine.cu`` behind the C ABI of ``include/blocksolve_b200.h``.
 """
 
+from .diagnostics import SpectralEstimate, iteration_operator, jacobi_iteration_operator, power_iteration
 from .errors import (ConfigurationError, DeviceError, ProtocolError, SolverBreakdownError,
                      ZeroRhsError)
 from .inner_solvers import InnerSolveReport, InnerSolverSpec, cg_solve, gmres_solve, jacobi_solve, solve
@@ -23,5 +24,6 @@ __all__ = [
     "ProtocolError", "ResidualTrace", "SolveResult", "SolverBreakdownError", "StencilOperator",
     "TRACE_HEADER", "TraceRow", "ZeroRhsError", "build_laplace_3d", "cg_solve",
     "check_termination", "combined_residual", "decompose", "gmres_solve", "jacobi_solve", "outer_solve",
-    "residual_norms", "seeded_rhs", "solve", "spmv",
+    "residual_norms", "seeded_rhs", "solve", "spmv", "SpectralEstimate", "iteration_operator",
+    "jacobi_iteration_operator", "power_iteration",
 ]

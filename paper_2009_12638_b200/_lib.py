@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("BS_LIB") or os.path.join(HERE, "_lib", "libbsgpu.so")
 NDIR = 6
 STOP_NAMES = {0: "none", 1: "tolerance_met", 2: "max_iterations", 3: "breakdown", 4: "stalled"}
 BASIS = {"rhs": 0, "initial": 1}
+VEC_WORK = 512  # BS_VEC_WORK
 
 
 class BlockDesc(ctypes.Structure):
@@ -68,6 +69,8 @@ _SIGS = {
     "bs_stencil_apply": ([_P, _I, _P, _P, _P], _I),
     "bs_cg_begin": ([_P, _I, ctypes.c_double, _I, _P, _P], _I),
     "bs_jacobi_begin": ([_P, _I, ctypes.c_double, _I, _P, _P], _I),
+    "bs_vec_nrm2": ([_P, ctypes.c_int64, _P, _P], _I),
+    "bs_vec_scale": ([_P, ctypes.c_int64, ctypes.c_double, _P, _P], _I),
     "bs_sweep_resid": ([_P, _P], _I),
     "bs_cancel": ([_P, _P, _P], _I),
     "bs_run": ([_P, _I, _I, _P, ctypes.POINTER(ctypes.c_int64)], _I),

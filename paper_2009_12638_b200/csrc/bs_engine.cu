@@ -1555,6 +1555,39 @@ __global__ void k_pcg64_uniform(double *out, long long n, unsigned long long s_h
     }
 }
 
+// ------------------------------------------------------------------ vector helpers
+// Power-iteration support (linalg.py:243-276): ||x||_2 with a fixed
+// reduction order (VEC_CTAS grid-stride partials, then one ordered tree), so
+// repeats are bitwise identical on any GPU; y = x / d elementwise.
+constexpr int VEC_CTAS = 296, VEC_NT = 256;
+
+__global__ void __launch_bounds__(VEC_NT) k_vec_sq_partial(const double *__restrict__ x, long long n,
+                                                            double *__restrict__ part) {
+    __shared__ double red[VEC_NT / 32];
+    double s = 0.0;
+    for (long long i = (long long)blockIdx.x * VEC_NT + threadIdx.x; i < n; i += (long long)VEC_CTAS * VEC_NT)
+        s = add(s, mul(x[i], x[i]));
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = red[0];
+        for (int w = 1; w < VEC_NT / 32; ++w) t = add(t, red[w]);
+        part[blockIdx.x] = t;
+    }
+}
+
+__global__ void __launch_bounds__(VEC_NT) k_vec_sq_final(double *work) {
+    __shared__ double scratch[256];
+    const double v = range_sum<VEC_NT>(work + 1, 0, VEC_CTAS, scratch);
+    if (threadIdx.x == 0) work[0] = sqrt(v);
+}
+
+__global__ void k_vec_div(const double *__restrict__ x, long long n, double d, double *__restrict__ y) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        y[i] = __ddiv_rn(x[i], d);
+}
+
 // ------------------------------------------------------------------ host helpers
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -2377,6 +2410,26 @@ int bs_uniform_pcg64(double *out, int64_t n, uint64_t state_hi, uint64_t state_l
     ++g_launches;
     k_pcg64_uniform<<<(unsigned)((threads + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
         out, n, state_hi, state_lo, inc_hi, inc_lo, low, high - low, chunk);
+    BS_CU(cudaGetLastError());
+    return BS_OK;
+}
+
+int bs_vec_nrm2(const double *x, int64_t n, double *work, void *stream) {
+    if (!work || n < 0 || (n > 0 && !x)) return fail(BS_EINVAL, "bs_vec_nrm2: bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    g_launches += 2;
+    k_vec_sq_partial<<<VEC_CTAS, VEC_NT, 0, st>>>(x, n, work + 1);
+    k_vec_sq_final<<<1, VEC_NT, 0, st>>>(work);
+    BS_CU(cudaGetLastError());
+    return BS_OK;
+}
+
+int bs_vec_scale(const double *x, int64_t n, double denom, double *y, void *stream) {
+    if (n < 0 || (n > 0 && (!x || !y))) return fail(BS_EINVAL, "bs_vec_scale: bad arguments");
+    if (n == 0) return BS_OK;
+    ++g_launches;
+    const long long blocks = std::min<long long>((n + 255) / 256, 148LL * 8);
+    k_vec_div<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(x, n, denom, y);
     BS_CU(cudaGetLastError());
     return BS_OK;
 }

@@ -32,8 +32,10 @@ from blocksolve import (  # noqa: E402  (reference, read-only)
     cg_solve,
     decompose,
     gmres_solve,
+    iteration_operator,
     jacobi_solve,
     outer_solve,
+    power_iteration,
     spmv,
 )
 
@@ -154,6 +156,26 @@ def main():
     pr = problem(4, 4, 4, rhs=np.zeros(64))
     x, rep = jacobi_solve(pr.matrix, pr.rhs, np.zeros(64), InnerSolverSpec("jacobi", 5, 0.0))
     add_report("jacobi/zero_rhs", x, rep)
+
+    # -- spectral diagnostics (linalg.py:243-276, multisplit.py:800-830)
+    def est_meta(e):
+        return dict(radius=e.radius, iterations_used=e.iterations_used, converged=e.converged)
+
+    meta["power/diag123"] = est_meta(power_iteration(lambda v: np.array([1.0, 2.0, 3.0]) * v, 3, tol=1e-12,
+                                                     seed=1))
+    lap8 = problem(8, 8, 8).matrix
+    meta["power/jacobi_8"] = est_meta(power_iteration(lambda v: v - spmv(lap8, v) / 6.0, 512, tol=1e-10,
+                                                      seed=1))
+    pr = problem(4, 4, 4, {"x_lo": 1.0, "y_hi": 0.5})
+    apply_map, dim = iteration_operator(pr, decompose(pr.grid, (2, 1, 1), 0))
+    arrays["itop/4_211_o0/matrix"] = np.stack([apply_map(e) for e in np.eye(dim)], axis=1)
+    for n, bg, ov in ((4, (2, 1, 1), 0), (4, (2, 2, 1), 1), (8, (2, 1, 1), 0), (8, (4, 1, 1), 0),
+                      (6, (1, 1, 3), 0), (6, (2, 2, 2), 1)):
+        pr = problem(n, n, n, {"x_lo": 1.0, "y_hi": 0.5})
+        dec = decompose(pr.grid, bg, ov)
+        apply_map, dim = iteration_operator(pr, dec)
+        key = "itop/%d_%d%d%d_o%d" % ((n,) + bg + (ov,))
+        meta[key] = dict(dim=dim, **est_meta(power_iteration(apply_map, dim, tol=1e-10, seed=0)))
 
     # -- outer sync traces (multisplit.py:742-797)
     cases = {

@@ -282,3 +282,47 @@ def test_threaded_csr_bit_identical():
     a = lap((16, 16, 16))
     x = A["spmv/16x16x16/x"]
     assert np.array_equal(O.ThreadedCSR(a, 3)(x), A["spmv/16x16x16/y"])
+
+
+# ---------------------------------------------------------------- spectral diagnostics
+
+
+def test_power_iteration_matches_reference():
+    M = meta()
+    e = O.power_iteration(lambda v: np.array([1.0, 2.0, 3.0]) * v, 3, tol=1e-12, seed=1)
+    ref = M["power/diag123"]
+    assert (e.iterations_used, e.converged) == (ref["iterations_used"], ref["converged"])
+    assert e.radius == ref["radius"]
+    a = lap((8, 8, 8))
+    e = O.power_iteration(lambda v: v - O.csr_spmv(a, v) / 6.0, 512, tol=1e-10, seed=1)
+    ref = M["power/jacobi_8"]
+    assert (e.iterations_used, e.converged, e.radius) == (ref["iterations_used"], ref["converged"], ref["radius"])
+    # known answers (test_linalg.py:163-195 restated)
+    assert O.power_iteration(lambda v: np.zeros_like(v), 5, seed=0) == O.Spectral(0.0, 1, True)
+    with pytest.raises(ValueError):
+        O.power_iteration(lambda v: v, 0)
+    with pytest.raises(ValueError):
+        O.power_iteration(lambda v: v, 3, tol=0.0)
+
+
+def test_iteration_operator_matrix_matches_reference():
+    A = arrays()
+    apply, dim = O.iteration_operator((4, 4, 4), (2, 1, 1), 0)
+    assert dim == 64
+    mat = np.stack([apply(e) for e in np.eye(dim)], axis=1)
+    assert np.abs(mat - A["itop/4_211_o0/matrix"]).max() <= 1e-14
+
+
+@pytest.mark.parametrize("key", ["itop/4_211_o0", "itop/4_221_o1", "itop/8_211_o0", "itop/8_411_o0",
+                                 "itop/6_113_o0", "itop/6_222_o1"])
+def test_iteration_operator_radius_matches_reference(key):
+    ref = meta()[key]
+    n, bg, ov = key.split("/")[1].split("_")
+    n, bg, ov = int(n), tuple(int(c) for c in bg), int(ov[1:])
+    apply, dim = O.iteration_operator((n, n, n), bg, ov)
+    assert dim == ref["dim"]
+    e = O.power_iteration(apply, dim, tol=1e-10, seed=0)
+    assert e.converged == ref["converged"]
+    if ref["converged"]:
+        assert abs(e.iterations_used - ref["iterations_used"]) <= 1
+    assert e.radius == pytest.approx(ref["radius"], rel=1e-9)
