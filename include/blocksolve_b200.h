@@ -214,6 +214,20 @@ int bs_async_post(bs_ctx *ctx, int block, int dir, double *ring, uint64_t *seqs,
 int bs_async_receive(bs_ctx *ctx, int block, int ghost_dir, const double *ring, const uint64_t *seqs, int R,
                      uint64_t *applied, double *stage, int *torn, void *stream);
 
+/* Injected-latency variants (DelayModel, comm.py:51-81 and 376-416; SURVEY
+ * §8(f) item 4).  The sender picks the ring slot itself (its host keeps the
+ * reference's R-slot in-flight accounting: reclaim once the receiver reached
+ * the delivery iteration, skip the send when no slot is free) and stamps
+ * deliver[slot] = deliver_at (sender iteration + drawn delay) before the seq
+ * release.  The receiver only considers slots with deliver[slot] <=
+ * receiver_k, the outer iteration it has reached.  deliver == NULL gives the
+ * plain calls above. */
+int bs_async_post_slot(bs_ctx *ctx, int block, int dir, double *ring, uint64_t *seqs, int64_t *deliver, int slot,
+                       uint64_t seq, int64_t deliver_at, void *stream);
+int bs_async_receive_at(bs_ctx *ctx, int block, int ghost_dir, const double *ring, const uint64_t *seqs,
+                        const int64_t *deliver, int R, int64_t receiver_k, uint64_t *applied, double *stage,
+                        int *torn, void *stream);
+
 /* Peer memory for one-sided halo puts across processes (one process per GPU,
  * NVLink): export a device pointer as a 64-byte CUDA IPC handle of its
  * allocation plus the offset inside it; open it in another process (peer

@@ -69,6 +69,8 @@ _SIGS = {
     "bs_stencil_apply": ([_P, _I, _P, _P, _P], _I),
     "bs_cg_begin": ([_P, _I, ctypes.c_double, _I, _P, _P], _I),
     "bs_jacobi_begin": ([_P, _I, ctypes.c_double, _I, _P, _P], _I),
+    "bs_async_post_slot": ([_P, _I, _I, _P, _P, _P, _I, ctypes.c_uint64, ctypes.c_int64, _P], _I),
+    "bs_async_receive_at": ([_P, _I, _I, _P, _P, _P, _I, ctypes.c_int64, _P, _P, _P, _P], _I),
     "bs_vec_nrm2": ([_P, ctypes.c_int64, _P, _P], _I),
     "bs_vec_scale": ([_P, ctypes.c_int64, ctypes.c_double, _P, _P], _I),
     "bs_sweep_resid": ([_P, _P], _I),

@@ -20,6 +20,17 @@ The global estimate is the square root of the sum of every block's latest
 published local residual squared (+inf until all blocks published once),
 refreshed every ``residual_check_every`` sweeps; when it drops below ``tol``
 the blocks meet in a confirmation round whose exact sum decides.
+
+Injected latency (``OuterConfig.delay``, comm.py:51-81): on top of the real
+asynchrony, every halo post and every published residual carries a delivery
+iteration ``k + d`` (d drawn from the seeded DelayModel; drop_free_jitter
+clamps it to be non-decreasing per channel).  A receiver that has begun
+sweep s only accepts payloads with delivery <= s - 1 (its last exchange
+iteration, the reference's unit), and a sender keeps the reference's R-slot
+pool: a slot is in flight until the receiver reached its delivery iteration,
+a post finding no free slot is skipped (comm.py:376-400).  Each ring has one
+extra slot reserved for the confirmation round's flush, which is never
+delayed (comm.py:542-598).
 """
 
 from __future__ import annotations
@@ -34,21 +45,29 @@ from . import _lib
 from .engine import BlockEngine, box_halo_plan, launch_bound, torch
 from .errors import SolverBreakdownError
 
-RING_SLOTS_MAX = 8  # real hardware has no injected delays: deeper rings only hold stale planes
+RING_SLOTS_MAX = 8  # without injected delays deeper rings only hold stale planes
+NO_FILTER = (1 << 63) - 1  # receiver_k that accepts every published slot
 
 
 class _Mailbox:
-    """Directed channel src -> dst, memory owned by dst."""
+    """Directed channel src -> dst, memory owned by dst.  Slots 0..R-1 carry
+    sweep posts, slot R the (never delayed) confirmation flush."""
 
     def __init__(self, dst: int, ghost_dir: int, src: int, plane: int, slots: int, device):
         self.dst, self.ghost_dir, self.src = dst, ghost_dir, src
         self.post_dir = 5 - ghost_dir  # the sender's own boundary plane facing the receiver
         self.R = slots
-        self.ring = torch.zeros(slots, plane, dtype=torch.float64, device=device)
-        self.seqs = torch.zeros(slots, dtype=torch.int64, device=device)
+        self.ring = torch.zeros(slots + 1, plane, dtype=torch.float64, device=device)
+        self.seqs = torch.zeros(slots + 1, dtype=torch.int64, device=device)
+        self.deliver = torch.zeros(slots + 1, dtype=torch.int64, device=device)
         self.applied = torch.zeros(1, dtype=torch.int64, device=device)
         self.stage = torch.zeros(plane, dtype=torch.float64, device=device)
         self.torn = torch.zeros(1, dtype=torch.int32, device=device)
+        # sender-side pool (HaloBufferPool, comm.py:94-132): slot -> delivery iteration
+        self.in_flight: dict = {}
+        self.last_delivery = -1
+        self.next_slot = 0
+        self.skipped = 0
 
 
 class _Board:
@@ -58,6 +77,8 @@ class _Board:
         self.nb = nb
         self.lock = threading.Lock()
         self.local_sq = [math.inf] * nb
+        self.progress = [0] * nb        # sweep each block has begun
+        self.pub = [[] for _ in range(nb)]  # delayed model: (deliver_at, value) per publisher
         self.confirm_requested = False
         self.stop = False
         self.converged = False
@@ -70,6 +91,20 @@ class _Board:
             total = float(sum(self.local_sq[w] for w in range(self.nb)))  # block order (comm.py:443-445)
         return math.sqrt(total) if math.isfinite(total) else math.inf
 
+    def estimate_delayed(self, reader: int, k: int) -> float:
+        """Reader's view under injected latency: its own latest value, and for
+        every other block the freshest one whose delivery iteration <= k."""
+        with self.lock:
+            vals = []
+            for w in range(self.nb):
+                if w == reader:
+                    vals.append(self.local_sq[w])
+                    continue
+                seen = [v for t, v in self.pub[w] if t <= k]
+                vals.append(seen[-1] if seen else math.inf)
+            total = float(sum(vals))
+        return math.sqrt(total) if math.isfinite(total) else math.inf
+
 
 def outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, spec):
     """Run the asynchronous two-stage solve; returns the pieces of a SolveResult."""
@@ -77,7 +112,13 @@ def outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, spec):
     nx, ny, nz = grid.shape
     nb = decomp.num_blocks
     every = max(1, int(getattr(config, "residual_check_every", 1)))
-    slots = max(1, min(int(config.buffer_slots), RING_SLOTS_MAX))
+    delay = config.delay
+    delayed = delay.kind != "none"
+    # with injected delays the reference's pool depth matters (sends are
+    # skipped when R are in flight), so keep it; otherwise a short ring
+    slots = max(1, int(config.buffer_slots) if delayed else min(int(config.buffer_slots), RING_SLOTS_MAX))
+    rng = np.random.default_rng(delay.seed)
+    rng_lock = threading.Lock()
     engines, streams = [], []
     with torch.cuda.device(dev):
         for i in range(nb):
@@ -113,10 +154,16 @@ def outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, spec):
                 estimate = math.inf
                 k = 0
                 while True:
-                    for mb in incoming[b]:  # freshest delivered payloads (comm.py:401-416)
-                        _lib.check(lib.bs_async_receive(eng.ctx, 0, mb.ghost_dir, mb.ring.data_ptr(),
-                                                        mb.seqs.data_ptr(), mb.R, mb.applied.data_ptr(),
-                                                        mb.stage.data_ptr(), mb.torn.data_ptr(), st))
+                    with board.lock:
+                        board.progress[b] = k
+                    # freshest delivered payloads (comm.py:401-416); under injected
+                    # latency only those due by the last exchange iteration k - 1
+                    limit = k - 1 if delayed else NO_FILTER
+                    for mb in incoming[b]:
+                        _lib.check(lib.bs_async_receive_at(eng.ctx, 0, mb.ghost_dir, mb.ring.data_ptr(),
+                                                           mb.seqs.data_ptr(), mb.deliver.data_ptr(), mb.R + 1,
+                                                           limit, mb.applied.data_ptr(), mb.stage.data_ptr(),
+                                                           mb.torn.data_ptr(), st))
                     begin = eng.cg_begin if spec.kind == "cg" else eng.jacobi_begin
                     begin(spec.max_iterations, spec.tolerance, config.tolerance_basis)
                     eng.run(batch=config.batch, max_launches=launch_bound(spec.max_iterations, config.batch))
@@ -125,8 +172,7 @@ def outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, spec):
                         raise SolverBreakdownError(b, k, f"{spec.kind} reported breakdown")
                     its = int(rep.iterations_used)
                     for mb in outgoing[b]:  # one-sided puts, never blocking (comm.py:380-400)
-                        _lib.check(lib.bs_async_post(eng.ctx, 0, mb.post_dir, mb.ring.data_ptr(),
-                                                     mb.seqs.data_ptr(), mb.R, 2 * k, st))
+                        _post(eng, mb, k, st)
                     # seq = 2k (sweep post) or 2k+1 (confirm flush): monotonic per channel
                     applied = [(int(mb.applied.item()) - 1) // 2 for mb in incoming[b]]
                     staleness = max([k - a for a in applied if a >= 0] + [0])
@@ -134,7 +180,10 @@ def outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, spec):
                         val = local_residual(b)
                         with board.lock:
                             board.local_sq[b] = val
-                        estimate = board.estimate()
+                            if delayed:
+                                board.pub[b].append((k + _draw(), val))
+                                _prune(board.pub[b], min(board.progress))
+                        estimate = board.estimate_delayed(b, k) if delayed else board.estimate()
                         if estimate < config.tol:
                             board.confirm_requested = True
                     if k + 1 >= config.max_outer:
@@ -149,6 +198,40 @@ def outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, spec):
             board.stop = True
             board.barrier.abort()
 
+    def _draw() -> int:
+        with rng_lock:  # one seeded stream shared by every channel (comm.py:236)
+            return delay.draw(rng)
+
+    def _prune(entries: list, floor: int) -> None:
+        """Drop publications superseded by a newer one every reader already sees."""
+        while len(entries) > 1 and entries[1][0] <= floor:
+            entries.pop(0)
+
+    def _post(eng, mb, k: int, st) -> None:
+        if not delayed:
+            slot = k % mb.R
+            _lib.check(eng.lib.bs_async_post_slot(eng.ctx, 0, mb.post_dir, mb.ring.data_ptr(), mb.seqs.data_ptr(),
+                                                  mb.deliver.data_ptr(), slot, 2 * k, 0, st))
+            return
+        with board.lock:
+            reached = board.progress[mb.dst] - 1  # receiver's last exchange iteration
+        mb.in_flight = {s_: t for s_, t in mb.in_flight.items() if t > reached}  # reclaim (comm.py:111-112)
+        free = [s_ for s_ in range(mb.R) if s_ not in mb.in_flight]
+        if not free:
+            mb.skipped += 1  # exhausted pool: skip, never block (comm.py:392-393)
+            return
+        deliver_at = k + _draw()
+        if delay.kind == "drop_free_jitter":
+            deliver_at = max(deliver_at, mb.last_delivery)
+        mb.last_delivery = deliver_at
+        # rotate through the free slots so a just-delivered payload is not
+        # overwritten before the receiver copies it
+        slot = min(free, key=lambda s_: (s_ - mb.next_slot) % mb.R)
+        mb.next_slot = (slot + 1) % mb.R
+        mb.in_flight[slot] = deliver_at
+        _lib.check(eng.lib.bs_async_post_slot(eng.ctx, 0, mb.post_dir, mb.ring.data_ptr(), mb.seqs.data_ptr(),
+                                              mb.deliver.data_ptr(), slot, 2 * k, deliver_at, st))
+
     def _confirm(b: int, k: int) -> bool:
         """Confirmation round (comm.py:542-598): flush current payloads, recompute
         the local residues on that consistent snapshot, exact sum.  Also the
@@ -159,18 +242,22 @@ def outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, spec):
             board.barrier.wait()
             if board.stop and not board.confirm_requested:
                 return True
-            for mb in outgoing[b]:
-                _lib.check(eng.lib.bs_async_post(eng.ctx, 0, mb.post_dir, mb.ring.data_ptr(), mb.seqs.data_ptr(),
-                                                 mb.R, 2 * k + 1, st))
+            for mb in outgoing[b]:  # the reserved slot R: a synchronous, undelayed flush
+                _lib.check(eng.lib.bs_async_post_slot(eng.ctx, 0, mb.post_dir, mb.ring.data_ptr(),
+                                                      mb.seqs.data_ptr(), mb.deliver.data_ptr(), mb.R, 2 * k + 1,
+                                                      0, st))
             torch.cuda.current_stream(dev).synchronize()
             board.barrier.wait()
             for mb in incoming[b]:
-                _lib.check(eng.lib.bs_async_receive(eng.ctx, 0, mb.ghost_dir, mb.ring.data_ptr(), mb.seqs.data_ptr(),
-                                                    mb.R, mb.applied.data_ptr(), mb.stage.data_ptr(),
-                                                    mb.torn.data_ptr(), st))
+                _lib.check(eng.lib.bs_async_receive_at(eng.ctx, 0, mb.ghost_dir, mb.ring.data_ptr(),
+                                                       mb.seqs.data_ptr(), mb.deliver.data_ptr(), mb.R + 1,
+                                                       NO_FILTER, mb.applied.data_ptr(), mb.stage.data_ptr(),
+                                                       mb.torn.data_ptr(), st))
             board.confirm_sq[b] = local_residual(b)
             with board.lock:
                 board.local_sq[b] = board.confirm_sq[b]
+                if delayed:
+                    board.pub[b].append((-1, board.confirm_sq[b]))  # the flush is seen by everyone
             board.barrier.wait()
             total = float(sum(board.confirm_sq[w] for w in range(nb)))
             done = math.sqrt(total) < config.tol
@@ -201,8 +288,9 @@ def outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, spec):
             eng.gather_owned(sol)
         torch.cuda.synchronize(dev)
         torn = int(sum(int(mb.torn.item()) for lst in incoming for mb in lst))
+        skipped = int(sum(mb.skipped for lst in incoming for mb in lst))
         for eng in engines:
             eng.close()
     # a lapped read (sender overwrote the slot mid-copy) kept the old halo,
     # i.e. behaved like "no fresh payload delivered"; reported, not an error
-    return sol, records, board.converged, torn
+    return sol, records, board.converged, torn, skipped

@@ -20,14 +20,15 @@ import numpy as np
 
 from .errors import ConfigurationError, DeviceError, ProtocolError, SolverBreakdownError
 from .inner_solvers import InnerSolverSpec, solve
-from .multisplit import OuterConfig, ResidualTrace, TraceRow, outer_solve
+from .multisplit import DelayModel, OuterConfig, ResidualTrace, TraceRow, outer_solve
 from .problems import FACES, DirichletBoundary, Grid3D, build_laplace_3d
 
 DEFAULTS = {
     "nx": "8", "ny": "8", "nz": "8", "boundary": "faces:x_lo=1", "gx": "1", "gy": "1", "gz": "1",
     "overlap": "0", "inner": "gmres", "inner_its": "10", "inner_tol": "0", "restart": "", "mode": "sync",
     "R": "100", "tol": "1e-6", "max_outer": "5000", "residual_mode": "paper", "true_res_every": "10",
-    "exec": "replay", "out": "trace.csv", "tolerance_basis": "rhs", "device": "cuda",
+    "exec": "replay", "out": "trace.csv", "tolerance_basis": "rhs", "device": "cuda", "delay": "none",
+    "seed": "0",
 }
 
 
@@ -58,6 +59,24 @@ def boundary_from(raw: str) -> DirichletBoundary:
             faces[name] = _float(value, "boundary")
         return DirichletBoundary(faces)
     raise ConfigurationError(f"boundary: expected const:v or faces:name=v,... got {raw!r}")
+
+
+def parse_delay(raw: str, seed: int) -> DelayModel:
+    """``none``, ``fixed:d``, ``uniform:lo:hi`` or ``jitter:lo:hi`` (cli.py:82-100)."""
+    parts = raw.split(":")
+    kind = parts[0]
+    try:
+        if kind == "none" and len(parts) == 1:
+            return DelayModel(seed=seed)
+        if kind == "fixed" and len(parts) == 2:
+            return DelayModel("fixed", fixed=int(parts[1]), seed=seed)
+        if kind == "uniform" and len(parts) == 3:
+            return DelayModel("uniform", low=int(parts[1]), high=int(parts[2]), seed=seed)
+        if kind in ("jitter", "drop_free_jitter") and len(parts) == 3:
+            return DelayModel("drop_free_jitter", low=int(parts[1]), high=int(parts[2]), seed=seed)
+    except ValueError:
+        raise ConfigurationError(f"delay: invalid delay bounds in {raw!r}") from None
+    raise ConfigurationError(f"delay: expected none, fixed:d, uniform:lo:hi or jitter:lo:hi, got {raw!r}")
 
 
 def read_config_file(path: str) -> dict:
@@ -103,7 +122,8 @@ def run(cfg: dict) -> tuple:
             mode=mode, buffer_slots=_int(cfg["R"], "R"), tol=_float(cfg["tol"], "tol"),
             max_outer=_int(cfg["max_outer"], "max_outer"), residual_check_mode=cfg["residual_mode"],
             true_residual_interval=_int(cfg["true_res_every"], "true_res_every"), execution=cfg["exec"],
-            tolerance_basis=cfg["tolerance_basis"], device=cfg["device"])
+            tolerance_basis=cfg["tolerance_basis"], device=cfg["device"],
+            delay=parse_delay(cfg["delay"], _int(cfg["seed"], "seed")))
         res = outer_solve(problem, config)
         trace, converged, outer = res.trace, res.converged, res.outer_iterations
         inner = sum(r.inner_iterations for r in trace.rows)

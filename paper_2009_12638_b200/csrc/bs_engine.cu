@@ -1433,18 +1433,22 @@ __host__ __device__ __forceinline__ long long plane_len(const int *pdim, int dir
 
 // Seqlock writer side: retire the slot before its payload is overwritten, so
 // a reader that picked the slot's previous seq fails its re-validation.
-__global__ void k_async_retire(unsigned long long *seqs, int R, unsigned long long seq) {
-    *((volatile unsigned long long *)&seqs[seq % (unsigned long long)R]) = 0ull;
+__global__ void k_async_retire(unsigned long long *seqs, int slot) {
+    *((volatile unsigned long long *)&seqs[slot]) = 0ull;
     __threadfence_system();
 }
 
+// Payload (x + pending alpha p of the boundary plane) into ring slot `sl`;
+// the last CTA stamps the delivery iteration (injected-delay model, may be
+// null) and then publishes seq+1 with a system-scope release.
 __global__ void k_async_post(const DBlock *__restrict__ blocks, const DState *states, int b, int dir, double *ring,
-                             unsigned long long *seqs, int R, unsigned long long seq, unsigned *counter) {
+                             unsigned long long *seqs, int sl, unsigned long long seq, long long *deliver,
+                             long long deliver_at, unsigned *counter) {
     const DBlock &B = blocks[b];
     const DState &S = states[b];
     const int nu = plane_nu(B.pdim, dir);
     const long long n = plane_len(B.pdim, dir);
-    double *slot = ring + (long long)(seq % (unsigned long long)R) * n;
+    double *slot = ring + (long long)sl * n;
     const double a = S.alpha_pend;
     const bool pend = S.pend != 0;
     const double *p = B.p[S.pcur];
@@ -1464,22 +1468,28 @@ __global__ void k_async_post(const DBlock *__restrict__ blocks, const DState *st
     }
     __syncthreads();
     if (last && threadIdx.x == 0) {
+        if (deliver) *((volatile long long *)&deliver[sl]) = deliver_at;
         __threadfence_system();  // payload visible system-wide before the seq (release)
-        *((volatile unsigned long long *)&seqs[seq % (unsigned long long)R]) = seq + 1;  // 0 = empty slot
+        *((volatile unsigned long long *)&seqs[sl]) = seq + 1;  // 0 = empty slot
         *counter = 0u;
     }
 }
 
 // pick[0] = chosen seq+1 (0: nothing newer), pick[1] = slot
-__global__ void k_async_pick(const unsigned long long *seqs, int R, const unsigned long long *applied,
-                             unsigned long long *pick) {
+// Freshest published slot; with a delivery table only slots whose delivery
+// iteration the receiver has reached (deliver <= receiver_k) qualify.
+__global__ void k_async_pick(const unsigned long long *seqs, const long long *deliver, int R, long long receiver_k,
+                             const unsigned long long *applied, unsigned long long *pick) {
     unsigned long long best = 0, slot = 0;
     for (int s = 0; s < R; ++s) {
         const unsigned long long v = ((const volatile unsigned long long *)seqs)[s];
-        if (v > best) {
-            best = v;
-            slot = s;
+        if (v <= best) continue;
+        if (deliver) {
+            __threadfence_system();  // the stamp was written before the seq
+            if (((const volatile long long *)deliver)[s] > receiver_k) continue;
         }
+        best = v;
+        slot = s;
     }
     __threadfence_system();  // acquire: payload reads below follow the seq read
     pick[0] = best > *applied ? best : 0ull;
@@ -2369,22 +2379,35 @@ int bs_owner_residual(bs_ctx *c, void *stream) {
     return BS_OK;
 }
 
-int bs_async_post(bs_ctx *c, int block, int dir, double *ring, uint64_t *seqs, int R, uint64_t seq,
-                  void *stream) {
-    if (!c || block < 0 || block >= c->nblocks || dir < 0 || dir >= BS_NDIR || !ring || !seqs || R < 1)
+int bs_async_post_slot(bs_ctx *c, int block, int dir, double *ring, uint64_t *seqs, int64_t *deliver, int slot,
+                       uint64_t seq, int64_t deliver_at, void *stream) {
+    if (!c || block < 0 || block >= c->nblocks || dir < 0 || dir >= BS_NDIR || !ring || !seqs || slot < 0)
         return fail(BS_EINVAL, "bs_async_post: bad arguments");
     if (int e = set_dev(c)) return e;
     g_launches += 2;
-    k_async_retire<<<1, 1, 0, (cudaStream_t)stream>>>((unsigned long long *)seqs, R, (unsigned long long)seq);
+    k_async_retire<<<1, 1, 0, (cudaStream_t)stream>>>((unsigned long long *)seqs, slot);
     k_async_post<<<64, 256, 0, (cudaStream_t)stream>>>(c->dblocks, c->dstates, block, dir, ring,
-                                                       (unsigned long long *)seqs, R, (unsigned long long)seq,
+                                                       (unsigned long long *)seqs, slot, (unsigned long long)seq,
+                                                       (long long *)deliver, (long long)deliver_at,
                                                        c->dpost_counter);
     BS_CU(cudaGetLastError());
     return BS_OK;
 }
 
+int bs_async_post(bs_ctx *c, int block, int dir, double *ring, uint64_t *seqs, int R, uint64_t seq,
+                  void *stream) {
+    if (R < 1) return fail(BS_EINVAL, "bs_async_post: bad arguments");
+    return bs_async_post_slot(c, block, dir, ring, seqs, nullptr, (int)(seq % (uint64_t)R), seq, 0, stream);
+}
+
 int bs_async_receive(bs_ctx *c, int block, int ghost_dir, const double *ring, const uint64_t *seqs, int R,
                      uint64_t *applied, double *stage, int *torn, void *stream) {
+    return bs_async_receive_at(c, block, ghost_dir, ring, seqs, nullptr, R, 0, applied, stage, torn, stream);
+}
+
+int bs_async_receive_at(bs_ctx *c, int block, int ghost_dir, const double *ring, const uint64_t *seqs,
+                        const int64_t *deliver, int R, int64_t receiver_k, uint64_t *applied, double *stage,
+                        int *torn, void *stream) {
     if (!c || block < 0 || block >= c->nblocks || ghost_dir < 0 || ghost_dir >= BS_NDIR || !ring || !seqs || R < 1 ||
         !applied || !stage || !torn)
         return fail(BS_EINVAL, "bs_async_receive: bad arguments");
@@ -2393,7 +2416,8 @@ int bs_async_receive(bs_ctx *c, int block, int ghost_dir, const double *ring, co
     cudaStream_t st = (cudaStream_t)stream;
     const long long n = plane_len(c->hblocks[block].pdim, ghost_dir);
     g_launches += 4;
-    k_async_pick<<<1, 1, 0, st>>>((const unsigned long long *)seqs, R, (const unsigned long long *)applied, c->dpick);
+    k_async_pick<<<1, 1, 0, st>>>((const unsigned long long *)seqs, (const long long *)deliver, R,
+                                  (long long)receiver_k, (const unsigned long long *)applied, c->dpick);
     k_async_copy<<<64, 256, 0, st>>>(c->dblocks, block, ghost_dir, ring, n, c->dpick, stage);
     k_async_check<<<1, 1, 0, st>>>((const unsigned long long *)seqs, c->dpick, (unsigned long long *)applied, torn);
     k_async_apply<<<64, 256, 0, st>>>(c->dblocks, block, ghost_dir, n, c->dpick, stage);

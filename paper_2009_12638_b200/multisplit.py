@@ -57,8 +57,12 @@ DEFAULT_BUFFER_SLOTS = 100
 
 @dataclass(frozen=True)
 class DelayModel:
-    """Injected delay (comm.py:51-81).  Accepted for API compatibility; the
-    device path has real asynchrony and only supports kind='none'."""
+    """In-flight delay distribution in receiver outer iterations (comm.py:51-81).
+
+    Async mode adds it on top of the device path's real asynchrony: halo posts
+    and published residuals become visible k + d iterations after they were
+    sent (see ``async_driver``).  Sync mode ignores it, as the reference's
+    rendezvous exchanges do."""
 
     kind: str = "none"
     fixed: int = 0
@@ -73,6 +77,14 @@ class DelayModel:
             raise ConfigurationError("delay: fixed delay must be non-negative")
         if self.kind in ("uniform", "drop_free_jitter") and not (0 <= self.low <= self.high):
             raise ConfigurationError("delay: bounds must satisfy 0 <= low <= high")
+
+    def draw(self, rng: np.random.Generator) -> int:
+        """One delay (comm.py:76-81)."""
+        if self.kind == "none":
+            return 0
+        if self.kind == "fixed":
+            return self.fixed
+        return int(rng.integers(self.low, self.high + 1))
 
 
 @dataclass
@@ -212,8 +224,6 @@ def _validate_device_path(config: OuterConfig) -> None:
     if config.inner.kind not in ("jacobi", "cg", "gmres"):
         raise ConfigurationError(
             f"inner: {config.inner.kind!r} is outside the accelerated path (device kinds: jacobi, cg, gmres)")
-    if config.delay.kind != "none":
-        raise ConfigurationError("delay: injected delays are a simulation knob; use kind='none'")
 
 
 def outer_solve(problem: LinearProblem, config: OuterConfig) -> SolveResult:
@@ -292,7 +302,7 @@ def _outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, on_devi
     from .linalg import residual_norms
 
     grid = problem.grid
-    sol, records, converged, lapped = outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev,
+    sol, records, converged, lapped, skipped = outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev,
                                                        config.inner)
     flat = sol.reshape(-1)
     final_true = residual_norms(problem.matrix, flat, b_dev.reshape(-1))[1]
@@ -311,4 +321,4 @@ def _outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, on_devi
     return SolveResult(solution=solution, trace=ResidualTrace(rows), converged=converged, outer_iterations=outer,
                        final_true_residual=final_true, inner_iterations_per_block=per_block,
                        wall_seconds=time.perf_counter() - t_start,
-                       comm_events=[("lapped_reads", lapped)])
+                       comm_events=[("lapped_reads", lapped), ("skipped_sends", skipped)])

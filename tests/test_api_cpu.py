@@ -120,3 +120,23 @@ def test_solver_kind_routing():
     assert set(DEVICE_KINDS) < set(SOLVER_KINDS)
     with pytest.raises(bs.ConfigurationError, match="outside the accelerated path"):
         bs.solve(bs.StencilOperator(2, 2, 2), np.ones(8), np.zeros(8), bs.InnerSolverSpec("direct", 1))
+
+
+def test_delay_model_draws_like_the_reference():
+    """DelayModel.draw (comm.py:76-81) and the CLI spelling (cli.py:82-100)."""
+    from paper_2009_12638_b200.cli import parse_delay
+
+    rng = np.random.default_rng(3)
+    assert bs.DelayModel().draw(rng) == 0
+    assert bs.DelayModel("fixed", fixed=4).draw(rng) == 4
+    m = bs.DelayModel("uniform", low=1, high=3, seed=7)
+    r1, r2 = np.random.default_rng(7), np.random.default_rng(7)
+    assert [m.draw(r1) for _ in range(50)] == [int(r2.integers(1, 4)) for _ in range(50)]
+    assert parse_delay("jitter:2:5", 9) == bs.DelayModel("drop_free_jitter", low=2, high=5, seed=9)
+    assert parse_delay("fixed:3", 0) == bs.DelayModel("fixed", fixed=3)
+    with pytest.raises(bs.ConfigurationError, match="delay"):
+        parse_delay("fixed", 0)
+    with pytest.raises(bs.ConfigurationError, match="delay"):
+        parse_delay("uniform:a:b", 0)
+    with pytest.raises(bs.ConfigurationError, match="delay"):
+        bs.DelayModel("uniform", low=3, high=1)
