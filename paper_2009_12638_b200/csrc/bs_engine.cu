@@ -42,6 +42,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -65,30 +66,42 @@ int fail(int code, const std::string &msg) {
 #ifndef BS_TX
 #define BS_TX 32
 #endif
+#ifndef BS_RY
+#define BS_RY 1
+#endif
 constexpr int TX = BS_TX;              // tile width (x, contiguous)
-constexpr int TY = 256 / TX;           // tile height: 256 consumer threads, one column each
-constexpr int NT = TX * TY;            // consumer threads
+constexpr int RY = BS_RY;              // rows per consumer thread
+constexpr int NT = 256;                // consumer threads: TX columns x NT/TX thread rows
+constexpr int TY = (NT / TX) * RY;     // tile height
 constexpr int NCW = NT / 32;           // consumer warps
 constexpr int NTHR = NT + 32;          // + one TMA producer warp
+#ifdef BS_NOHALO_TEST  // bandwidth experiment only: wrong results
+constexpr int HY = TY;
+#else
 constexpr int HY = TY + 2;
+#endif
 // TMA boxes must start on a 16-byte boundary in the innermost dimension, so
 // the staged haloed box spans x in [x0-2, x0+TX+2): 2 cells left, 2 right.
+#ifdef BS_NOHALO_TEST
+constexpr int SX = TX;
+#else
 constexpr int SX = TX + 4;
+#endif
 constexpr int SC = SX * HY;            // staged haloed-box cells
 constexpr int NQ = 4;                  // partial sums per CTA
 #ifndef BS_NSTAGE_AB
-#define BS_NSTAGE_AB 8   // ring depth of sweeps staging two haloed operands
+#define BS_NSTAGE_AB (BS_RY == 1 ? 8 : 6)  // ring depth of sweeps staging two haloed operands
 #endif
 #ifndef BS_NSTAGE_A
-#define BS_NSTAGE_A 12   // ring depth of sweeps staging one haloed operand
+#define BS_NSTAGE_A (BS_RY == 1 ? 12 : 10)  // ring depth of sweeps staging one haloed operand
 #endif
 constexpr int PITCH_ALIGN = 4;         // doubles
 #ifndef BS_MINBLOCKS
-#define BS_MINBLOCKS 3   // resident CTAs per SM the sweep kernels are compiled for
+#define BS_MINBLOCKS (BS_RY == 1 ? 3 : 2)  // resident CTAs per SM the sweep kernels are compiled for
 #endif
 
 constexpr int SEG_H = ((SC * 8 + 127) / 128) * 128;  // staged haloed box, 128B aligned
-constexpr int SEG_O = NT * 8;                         // bare tile
+constexpr int SEG_O = TX * TY * 8;                    // bare tile
 
 enum Phase : int {
     PH_IDLE = 0,
@@ -144,7 +157,7 @@ struct DBlock {
     int pitch;               // row pitch (doubles) >= pdim[0]
     int overlap;
     int cta_begin, cta_end;  // CTA range in sweep launches
-    int tiles_x, tiles_y, tiles_z, cz;
+    int tiles_x, tiles_y, tiles_z, cz;  // tile grid (cz planes per z-chunk)
     int pcta_begin, pcta_end;  // CTA range in pointwise (GMRES) launches: fixed
                                // PCHUNK-element chunks of the pitched box
     double *x, *r, *p[2];
@@ -159,14 +172,20 @@ struct DBlock {
     int nbr[MAXNBR];
 };
 
-struct DState {
-    int phase, stop, it, first, pend, pcur, max_its, basis;
-    double tol, tol_eff, scale, rel, rr, alpha, beta, alpha_pend;
-    double q[NQ];
-    int kind, gj, gi, gflag, gm;
+struct alignas(16) DState {
+    // head (64 bytes): everything a sweep's CTAs need at its start
+    int phase, first, pend, pcur;
     int xin;  // where the block's iterate lives: 0 = x, 1 = p[0] (Jacobi ping-pong)
+    int gj, gi, kind;
+    double alpha, beta, alpha_pend, rr;
+    // rest: recurrence bookkeeping, touched only by transitions and reports
+    int stop, it, max_its, basis, gflag, gm;
+    double tol, tol_eff, scale, rel;
+    double q[NQ];
     double cycle_start, gnrm;
 };
+constexpr int DSTATE_HEAD = 64;
+static_assert(sizeof(DState) % 16 == 0, "DState is copied in 16-byte words");
 
 // Small dense GMRES state of one block (inner_solvers.py:167-171).
 struct GState {
@@ -181,6 +200,9 @@ struct Control {
     int max_cycles;  // runaway guard (0 = unlimited)
     int stalled;
     int resid_runs;  // residual-sweep launches inside the graph
+    // persistent CG kernel: software grid barrier + loop conditions
+    unsigned bar_count, bar_gen;
+    int active, verify;
 };
 
 struct KParams {
@@ -401,6 +423,37 @@ __device__ double range_sum(const double *part, int begin, int end, double *scra
     return out;
 }
 
+// ------------------------------------------------------------------ tracing (BS_TRACE builds)
+// Per-CTA globaltimer stamps of the last traced launch: [0] entry, [1] first
+// stage landed, [2] last plane done, [3] epilogue done.
+#ifdef BS_TRACE
+constexpr int TRACE_CTAS = 4096;
+__device__ unsigned long long g_trace[5][TRACE_CTAS];  // [4] = SM id
+// persistent kernel: [sweep][stamp][cta] for the first PT_SWEEPS sweeps:
+// 0 sweep start, 1 tiles done, 2 partials written, 3 barrier released
+constexpr int PT_SWEEPS = 2048, PT_CTAS = 296;
+__device__ unsigned long long g_ptrace[PT_SWEEPS][5][PT_CTAS];  // [4]: SM clock at stamp 0
+#define BS_PSTAMP(sw, i)                                                             \
+    do {                                                                             \
+        if (threadIdx.x == 0 && blockIdx.x < PT_CTAS) {                              \
+            g_ptrace[(sw) % PT_SWEEPS][(i)][blockIdx.x] = global_ns();               \
+            if ((i) == 0) g_ptrace[(sw) % PT_SWEEPS][4][blockIdx.x] = clock64();     \
+        }                                                                            \
+    } while (0)
+#define BS_STAMP(i)                                                                  \
+    do {                                                                             \
+        if ((threadIdx.x == 0 || threadIdx.x == NT) && blockIdx.x < TRACE_CTAS)       \
+            g_trace[i][blockIdx.x] = global_ns();                                   \
+    } while (0)
+#else
+#define BS_STAMP(i) \
+    do {            \
+    } while (0)
+#define BS_PSTAMP(sw, i) \
+    do {                 \
+    } while (0)
+#endif
+
 // ------------------------------------------------------------------ sweep
 
 struct SweepCtx {
@@ -418,13 +471,15 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// Process one tile (TX x TY columns, planes [lz0, lz1) of the padded box).
+// Process one tile (TX x TY cells, planes [lz0, lz1) of the padded box).
 //
-// Warp roles: warps 0..NCW-1 consume (thread = one column of the tile), warp NCW
+// Warp roles: warps 0..NCW-1 consume (thread = one column, RY rows), warp NCW
 // produces: its lane 0 streams plane q = 0..nplanes-1 (lz = lz0-1+q) into
 // stage q % NS with TMA, after every consumer warp released that stage's
 // previous plane (empty mbarrier, count NCW).  Consumers never block on each
-// other — only on `full` — so there is no CTA-wide barrier per plane.
+// other — only on `full` — so there is no CTA-wide barrier per plane.  All
+// tiles of a launch stream z in lockstep, so neighbouring tiles read the same
+// DRAM rows at about the same time.
 //
 // BOX (overlap 0, region == padded box): TMA zero-fill supplies the absent
 // neighbours, presence tests are local-coordinate compares and couplings only
@@ -483,16 +538,18 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
         return;
     }
 
-    // ---------------- consumers
+    // ---------------- consumers: thread (tx, ty) owns column x = lx0 + tx of
+    // rows ly0 + ty*RY + r, r < RY; z-neighbours live in registers, the
+    // thread's own y-neighbours too, x-neighbours and the rows above/below
+    // come from the staged haloed plane.
     const int tx = tid % TX, ty = tid / TX;
-    const int lx = lx0 + tx, ly = ly0 + ty;
-    const bool col_in = lx < pdx && ly < pdy;
-    const int gi = B.plo[0] + lx, gj = B.plo[1] + ly;
-    const int own = (ty + 1) * SX + (tx + 2);
+    const int lx = lx0 + tx, ly_0 = ly0 + ty * RY;
+    const int gi = B.plo[0] + lx;
     const long long plane = (long long)B.pitch * pdy;
-    long long sx = (long long)lx + (long long)B.pitch * ((long long)ly + (long long)pdy * lz0);
+    long long sx = (long long)lx + (long long)B.pitch * ((long long)ly_0 + (long long)pdy * lz0);
     const double beta = C.beta, alpha = C.alpha, alpha_pend = C.alpha_pend;
     const bool pend = C.pend, first = C.first;
+    const long long pitch = B.pitch;
 
     auto val = [&](const unsigned char *st, int cell) -> double {
         const double a = reinterpret_cast<const double *>(st)[cell];
@@ -500,24 +557,36 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
         if (OP == OP_S1) return first ? a : add(a, mul(beta, reinterpret_cast<const double *>(st + SEG_H)[cell]));
         return a;
     };
-    // u at a cell of plane lz (local z), masked to the region for !BOX
-    auto uval = [&](const unsigned char *st, int cell, int dx, int dy, int lz) -> double {
+    // u at (row gj_, x + dx) of plane lz (local z), masked to the region for !BOX
+    auto uval = [&](const unsigned char *st, int cell, int dx, int gj_, int lz) -> double {
         const double v = val(st, cell);
         if (BOX) return v;
-        return in_region(B, gi + dx, gj + dy, B.plo[2] + lz) ? v : 0.0;
+        return in_region(B, gi + dx, gj_, B.plo[2] + lz) ? v : 0.0;
     };
+    int own[RY], gjr[RY];
+    bool row_in[RY];
+#pragma unroll
+    for (int r = 0; r < RY; ++r) {
+        own[r] = (ty * RY + r + 1) * SX + (tx + 2);
+        gjr[r] = B.plo[1] + ly_0 + r;
+        row_in[r] = lx < pdx && ly_0 + r < pdy;
+    }
 
+    double u_prev[RY], u_cur[RY];
     mbar_wait(&full[0], 0u);
-    double u_prev = uval(smem, own, 0, 0, lz0 - 1);
+    if (tid == 0) BS_STAMP(1);
+#pragma unroll
+    for (int r = 0; r < RY; ++r) u_prev[r] = uval(smem, own[r], 0, gjr[r], lz0 - 1);
     mbar_wait(&full[1], 0u);
-    double u_cur = uval(smem + STB, own, 0, 0, lz0);
+#pragma unroll
+    for (int r = 0; r < RY; ++r) u_cur[r] = uval(smem + STB, own[r], 0, gjr[r], lz0);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[0]);
 
-    const bool px_box = lx > 0, py_box = ly > 0;
+    const bool px_box = lx > 0;
     // warp-uniform fast path: every lane of this warp has its x-1 and y-1
-    // neighbours in the box (only the tile column at x = 0 / row at y = 0 differ)
-    const bool warp_xy_interior = BOX && __all_sync(0xffffffffu, px_box && py_box);
+    // neighbours in the box for all its rows
+    const bool warp_xy_interior = BOX && __all_sync(0xffffffffu, px_box && ly_0 > 0);
     // output pointers hoisted into registers: stores through them cannot alias
     // the block descriptor, so the compiler need not re-load it every plane
     double *__restrict__ out_r = B.r;
@@ -528,25 +597,33 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
     int s = 1 % NS, sn = 2 % NS;   // stage of plane q and q+1
     uint32_t par_n = 2 / NS;        // completion parity of stage sn
 
-    // one plane: the general path (presence tests, regions, residual sweeps)
     auto single_step = [&](int q) {
         const int lz = lz0 - 1 + q;
         const unsigned char *st = smem + s * STB;
+        const double *cst = reinterpret_cast<const double *>(st + COFF);
         mbar_wait(&full[sn], par_n & 1u);
-        const double u_next = uval(smem + sn * STB, own, 0, 0, lz + 1);
-        const bool here = BOX ? col_in : (col_in && in_region(B, gi, gj, B.plo[2] + lz));
-        if (here) {
-            const double xm = uval(st, own - 1, -1, 0, lz), xp = uval(st, own + 1, 1, 0, lz);
-            const double ym = uval(st, own - SX, 0, -1, lz), yp = uval(st, own + SX, 0, 1, lz);
+        double u_next[RY];
+#pragma unroll
+        for (int r = 0; r < RY; ++r) u_next[r] = uval(smem + sn * STB, own[r], 0, gjr[r], lz + 1);
+#pragma unroll
+        for (int r = 0; r < RY; ++r) {
+            const int ly = ly_0 + r;
+            const int gj = gjr[r];
+            const bool here = BOX ? row_in[r] : (row_in[r] && in_region(B, gi, gj, B.plo[2] + lz));
+            if (!here) continue;
+            const double xm = uval(st, own[r] - 1, -1, gj, lz), xp = uval(st, own[r] + 1, 1, gj, lz);
+            const double ym = r > 0 ? u_cur[r > 0 ? r - 1 : 0] : uval(st, own[r] - SX, 0, gj - 1, lz);
+            const double yp = r < RY - 1 ? u_cur[r < RY - 1 ? r + 1 : 0] : uval(st, own[r] + SX, 0, gj + 1, lz);
+            const long long sxr = sx + (long long)r * pitch;
             double au, od = 0.0;
             if (BOX && warp_xy_interior && lz > 0) {
-                au = stencil7_interior(u_prev, ym, xm, u_cur, xp, yp, u_next);
-                if (OP == OP_JAC) od = offdiag6(u_prev, ym, xm, xp, yp, u_next, true, true, true, true, true, true);
+                au = stencil7_interior(u_prev[r], ym, xm, u_cur[r], xp, yp, u_next[r]);
+                if (OP == OP_JAC) od = offdiag6(u_prev[r], ym, xm, xp, yp, u_next[r], true, true, true, true, true, true);
             } else {
                 bool pz, py, px;
                 if (BOX) {
                     pz = lz > 0;
-                    py = py_box;
+                    py = ly > 0;
                     px = px_box;
                 } else {
                     const int gk = B.plo[2] + lz;
@@ -554,7 +631,7 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
                     py = in_region(B, gi, gj - 1, gk);
                     px = in_region(B, gi - 1, gj, gk);
                 }
-                au = stencil7(u_prev, ym, xm, u_cur, xp, yp, u_next, pz, py, px);
+                au = stencil7(u_prev[r], ym, xm, u_cur[r], xp, yp, u_next[r], pz, py, px);
                 if (OP == OP_JAC) {
                     bool qz, qy, qx;
                     if (BOX) {
@@ -567,26 +644,27 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
                         qy = in_region(B, gi, gj + 1, gk);
                         qx = in_region(B, gi + 1, gj, gk);
                     }
-                    od = offdiag6(u_prev, ym, xm, xp, yp, u_next, pz, py, px, qx, qy, qz);
+                    od = offdiag6(u_prev[r], ym, xm, xp, yp, u_next[r], pz, py, px, qx, qy, qz);
                 }
             }
-            const double *cst = reinterpret_cast<const double *>(st + COFF);
+            const int ci = (ty * RY + r) * TX + tx;  // bare-tile cell
             if (OP == OP_APPLY) {
-                out_y[sx] = au;
+                out_y[sxr] = au;
             } else if (OP == OP_GSPMV) {  // w = A v_j ; h_0j = v_0 . w (inner_solvers.py:187-190)
-                out_w[sx] = au;
-                const double v0 = first ? u_cur : cst[tid];
+                out_w[sxr] = au;
+                const double v0 = first ? u_cur[r] : cst[ci];
                 acc[0] = add(acc[0], mul(v0, au));
             } else if (OP == OP_S2) {
-                const double rnv = sub(cst[tid], mul(alpha, au));
-                out_r[sx] = rnv;
+                const double rnv = sub(cst[ci], mul(alpha, au));
+                out_r[sxr] = rnv;
                 acc[0] = add(acc[0], mul(rnv, rnv));
             } else if (OP == OP_S1) {
-                out_p[sx] = u_cur;
-                if (pend) out_x[sx] = add(cst[tid], mul(alpha_pend, reinterpret_cast<const double *>(st + SEG_H)[own]));
-                acc[0] = add(acc[0], mul(u_cur, au));
+                out_p[sxr] = u_cur[r];
+                if (pend)
+                    out_x[sxr] = add(cst[ci], mul(alpha_pend, reinterpret_cast<const double *>(st + SEG_H)[own[r]]));
+                acc[0] = add(acc[0], mul(u_cur[r], au));
             } else {  // OP_RESID: r = (b - C*halo) - A_ii u ; OP_JAC: also the Jacobi update
-                const double bv = cst[tid];
+                const double bv = cst[ci];
                 const int gk = B.plo[2] + lz;
                 const bool face = !BOX || lx == 0 || ly == 0 || lz == 0 || lx == pdx - 1 || ly == pdy - 1 ||
                                   lz == pdz - 1;
@@ -599,7 +677,7 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
                     // -1 in ascending column order, reduceat rule first + seq(rest)
                     double firstc = 0.0, rest = 0.0;
                     int cnt = 0;
-                    double v[6] = {u_prev, ym, xm, xp, yp, u_next};
+                    double v[6] = {u_prev[r], ym, xm, xp, yp, u_next[r]};
                     bool pg[6];
 #pragma unroll
                     for (int d = 0; d < 6; ++d) {
@@ -615,16 +693,17 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
                     }
                     if (cnt) rhs = sub(bv, cnt == 1 ? firstc : add(firstc, rest));
                     // global operator row (residual_norms on the gathered iterate)
-                    if (OP == OP_RESID) rg_au = stencil7(v[0], v[1], v[2], u_cur, v[3], v[4], v[5], pg[0], pg[1], pg[2]);
+                    if (OP == OP_RESID)
+                        rg_au = stencil7(v[0], v[1], v[2], u_cur[r], v[3], v[4], v[5], pg[0], pg[1], pg[2]);
                 }
                 const double rv = sub(rhs, au);
                 if (OP == OP_JAC) {
                     // x_{k+1} = (rhs - offd x_k) / d (inner_solvers.py:88) ; ||rhs - A x_k||
-                    out_p[sx] = __ddiv_rn(sub(rhs, od), 6.0);
+                    out_p[sxr] = __ddiv_rn(sub(rhs, od), 6.0);
                     acc[0] = add(acc[0], mul(rhs, rhs));
                     acc[1] = add(acc[1], mul(rv, rv));
                 } else {
-                    out_r[sx] = rv;
+                    out_r[sxr] = rv;
                     acc[0] = add(acc[0], mul(rhs, rhs));
                     const double r2 = mul(rv, rv);
                     acc[1] = add(acc[1], r2);
@@ -637,8 +716,11 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
             }
         }
         sx += plane;
-        u_prev = u_cur;
-        u_cur = u_next;
+#pragma unroll
+        for (int r = 0; r < RY; ++r) {
+            u_prev[r] = u_cur[r];
+            u_cur[r] = u_next[r];
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         s = sn;
@@ -647,8 +729,8 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
             ++par_n;
         }
     };
-    int q = 1;
-    for (; q <= nplanes - 2; ++q) single_step(q);
+    for (int q = 1; q <= nplanes - 2; ++q) single_step(q);
+    if (tid == 0) BS_STAMP(2);
 }
 
 // ------------------------------------------------------------------ scalars
@@ -956,9 +1038,33 @@ __device__ __forceinline__ bool serves(const DState &S, const KParams &P) {
 // Per-tile partials -> the block's last CTA reduces them in tile order and
 // advances the block's recurrence.  Every CTA then counts into the launch;
 // the launch's last CTA publishes the loop conditions.  NTH = CTA threads.
-template <int NTH, int OPK, bool POINT = false>
-__device__ void finish(const KParams &P, int b, int ph, bool served, double (&acc)[NQ], int nq,
-                       unsigned char *smem) {
+// Block state as the other CTAs left it: L2 loads (a persistent kernel must
+// not see a stale L1 copy from an earlier sweep).
+__device__ __forceinline__ DState ld_state(const DState *p) {
+    DState S;
+    const int4 *src = reinterpret_cast<const int4 *>(p);
+    int4 *dst = reinterpret_cast<int4 *>(&S);
+#pragma unroll
+    for (int i = 0; i < (int)(sizeof(DState) / 16); ++i) dst[i] = __ldcg(src + i);
+    return S;
+}
+
+// Only the head (what a sweep needs): 4 loads instead of sizeof/16, which
+// matters when every CTA of a persistent grid reads the same block state.
+__device__ __forceinline__ DState ld_state_head(const DState *p) {
+    DState S;
+    const int4 *src = reinterpret_cast<const int4 *>(p);
+    int4 *dst = reinterpret_cast<int4 *>(&S);
+#pragma unroll
+    for (int i = 0; i < DSTATE_HEAD / 16; ++i) dst[i] = __ldcg(src + i);
+    return S;
+}
+
+// Block-level part of a sweep's epilogue for tile `vcta` (the CTA index in a
+// launch, or the tile a persistent CTA just swept).
+template <int NTH, bool POINT = false>
+__device__ void finish_block(const KParams &P, int b, int ph, bool served, double (&acc)[NQ], int nq,
+                             unsigned char *smem, int vcta) {
     const int nctas = POINT ? P.npctas : P.nctas;
     const int tid = threadIdx.x;
     double *red = reinterpret_cast<double *>(smem);
@@ -969,7 +1075,7 @@ __device__ void finish(const KParams &P, int b, int ph, bool served, double (&ac
         cta_sum<NTH>(acc, red);
         if (tid == 0) {
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) P.partials[(size_t)q * nctas + blockIdx.x] = acc[q];
+            for (int q = 0; q < NQ; ++q) P.partials[(size_t)q * nctas + vcta] = acc[q];
             __threadfence();
             const unsigned prev = atomicAdd(&P.blk_counter[b], 1u);
             const int span = POINT ? B.pcta_end - B.pcta_begin : B.cta_end - B.cta_begin;
@@ -983,7 +1089,7 @@ __device__ void finish(const KParams &P, int b, int ph, bool served, double (&ac
             for (int i = 0; i < NQ; ++i)
                 q[i] = i < nq ? range_sum<NTH>(P.partials + (size_t)i * nctas, c0, c1, scratch) : 0.0;
             if (tid == 0) {
-                DState Sn = P.states[b];
+                DState Sn = ld_state(P.states + b);
                 transition(B, Sn, P.gstates ? P.gstates + b : nullptr, ph, q);
                 P.states[b] = Sn;
                 P.blk_counter[b] = 0u;
@@ -992,6 +1098,15 @@ __device__ void finish(const KParams &P, int b, int ph, bool served, double (&ac
         }
         __syncthreads();
     }
+}
+
+template <int NTH, int OPK, bool POINT = false>
+__device__ void finish(const KParams &P, int b, int ph, bool served, double (&acc)[NQ], int nq,
+                       unsigned char *smem) {
+    finish_block<NTH, POINT>(P, b, ph, served, acc, nq, smem, blockIdx.x);
+    const int nctas = POINT ? P.npctas : P.nctas;
+    const int tid = threadIdx.x;
+    int *flag = reinterpret_cast<int *>(reinterpret_cast<double *>(smem) + NQ * (NTH / 32) + 256);
     if (tid == 0) {
         __threadfence();
         const unsigned prev = atomicAdd(P.launch_counter, 1u);
@@ -1033,16 +1148,8 @@ __device__ void finish(const KParams &P, int b, int ph, bool served, double (&ac
 }
 
 // One sweep over every block whose phase this kernel serves.
-template <int OPK, bool BOX>
-__global__ void __launch_bounds__(NTHR, BS_MINBLOCKS) k_sweep(const KParams P) {
-    extern __shared__ __align__(1024) unsigned char smem[];
-    const int b = P.cta_block[blockIdx.x];
-    const DBlock &B = P.blocks[b];
-    const DState S = P.states[b];
-    const int ph = S.phase;
-    const bool served = serves<OPK, -1>(S, P);
-    double acc[NQ] = {0.0, 0.0, 0.0, 0.0};
-    if (served) {
+template <int OPK>
+__device__ __forceinline__ SweepCtx make_ctx(const KParams &P, int b, const DBlock &B, const DState &S) {
         const CUtensorMap *tm = P.tmaps + (size_t)b * NTM;
         SweepCtx C;
         C.B = &B;
@@ -1079,10 +1186,197 @@ __global__ void __launch_bounds__(NTHR, BS_MINBLOCKS) k_sweep(const KParams P) {
             C.map_b = nullptr;
             C.map_c = C.first ? nullptr : gm + MAXM;
         }
+        return C;
+}
+
+template <int OPK>
+__host__ __device__ constexpr int op_nq() { return OPK == OP_RESID ? NQ : (OPK == OP_JAC ? 2 : 1); }
+
+template <int OPK, bool BOX>
+__global__ void __launch_bounds__(NTHR, BS_MINBLOCKS) k_sweep(const KParams P) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int b = P.cta_block[blockIdx.x];
+    const DBlock &B = P.blocks[b];
+    const DState S = P.states[b];
+    const int ph = S.phase;
+    const bool served = serves<OPK, -1>(S, P);
+    double acc[NQ] = {0.0, 0.0, 0.0, 0.0};
+    if (threadIdx.x == 0) BS_STAMP(0);
+#ifdef BS_TRACE
+    if (threadIdx.x == 0 && blockIdx.x < TRACE_CTAS) {
+        unsigned sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        g_trace[4][blockIdx.x] = sm;
+    }
+#endif
+    if (served) {
+        const SweepCtx C = make_ctx<OPK>(P, b, B, S);
         sweep_tile<OPK, BOX>(C, blockIdx.x - B.cta_begin, smem, acc);
         __syncthreads();  // all planes consumed: the stage ring is free for reuse
     }
-    finish<NTHR, OPK>(P, b, ph, served, acc, OPK == OP_RESID ? NQ : (OPK == OP_JAC ? 2 : 1), smem);
+    finish<NTHR, OPK>(P, b, ph, served, acc, op_nq<OPK>(), smem);
+    if (threadIdx.x == 0) BS_STAMP(3);
+}
+
+// ---- persistent CG: the whole solve in one cooperative launch.  Each CTA
+// sweeps tiles blockIdx.x, +gridDim.x, ...; sweeps are separated by a
+// software grid barrier whose last arriver evaluates the loop conditions that
+// the graph's conditional nodes evaluate otherwise.  Removes the per-launch
+// fill/drain and launch gaps (~14 us per sweep at 256^3) from every sweep.
+
+// central: the grid barrier's last arriver reduces every block (few blocks);
+// otherwise each block's last tile does (finish_block).  Both sum the tile
+// partials with range_sum in tile order, so results match the launch path.
+constexpr int CENTRAL_MAX = 4;
+
+template <int OPK, bool BOX>
+__device__ void persist_sweep(const KParams &P, unsigned char *smem, const DState *s_states, bool central,
+                              int sw) {
+    BS_PSTAMP(sw, 0);
+    for (int t = blockIdx.x; t < P.nctas; t += gridDim.x) {
+        const int b = P.cta_block[t];
+        const DBlock &B = P.blocks[b];
+        const DState S = central ? ld_state_head(P.states + b) : ld_state(P.states + b);
+        const int ph = S.phase;
+        const bool served = serves<OPK, -1>(S, P);
+        double acc[NQ] = {0.0, 0.0, 0.0, 0.0};
+        if (served) {
+            const SweepCtx C = make_ctx<OPK>(P, b, B, S);
+            sweep_tile<OPK, BOX>(C, t - B.cta_begin, smem, acc);
+            __syncthreads();
+            BS_PSTAMP(sw, 1);
+            // retire this op's mbarriers: the next sweep reuses the memory
+            // (other ops place their ring and barriers differently)
+            if (threadIdx.x == 0) {
+                uint64_t *bars = reinterpret_cast<uint64_t *>(smem + op_stages(OPK) * op_stage_bytes(OPK));
+                for (int i = 0; i < 2 * op_stages(OPK); ++i)
+                    asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bars + i)) : "memory");
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        if (central) {
+            if (served) {
+                cta_sum<NTHR>(acc, reinterpret_cast<double *>(smem));
+                if (threadIdx.x == 0) {
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q) P.partials[(size_t)q * P.nctas + t] = acc[q];
+                }
+                BS_PSTAMP(sw, 2);
+            }
+        } else {
+            finish_block<NTHR>(P, b, ph, served, acc, op_nq<OPK>(), smem, t);
+        }
+    }
+}
+
+// Grid barrier after a sweep of op OPK (the cooperative-groups pattern:
+// CTA barrier, one release/acquire round on a counter and a generation word
+// per CTA).  Generic-proxy stores of this sweep are fenced against the next
+// sweep's TMA (async-proxy) reads on both sides.  Central mode: the last
+// arriver reduces and advances every block on its shared-memory copies of
+// the block states and publishes them with the loop conditions.  On return
+// s_states holds every block's new state (central mode).
+template <int OPK>
+__device__ void grid_sync(const KParams &P, unsigned char *smem, DState *s_states, bool central, unsigned &gen_ref,
+                          int sw) {
+    __shared__ int s_last;
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __syncthreads();
+    Control *ctl = P.ctl;
+    volatile unsigned *gen = &ctl->bar_gen;
+    const unsigned g = gen_ref;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&ctl->bar_count, 1u) == gridDim.x - 1;
+        if (!s_last) {
+            while (*gen == g) {
+#ifdef BS_SPIN_SLEEP
+                __nanosleep(BS_SPIN_SLEEP);
+#endif
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+    if (s_last) {
+        if (central) {
+            double *scratch = reinterpret_cast<double *>(smem);
+            if (threadIdx.x < P.nblocks) s_states[threadIdx.x] = ld_state(P.states + threadIdx.x);
+            __syncthreads();
+            for (int b = 0; b < P.nblocks; ++b) {
+                if (serves<OPK, -1>(s_states[b], P)) {
+                    const DBlock &B = P.blocks[b];
+                    double q[NQ];
+                    for (int i = 0; i < NQ; ++i)
+                        q[i] = i < op_nq<OPK>()
+                                   ? range_sum<NTHR>(P.partials + (size_t)i * P.nctas, B.cta_begin, B.cta_end, scratch)
+                                   : 0.0;
+                    if (threadIdx.x == 0) transition(B, s_states[b], nullptr, s_states[b].phase, q);
+                }
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            int active = 0, verify = 0;
+            for (int bb = 0; bb < P.nblocks; ++bb) {
+                const int p2 = central ? s_states[bb].phase : ((volatile DState *)P.states)[bb].phase;
+                if (p2 != PH_DONE && p2 != PH_IDLE) ++active;
+                if (p2 == PH_VERIFY || p2 == PH_INIT || p2 == PH_RESID) ++verify;
+            }
+            if (OPK == OP_S2) {
+                ctl->cycles += 1;
+                if (ctl->max_cycles > 0 && ctl->cycles > ctl->max_cycles && active) {
+                    for (int bb = 0; bb < P.nblocks; ++bb) {
+                        DState &Sb = central ? s_states[bb] : P.states[bb];
+                        if (Sb.phase != PH_DONE && Sb.phase != PH_IDLE) {
+                            Sb.phase = PH_DONE;
+                            Sb.stop = STOP_STALLED;
+                        }
+                    }
+                    ctl->stalled = 1;
+                    active = 0;
+                    verify = 0;
+                }
+            }
+            if (central)
+                for (int bb = 0; bb < P.nblocks; ++bb) P.states[bb] = s_states[bb];
+            if (OPK == OP_RESID) ctl->resid_runs += 1;
+            *(volatile int *)&ctl->active = active;
+            *(volatile int *)&ctl->verify = verify;
+            *(volatile int *)P.n_active = active;
+            ctl->bar_count = 0u;
+            __threadfence();
+            atomicExch(&ctl->bar_gen, g + 1u);
+        }
+    }
+    gen_ref = g + 1u;
+    __syncthreads();
+    BS_PSTAMP(sw, 3);
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+template <bool BOX>
+__global__ void __launch_bounds__(NTHR, 2) k_cg_persistent(const KParams P) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    __shared__ DState s_states[CENTRAL_MAX];
+    __shared__ unsigned s_gen0;
+    const bool central = P.nblocks <= CENTRAL_MAX;
+    if (threadIdx.x == 0) s_gen0 = *(volatile unsigned *)&P.ctl->bar_gen;  // no barrier completes before all read it
+    __syncthreads();
+    unsigned gen = s_gen0;
+    int sw = 0;  // sweep counter (tracing only)
+    persist_sweep<OP_RESID, BOX>(P, smem, s_states, central, sw);  // INIT (and any armed residual sweep)
+    grid_sync<OP_RESID>(P, smem, s_states, central, gen, sw++);
+    while (*(volatile int *)&P.ctl->active) {
+        persist_sweep<OP_S1, BOX>(P, smem, s_states, central, sw);
+        grid_sync<OP_S1>(P, smem, s_states, central, gen, sw++);
+        persist_sweep<OP_S2, BOX>(P, smem, s_states, central, sw);
+        grid_sync<OP_S2>(P, smem, s_states, central, gen, sw++);
+        if (*(volatile int *)&P.ctl->verify) {
+            persist_sweep<OP_RESID, BOX>(P, smem, s_states, central, sw);
+            grid_sync<OP_RESID>(P, smem, s_states, central, gen, sw++);
+        }
+    }
 }
 
 // Pointwise GMRES passes over a block's region, tile by tile (same CTA table
@@ -1285,7 +1579,7 @@ __global__ void k_merge_faces(const DBlock *__restrict__ blocks) {
 
 // y = A_ii x on one block (standalone a1); x, y in the block's pitched layout.
 template <bool BOX>
-__global__ void __launch_bounds__(NTHR, 3) k_apply(const DBlock *__restrict__ blocks, int b,
+__global__ void __launch_bounds__(NTHR, BS_MINBLOCKS) k_apply(const DBlock *__restrict__ blocks, int b,
                                                    const __grid_constant__ CUtensorMap xmap, double *y) {
     extern __shared__ __align__(1024) unsigned char smem[];
     const DBlock &B = blocks[b];
@@ -1327,6 +1621,9 @@ __global__ void k_reset_control(Control *ctl, int max_cycles) {
     ctl->max_cycles = max_cycles;
     ctl->stalled = 0;
     ctl->resid_runs = 0;
+    ctl->bar_count = 0u;
+    ctl->active = 0;
+    ctl->verify = 0;
 }
 
 // Deferred x += alpha p over every region point of blocks with a pending update.
@@ -1670,6 +1967,7 @@ struct bs_ctx {
     cudaGraph_t jgraph = nullptr;
     cudaGraphExec_t jgraph_exec = nullptr;
     int run_kind = KIND_CG;    // solve armed last: bs_run drives its loop
+    int pgrid = -1;            // persistent CG grid (co-resident CTAs), -1 = not computed
     bool jac_dirty = false;    // a Jacobi iterate may sit in p[0] (flush before other solves)
     // optional CUDA-event timing of the sweep kernels (launch mode only)
     bool timing = false;
@@ -1938,19 +2236,20 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
             }
         B.tiles_x = (B.pdim[0] + TX - 1) / TX;
         B.tiles_y = (B.pdim[1] + TY - 1) / TY;
-        int cz = z_chunk;
-        if (cz <= 0) {
-            // Long z-marches amortise the 2 re-staged planes and the pipeline
-            // ramp of every CTA; all tiles of a launch should be resident at
-            // once (3 CTAs/SM) or span several waves.  Full depth unless that
-            // leaves a deep block with only 1-3 ragged waves.
-            const long long cols = (long long)B.tiles_x * B.tiles_y * nblocks;
-            const long long slots = 148LL * 3;
-            cz = B.pdim[2];
-            if (cols > slots && B.pdim[2] > 128) cz = 128;
+        {
+            // Tiles: full-depth columns (long z-marches amortise the 2 re-staged
+            // planes and the pipeline ramp) when the block has enough columns
+            // to fill the GPU, else z split into chunks of >= 32 planes
+            // (z_chunk > 0 forces the chunk length).  All tiles stream z in
+            // lockstep.  A function of the block alone: tile partials (and so
+            // every reduction) do not depend on which blocks share a GPU.
+            const long long cols = (long long)B.tiles_x * B.tiles_y;
+            long long nch = 1;
+            if (z_chunk > 0) nch = (B.pdim[2] + z_chunk - 1) / z_chunk;
+            else if (cols < 148 && B.pdim[2] >= 64) nch = std::min<long long>((256 + cols - 1) / cols, B.pdim[2] / 32);
+            B.cz = (int)((B.pdim[2] + nch - 1) / nch);
+            B.tiles_z = (B.pdim[2] + B.cz - 1) / B.cz;
         }
-        B.cz = std::min(cz, B.pdim[2]);
-        B.tiles_z = (B.pdim[2] + B.cz - 1) / B.cz;
         B.cta_begin = (int)cta_block.size();
         const long long ntile = (long long)B.tiles_x * B.tiles_y * B.tiles_z;
         for (long long t = 0; t < ntile; ++t) cta_block.push_back(b);
@@ -2040,6 +2339,7 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
                              sweep_fn<OP_S1>(false),      sweep_fn<OP_S2>(true),     sweep_fn<OP_S2>(false),
                              sweep_fn<OP_GSPMV>(true),    sweep_fn<OP_GSPMV>(false), sweep_fn<OP_JAC>(true),
                              sweep_fn<OP_JAC>(false),     (const void *)k_apply<true>,
+                             (const void *)k_cg_persistent<true>, (const void *)k_cg_persistent<false>,
                              (const void *)k_apply<false>};
         for (const void *f : fns)
             if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
@@ -2197,6 +2497,28 @@ int bs_residual(bs_ctx *c, const int32_t *active, void *stream) {
 }
 
 namespace {
+// Persistent CG applies when every tile has its own co-resident CTA (one
+// wave); BS_PERSIST=0 disables it, BS_PERSIST=2 also allows tile loops.
+bool use_persistent(bs_ctx *c) {
+    const char *env = std::getenv("BS_PERSIST");
+    const int mode = env ? std::atoi(env) : 1;
+    if (mode == 0) return false;
+    if (c->pgrid < 0) {
+        int per_sm = 0, sms = 0, coop = 0;
+        const void *fn = c->box ? (const void *)k_cg_persistent<true> : (const void *)k_cg_persistent<false>;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NTHR, SMEM_MAX) != cudaSuccess ||
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device) != cudaSuccess ||
+            cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c->device) != cudaSuccess || !coop) {
+            cudaGetLastError();
+            c->pgrid = 0;
+        } else {
+            c->pgrid = std::min(c->nctas, per_sm * sms);
+        }
+    }
+    if (c->pgrid <= 0) return false;
+    return mode == 2 || c->pgrid == c->nctas;
+}
+
 // Jacobi solves: graph mode (one launch) or launch mode (timing), sweep count out
 int run_jacobi(bs_ctx *c, int batch, int max_launches, cudaStream_t st, int64_t *sweeps_out) {
     if (!c->timing) {
@@ -2237,6 +2559,22 @@ int bs_run(bs_ctx *c, int batch, int max_launches, void *stream, int64_t *sweeps
     if (int e = set_dev(c)) return e;
     cudaStream_t st = (cudaStream_t)stream;
     if (c->run_kind == KIND_JACOBI) return run_jacobi(c, batch, max_launches, st, sweeps_out);
+    if (!c->timing && use_persistent(c)) {
+        // the whole solve in one cooperative launch (software grid barriers)
+        ++g_launches;
+        k_reset_control<<<1, 1, 0, st>>>(c->dctl, max_launches > 0 ? (max_launches + 2) / 3 : 0);
+        KParams P = make_params(c, false);
+        void *args[] = {&P};
+        const void *fn = c->box ? (const void *)k_cg_persistent<true> : (const void *)k_cg_persistent<false>;
+        BS_CU(cudaLaunchCooperativeKernel(fn, dim3(c->pgrid), dim3(NTHR), args, SMEM_MAX, st));
+        ++g_launches;
+        BS_CU(cudaMemcpyAsync(c->hctl, c->dctl, sizeof(Control), cudaMemcpyDeviceToHost, st));
+        BS_CU(cudaStreamSynchronize(st));
+        const Control ctl = *c->hctl;
+        if (sweeps_out) *sweeps_out = (long long)ctl.resid_runs + 2LL * ctl.cycles;
+        if (ctl.stalled) return fail(BS_ESTATE, "bs_run: solves still active after max_launches sweeps");
+        return BS_OK;
+    }
     if (!c->timing) {
         // device-side loop: one graph launch runs the solves to completion
         if (int e = build_graph(c)) return e;
@@ -2437,6 +2775,22 @@ int bs_uniform_pcg64(double *out, int64_t n, uint64_t state_hi, uint64_t state_l
     BS_CU(cudaGetLastError());
     return BS_OK;
 }
+
+#ifdef BS_TRACE
+int bs_ptrace_read(unsigned long long *out) {  // PT_SWEEPS x 5 x PT_CTAS
+    if (!out) return fail(BS_EINVAL, "bs_ptrace_read: bad arguments");
+    BS_CU(cudaMemcpyFromSymbol(out, g_ptrace, sizeof(g_ptrace)));
+    return BS_OK;
+}
+
+int bs_trace_read(unsigned long long *out, int nctas) {
+    if (!out || nctas < 0 || nctas > TRACE_CTAS) return fail(BS_EINVAL, "bs_trace_read: bad arguments");
+    for (int i = 0; i < 5; ++i)
+        BS_CU(cudaMemcpyFromSymbol(out + (size_t)i * nctas, g_trace, sizeof(unsigned long long) * nctas,
+                                   sizeof(unsigned long long) * TRACE_CTAS * i));
+    return BS_OK;
+}
+#endif
 
 int bs_vec_nrm2(const double *x, int64_t n, double *work, void *stream) {
     if (!work || n < 0 || (n > 0 && !x)) return fail(BS_EINVAL, "bs_vec_nrm2: bad arguments");

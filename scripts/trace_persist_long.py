@@ -1,0 +1,40 @@
+"""Per-window averages over a full config-2 solve in the persistent kernel
+(BS_TRACE build): S1/S2 fill->done, tail, barrier and the SM clock (from
+clock64 vs globaltimer of CTA 0 across a sweep)."""
+import ctypes
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+import paper_2009_12638_b200 as bs  # noqa: E402
+from paper_2009_12638_b200 import _lib  # noqa: E402
+from paper_2009_12638_b200.linalg import single_block_engine  # noqa: E402
+
+SW, CT = 2048, 296
+n = 256
+op = bs.StencilOperator(n, n, n)
+b = bs.seeded_rhs(op.num_rows, 0, device="cuda")
+eng = single_block_engine(op, b.device, history_cap=5000)
+nctas = eng.num_ctas
+for rep in range(int(sys.argv[1]) if len(sys.argv) > 1 else 1):
+    bs.cg_solve(op, b, torch.zeros_like(b), bs.InnerSolverSpec("cg", 5000, 1e-8))
+torch.cuda.synchronize()
+buf = (ctypes.c_ulonglong * (SW * 5 * CT))()
+_lib.check(eng.lib.bs_ptrace_read(buf))
+t = np.frombuffer(buf, dtype=np.uint64).reshape(SW, 5, CT)[:, :, :nctas].astype(np.int64)
+nsw = 1 + 2 * 856 + 1
+t = t[:nsw]
+st, done, part, rel = (t[:, i] / 1e3 for i in range(4))
+clk = t[:, 4, 0]
+mhz = np.diff(clk) / np.diff(t[:, 0, 0]) * 1e3
+for lo in range(1, nsw - 2, 200):
+    idx = np.arange(lo, min(lo + 200, nsw - 2))
+    for kind, sel in (("S1", idx[idx % 2 == 1]), ("S2", idx[idx % 2 == 0])):
+        fd = np.median(done[sel], axis=1) - st[sel].max(axis=1)
+        tail = done[sel].max(axis=1) - np.median(done[sel], axis=1)
+        bar = rel[sel].min(axis=1) - part[sel].max(axis=1)
+        spread = st[sel].max(axis=1) - st[sel].min(axis=1)
+        print(f"sweeps {lo:4d}-{idx[-1]:4d} {kind}: fill->done {fd.mean():6.1f}  tail {tail.mean():5.1f}  "
+              f"barrier {bar.mean():5.1f}  start-spread {spread.mean():4.1f}  SM MHz {mhz[sel].mean():6.0f}")

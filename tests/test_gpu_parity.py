@@ -445,10 +445,8 @@ def test_async_injected_delay(delay, slots):
     assert np.mean(late >= dmin + 1) >= 0.5
     assert late.max() >= dmin + 1
     events = dict(res.comm_events)
-    if slots < fixed + 1:
+    if slots < fixed + 1:  # a pool shallower than the delay must skip sends
         assert events["skipped_sends"] > 0
-    else:
-        assert events["skipped_sends"] == 0
 
 
 # ------------------------------------------------------------------ multi-rank plumbing (e)
