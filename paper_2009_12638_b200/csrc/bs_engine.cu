@@ -71,7 +71,11 @@ int fail(int code, const std::string &msg) {
 #endif
 constexpr int TX = BS_TX;              // tile width (x, contiguous)
 constexpr int RY = BS_RY;              // rows per consumer thread
-constexpr int NT = 256;                // consumer threads: TX columns x NT/TX thread rows
+#ifndef BS_NT
+#define BS_NT 256
+#endif
+constexpr int NT = BS_NT;              // sweep consumer threads: TX columns x NT/TX thread rows
+constexpr int NPT = 256;               // threads of the pointwise (GMRES) passes
 constexpr int TY = (NT / TX) * RY;     // tile height
 constexpr int NCW = NT / 32;           // consumer warps
 constexpr int NTHR = NT + 32;          // + one TMA producer warp
@@ -408,10 +412,12 @@ __device__ __forceinline__ void cta_sum(double (&acc)[NQ], double *red) {
 template <int NTH>
 __device__ double range_sum(const double *part, int begin, int end, double *scratch) {
     const int tid = threadIdx.x;
-    if (tid < 256) {
+    // 256 virtual lanes whatever the CTA size, so the order is the same in
+    // every kernel: lane l sums part[begin + l + 256 k], then a binary tree
+    for (int l = tid; l < 256; l += NTH) {
         double s = 0.0;
-        for (int c = begin + tid; c < end; c += 256) s = add(s, __ldcg(part + c));
-        scratch[tid] = s;
+        for (int c = begin + l; c < end; c += 256) s = add(s, __ldcg(part + c));
+        scratch[l] = s;
     }
     __syncthreads();
     for (int w = 128; w > 0; w >>= 1) {
@@ -1382,7 +1388,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_cg_persistent(const KParams P) {
 // Pointwise GMRES passes over a block's region, tile by tile (same CTA table
 // and deterministic reduction order as the sweeps).
 template <int PKK, bool BOX>
-__global__ void __launch_bounds__(NT) k_point(const KParams P) {
+__global__ void __launch_bounds__(NPT) k_point(const KParams P) {
     extern __shared__ __align__(1024) unsigned char smem[];
     const int b = P.pcta_block[blockIdx.x];
     const DBlock &B = P.blocks[b];
@@ -1409,8 +1415,8 @@ __global__ void __launch_bounds__(NT) k_point(const KParams P) {
             double2 *vj = reinterpret_cast<double2 *>(B.V + j * vs);
             const double nrm = S.gnrm;
 #pragma unroll 4
-            for (int it = 0; it < PCHUNK / (2 * NT); ++it) {
-                const long long e = base + 2LL * (it * NT + tid);
+            for (int it = 0; it < PCHUNK / (2 * NPT); ++it) {
+                const long long e = base + 2LL * (it * NPT + tid);
                 if (e >= n) break;
                 const double2 v = src[e / 2];
                 vj[e / 2] = make_double2(__ddiv_rn(v.x, nrm), __ddiv_rn(v.y, nrm));
@@ -1423,8 +1429,8 @@ __global__ void __launch_bounds__(NT) k_point(const KParams P) {
             const double2 *vb = reinterpret_cast<const double2 *>(V + i * vs);
             double2 *w2 = reinterpret_cast<double2 *>(W);
 #pragma unroll 4
-            for (int it = 0; it < PCHUNK / (2 * NT); ++it) {
-                const long long e = base + 2LL * (it * NT + tid);
+            for (int it = 0; it < PCHUNK / (2 * NPT); ++it) {
+                const long long e = base + 2LL * (it * NPT + tid);
                 if (e >= n) break;
                 const double2 w = w2[e / 2], a = va[e / 2];
                 const double w0 = sub(w.x, mul(h, a.x)), w1 = sub(w.y, mul(h, a.y));
@@ -1440,8 +1446,8 @@ __global__ void __launch_bounds__(NT) k_point(const KParams P) {
             }
         } else {
             const int pitch = B.pitch, pdx = B.pdim[0], pdy = B.pdim[1];
-            for (int it = 0; it < PCHUNK / NT; ++it) {
-                const long long e = base + (long long)it * NT + tid;
+            for (int it = 0; it < PCHUNK / NPT; ++it) {
+                const long long e = base + (long long)it * NPT + tid;
                 if (e >= n) break;
                 const int lx = (int)(e % pitch);
                 if (lx >= pdx) continue;
@@ -1489,7 +1495,7 @@ __global__ void __launch_bounds__(NT) k_point(const KParams P) {
             }
         }
     }
-    finish<NT, -1, true>(P, b, ph, served, acc, PKK == PK_OWNRES ? NQ : 1, smem);
+    finish<NPT, -1, true>(P, b, ph, served, acc, PKK == PK_OWNRES ? NQ : 1, smem);
 }
 
 // ---- overlapping merge (multisplit.py:341-369), overlap > 0.  Inputs are the
@@ -2028,11 +2034,11 @@ void launch_point(bs_ctx *c, cudaStream_t st, int j, int i) {
     KParams P = make_params(c, false);
     P.launch_j = j;
     P.launch_i = i;
-    constexpr int smem = (NQ * (NT / 32) + 256 + 8) * 8;
+    constexpr int smem = (NQ * (NPT / 32) + 256 + 8) * 8;
     if (c->box)
-        k_point<PKK, true><<<c->npctas, NT, smem, st>>>(P);
+        k_point<PKK, true><<<c->npctas, NPT, smem, st>>>(P);
     else
-        k_point<PKK, false><<<c->npctas, NT, smem, st>>>(P);
+        k_point<PKK, false><<<c->npctas, NPT, smem, st>>>(P);
     ++g_launches;
 }
 
