@@ -25,10 +25,11 @@ Injected latency (``OuterConfig.delay``, comm.py:51-81): on top of the real
 asynchrony, every halo post and every published residual carries a delivery
 iteration ``k + d`` (d drawn from the seeded DelayModel; drop_free_jitter
 clamps it to be non-decreasing per channel).  A receiver that has begun
-sweep s only accepts payloads with delivery <= s - 1 (its last exchange
-iteration, the reference's unit), and a sender keeps the reference's R-slot
-pool: a slot is in flight until the receiver reached its delivery iteration,
-a post finding no free slot is skipped (comm.py:376-400).  Each ring has one
+sweep s only accepts payloads with delivery <= s - 1 (its exchange at the
+end of sweep s - 1 in the reference's schedule), and a sender keeps the
+reference's R-slot pool (``SendPool``): a slot is in flight until the
+receiver has begun its delivery iteration, a post finding no free slot is
+skipped (comm.py:376-400).  Each ring has one
 extra slot reserved for the confirmation round's flush, which is never
 delayed (comm.py:542-598).
 """
@@ -49,6 +50,47 @@ RING_SLOTS_MAX = 8  # without injected delays deeper rings only hold stale plane
 NO_FILTER = (1 << 63) - 1  # receiver_k that accepts every published slot
 
 
+class SendPool:
+    """Sender-side R-slot pool of one directed channel under injected latency
+    (HaloBufferPool, comm.py:94-132, and the post rule of comm.py:376-393).
+
+    A post stamped with delivery iteration t occupies its slot until the
+    receiver's last exchange iteration reaches t (then it is reclaimed); a
+    post finding every slot in flight is skipped, never blocks.
+    drop_free_jitter clamps delivery times to be non-decreasing (FIFO).
+    Slots rotate so a just-delivered payload is not overwritten first."""
+
+    def __init__(self, capacity: int, delay):
+        self.capacity = int(capacity)
+        self.delay = delay
+        self.in_flight: dict = {}  # slot -> delivery iteration
+        self.last_delivery = -1
+        self.next_slot = 0
+        self.skipped = 0
+
+    def reclaim(self, receiver_reached: int) -> None:
+        self.in_flight = {s: t for s, t in self.in_flight.items() if t > receiver_reached}
+
+    @property
+    def free_slots(self) -> int:
+        return self.capacity - len(self.in_flight)
+
+    def post(self, k: int, drawn_delay: int):
+        """(slot, delivery iteration) for sender iteration k, or None (skipped)."""
+        free = [s for s in range(self.capacity) if s not in self.in_flight]
+        if not free:
+            self.skipped += 1
+            return None
+        deliver_at = k + int(drawn_delay)
+        if self.delay.kind == "drop_free_jitter":
+            deliver_at = max(deliver_at, self.last_delivery)
+        self.last_delivery = deliver_at
+        slot = min(free, key=lambda s: (s - self.next_slot) % self.capacity)
+        self.next_slot = (slot + 1) % self.capacity
+        self.in_flight[slot] = deliver_at
+        return slot, deliver_at
+
+
 class _Mailbox:
     """Directed channel src -> dst, memory owned by dst.  Slots 0..R-1 carry
     sweep posts, slot R the (never delayed) confirmation flush."""
@@ -63,11 +105,7 @@ class _Mailbox:
         self.applied = torch.zeros(1, dtype=torch.int64, device=device)
         self.stage = torch.zeros(plane, dtype=torch.float64, device=device)
         self.torn = torch.zeros(1, dtype=torch.int32, device=device)
-        # sender-side pool (HaloBufferPool, comm.py:94-132): slot -> delivery iteration
-        self.in_flight: dict = {}
-        self.last_delivery = -1
-        self.next_slot = 0
-        self.skipped = 0
+        self.pool = None  # SendPool under injected latency
 
 
 class _Board:
@@ -133,6 +171,8 @@ def outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, spec):
         for dst, gdir, src in plan.tolist():
             plane = engines[dst].blocks[0].ghost[gdir].numel()
             mb = _Mailbox(dst, gdir, src, plane, slots, dev)
+            if delayed:
+                mb.pool = SendPool(slots, delay)
             incoming[dst].append(mb)
             outgoing[src].append(mb)
     board = _Board(nb)
@@ -214,21 +254,12 @@ def outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, spec):
                                                   mb.deliver.data_ptr(), slot, 2 * k, 0, st))
             return
         with board.lock:
-            reached = board.progress[mb.dst] - 1  # receiver's last exchange iteration
-        mb.in_flight = {s_: t for s_, t in mb.in_flight.items() if t > reached}  # reclaim (comm.py:111-112)
-        free = [s_ for s_ in range(mb.R) if s_ not in mb.in_flight]
-        if not free:
-            mb.skipped += 1  # exhausted pool: skip, never block (comm.py:392-393)
-            return
-        deliver_at = k + _draw()
-        if delay.kind == "drop_free_jitter":
-            deliver_at = max(deliver_at, mb.last_delivery)
-        mb.last_delivery = deliver_at
-        # rotate through the free slots so a just-delivered payload is not
-        # overwritten before the receiver copies it
-        slot = min(free, key=lambda s_: (s_ - mb.next_slot) % mb.R)
-        mb.next_slot = (slot + 1) % mb.R
-        mb.in_flight[slot] = deliver_at
+            reached = board.progress[mb.dst]  # the receiver's begun iteration (comm.py:383)
+        mb.pool.reclaim(reached)
+        got = mb.pool.post(k, _draw() if mb.pool.free_slots else 0)
+        if got is None:
+            return  # exhausted pool: skip, never block (comm.py:392-393)
+        slot, deliver_at = got
         _lib.check(eng.lib.bs_async_post_slot(eng.ctx, 0, mb.post_dir, mb.ring.data_ptr(), mb.seqs.data_ptr(),
                                               mb.deliver.data_ptr(), slot, 2 * k, deliver_at, st))
 
@@ -288,7 +319,7 @@ def outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, spec):
             eng.gather_owned(sol)
         torch.cuda.synchronize(dev)
         torn = int(sum(int(mb.torn.item()) for lst in incoming for mb in lst))
-        skipped = int(sum(mb.skipped for lst in incoming for mb in lst))
+        skipped = int(sum(mb.pool.skipped for lst in incoming for mb in lst if mb.pool is not None))
         for eng in engines:
             eng.close()
     # a lapped read (sender overwrote the slot mid-copy) kept the old halo,

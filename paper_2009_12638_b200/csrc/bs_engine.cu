@@ -1297,16 +1297,27 @@ __device__ void grid_sync(const KParams &P, unsigned char *smem, DState *s_state
     volatile unsigned *gen = &ctl->bar_gen;
     const unsigned g = gen_ref;
     if (threadIdx.x == 0) {
+#ifdef BS_BAR_FENCES
         __threadfence();
         s_last = atomicAdd(&ctl->bar_count, 1u) == gridDim.x - 1;
-        if (!s_last) {
+        if (!s_last)
             while (*gen == g) {
-#ifdef BS_SPIN_SLEEP
-                __nanosleep(BS_SPIN_SLEEP);
-#endif
             }
-        }
         __threadfence();
+#else
+        // arrive: one acq_rel RMW (release: this CTA's writes, ordered by the
+        // CTA barrier, before the count; acquire: everything the earlier
+        // arrivals released, for the last arriver)
+        unsigned prev;
+        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&ctl->bar_count) : "memory");
+        s_last = prev == gridDim.x - 1;
+        if (!s_last) {
+            unsigned cur;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(&ctl->bar_gen) : "memory");
+            } while (cur == g);
+        }
+#endif
     }
     __syncthreads();
     if (s_last) {
@@ -1356,8 +1367,12 @@ __device__ void grid_sync(const KParams &P, unsigned char *smem, DState *s_state
             *(volatile int *)&ctl->verify = verify;
             *(volatile int *)P.n_active = active;
             ctl->bar_count = 0u;
+#ifdef BS_BAR_FENCES
             __threadfence();
             atomicExch(&ctl->bar_gen, g + 1u);
+#else
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&ctl->bar_gen), "r"(g + 1u) : "memory");
+#endif
         }
     }
     gen_ref = g + 1u;

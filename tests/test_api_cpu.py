@@ -140,3 +140,42 @@ def test_delay_model_draws_like_the_reference():
         parse_delay("uniform:a:b", 0)
     with pytest.raises(bs.ConfigurationError, match="delay"):
         bs.DelayModel("uniform", low=3, high=1)
+
+
+def test_send_pool_mirrors_the_reference_halo_buffer_pool():
+    """SendPool (async_driver) against the reference pool semantics
+    (comm.py:94-132, 376-393; test_comm.py TestAsyncExchange restated)."""
+    from paper_2009_12638_b200.async_driver import SendPool
+
+    # one slot, fixed delay 3: a post lands every 3 iterations, the rest skip
+    pool = SendPool(1, bs.DelayModel("fixed", fixed=3))
+    landed = []
+    for k in range(31):
+        pool.reclaim(k)  # the receiver (in lockstep) has begun iteration k
+        got = pool.post(k, 3 if pool.free_slots else 0)
+        if got is not None:
+            landed.append(got[1] - 3)
+    assert landed == list(range(0, 31, 3))  # sends at 0, 3, 6, ... (test_comm.py:149-157)
+    assert pool.skipped == 31 - len(landed) > 0
+    # conservation: in flight + free == capacity at every step
+    rng = np.random.default_rng(13)
+    m = bs.DelayModel("uniform", low=0, high=3, seed=13)
+    pool = SendPool(4, m)
+    for k in range(500):
+        pool.reclaim(k)
+        if pool.free_slots:
+            pool.post(k, m.draw(rng))
+        else:
+            assert pool.post(k, 0) is None
+        assert len(pool.in_flight) + pool.free_slots == pool.capacity == 4
+    # drop_free_jitter: delivery times never regress (FIFO, no stale discards)
+    m = bs.DelayModel("drop_free_jitter", low=0, high=4, seed=21)
+    rng = np.random.default_rng(21)
+    pool = SendPool(100, m)
+    times = []
+    for k in range(300):
+        pool.reclaim(k)
+        got = pool.post(k, m.draw(rng))
+        times.append(got[1])
+    assert all(b >= a for a, b in zip(times, times[1:]))
+    assert all(t >= k for k, t in enumerate(times))
