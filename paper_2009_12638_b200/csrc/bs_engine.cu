@@ -128,7 +128,10 @@ enum Pk : int { PK_NORM = 0, PK_MGS = 1, PK_FINAL = 2, PK_FORM = 3, PK_OWNRES = 
 
 constexpr int MAXM = 64;    // largest supported GMRES restart length
 constexpr int MAXNBR = 32;  // neighbour list capacity per block (overlapping merge)
-constexpr int PCHUNK = 4096; // doubles per CTA in pointwise passes
+#ifndef BS_PCHUNK
+#define BS_PCHUNK 16384
+#endif
+constexpr int PCHUNK = BS_PCHUNK;  // doubles per CTA in pointwise passes
 enum GFlag : int { GF_NONE = 0, GF_HAPPY = 1, GF_CHECK = 2, GF_CYCLE = 3 };
 
 // Stage layout per op: [A haloed][B haloed, if the op has one][C bare tile].
@@ -1115,6 +1118,10 @@ template <int NTH, int OPK, bool POINT = false>
 __device__ void finish(const KParams &P, int b, int ph, bool served, double (&acc)[NQ], int nq,
                        unsigned char *smem) {
     finish_block<NTH, POINT>(P, b, ph, served, acc, nq, smem, blockIdx.x);
+    // Pointwise (GMRES) passes are host-sequenced and never end a loop: the
+    // launch-level bookkeeping (one atomic per CTA on a single counter) is
+    // only needed by sweeps.
+    if (POINT) return;
     const int nctas = POINT ? P.npctas : P.nctas;
     const int tid = threadIdx.x;
     int *flag = reinterpret_cast<int *>(reinterpret_cast<double *>(smem) + NQ * (NTH / 32) + 256);
@@ -1430,16 +1437,31 @@ __global__ void __launch_bounds__(NPT) k_point(const KParams P) {
         const long long vs = B.vstride;
         double *__restrict__ W = B.W;
         const double *__restrict__ V = B.V;
+        // element pairs of this CTA: e = base + 2 (it * NPT + tid); the chunk
+        // is processed in batches of PB pairs per thread, every load of a
+        // batch issued before any use (memory-level parallelism), with no
+        // bounds test on full chunks
+        constexpr int PITER = PCHUNK / (2 * NPT), PB = 4;
+        const long long pair0 = base / 2 + tid;  // in double2 units
+        const long long npairs = n / 2;          // n is even (pitch % 4 == 0)
+        const bool full_chunk = base + PCHUNK <= n;
         if (PKK == PK_NORM) {  // v_j = src / nrm (inner_solvers.py:164, 237)
             const double2 *src = reinterpret_cast<const double2 *>(j == 0 ? B.r : W);
             double2 *vj = reinterpret_cast<double2 *>(B.V + j * vs);
             const double nrm = S.gnrm;
-#pragma unroll 4
-            for (int it = 0; it < PCHUNK / (2 * NPT); ++it) {
-                const long long e = base + 2LL * (it * NPT + tid);
-                if (e >= n) break;
-                const double2 v = src[e / 2];
-                vj[e / 2] = make_double2(__ddiv_rn(v.x, nrm), __ddiv_rn(v.y, nrm));
+            for (int it0 = 0; it0 < PITER; it0 += PB) {
+                double2 v[PB];
+#pragma unroll
+                for (int u = 0; u < PB; ++u) {
+                    const long long e2 = pair0 + (long long)(it0 + u) * NPT;
+                    if (full_chunk || e2 < npairs) v[u] = __ldcs(src + e2);
+                }
+#pragma unroll
+                for (int u = 0; u < PB; ++u) {
+                    const long long e2 = pair0 + (long long)(it0 + u) * NPT;
+                    if (full_chunk || e2 < npairs)
+                        __stcs(vj + e2, make_double2(__ddiv_rn(v[u].x, nrm), __ddiv_rn(v[u].y, nrm)));
+                }
             }
         } else if (PKK == PK_MGS || PKK == PK_FINAL) {
             // MGS:   w -= h_{i-1,j} v_{i-1} ; h_ij = v_i . w   (inner_solvers.py:189-193)
@@ -1448,20 +1470,30 @@ __global__ void __launch_bounds__(NPT) k_point(const KParams P) {
             const double2 *va = reinterpret_cast<const double2 *>(V + (PKK == PK_MGS ? i - 1 : j) * vs);
             const double2 *vb = reinterpret_cast<const double2 *>(V + i * vs);
             double2 *w2 = reinterpret_cast<double2 *>(W);
-#pragma unroll 4
-            for (int it = 0; it < PCHUNK / (2 * NPT); ++it) {
-                const long long e = base + 2LL * (it * NPT + tid);
-                if (e >= n) break;
-                const double2 w = w2[e / 2], a = va[e / 2];
-                const double w0 = sub(w.x, mul(h, a.x)), w1 = sub(w.y, mul(h, a.y));
-                w2[e / 2] = make_double2(w0, w1);
-                if (PKK == PK_MGS) {
-                    const double2 c = vb[e / 2];
-                    acc[0] = add(acc[0], mul(c.x, w0));
-                    acc[0] = add(acc[0], mul(c.y, w1));
-                } else {
-                    acc[0] = add(acc[0], mul(w0, w0));
-                    acc[0] = add(acc[0], mul(w1, w1));
+            for (int it0 = 0; it0 < PITER; it0 += PB) {
+                double2 w[PB], a[PB], c[PB];
+#pragma unroll
+                for (int u = 0; u < PB; ++u) {
+                    const long long e2 = pair0 + (long long)(it0 + u) * NPT;
+                    if (full_chunk || e2 < npairs) {
+                        w[u] = __ldcs(w2 + e2);
+                        a[u] = __ldg(va + e2);
+                        if (PKK == PK_MGS) c[u] = __ldg(vb + e2);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < PB; ++u) {
+                    const long long e2 = pair0 + (long long)(it0 + u) * NPT;
+                    if (!(full_chunk || e2 < npairs)) continue;
+                    const double w0 = sub(w[u].x, mul(h, a[u].x)), w1 = sub(w[u].y, mul(h, a[u].y));
+                    __stcs(w2 + e2, make_double2(w0, w1));
+                    if (PKK == PK_MGS) {
+                        acc[0] = add(acc[0], mul(c[u].x, w0));
+                        acc[0] = add(acc[0], mul(c[u].y, w1));
+                    } else {
+                        acc[0] = add(acc[0], mul(w0, w0));
+                        acc[0] = add(acc[0], mul(w1, w1));
+                    }
                 }
             }
         } else {
