@@ -318,6 +318,77 @@ __device__ __forceinline__ double offdiag6(double zm, double ym, double xm, doub
     return 0.0;
 }
 
+// Rows on a region face: rhs = b - C*halo with the coupling row summed by the
+// reduceat rule (entries of -1 in ascending column order, first + seq(rest);
+// multisplit.py:333-338), and (want_global) the global operator row on the
+// gathered iterate for the true residual (residual_norms).  Out of line: only
+// face rows call it.
+__device__ __noinline__ void face_coupling(const DBlock &B, int gi, int gj, int gk, double bv, double zm, double ym,
+                                           double xm, double c, double xp, double yp, double zp, bool want_global,
+                                           double &rhs, double &rg_au) {
+    const int ni[6] = {gi, gi, gi - 1, gi + 1, gi, gi};
+    const int nj[6] = {gj, gj - 1, gj, gj, gj + 1, gj};
+    const int nk[6] = {gk - 1, gk, gk, gk, gk, gk + 1};
+    double firstc = 0.0, rest = 0.0;
+    int cnt = 0;
+    double v[6] = {zm, ym, xm, xp, yp, zp};
+    bool pg[6];
+#pragma unroll
+    for (int d = 0; d < 6; ++d) {
+        pg[d] = in_grid(B, ni[d], nj[d], nk[d]);
+        if (pg[d] && !in_region(B, ni[d], nj[d], nk[d])) {
+            const double h = ghost_at(B, ni[d], nj[d], nk[d], d);
+            v[d] = h;  // the global operator sees the coupled value
+            if (cnt == 0) firstc = -h;
+            else if (cnt == 1) rest = -h;
+            else rest = add(rest, -h);
+            ++cnt;
+        }
+    }
+    if (cnt) rhs = sub(bv, cnt == 1 ? firstc : add(firstc, rest));
+    if (want_global) rg_au = stencil7(v[0], v[1], v[2], c, v[3], v[4], v[5], pg[0], pg[1], pg[2]);
+}
+
+// Box blocks (overlap 0): the same on local coordinates — a neighbour across
+// a block face is coupled iff that face is not a grid face, and its value is
+// the face plane's entry; no region tests, no local arrays.
+__device__ __forceinline__ void face_coupling_box(const DBlock &B, int lx, int ly, int lz, double bv, double zm,
+                                                  double ym, double xm, double c, double xp, double yp, double zp,
+                                                  bool want_global, double &rhs, double &rg_au) {
+    const int pdx = B.pdim[0], pdy = B.pdim[1], pdz = B.pdim[2];
+    // coupled (in the grid, outside the block) and in-block presence per direction
+    const bool cz0 = lz == 0 && B.plo[2] > 0, cy0 = ly == 0 && B.plo[1] > 0, cx0 = lx == 0 && B.plo[0] > 0;
+    const bool cx1 = lx == pdx - 1 && B.plo[0] + pdx < B.gn[0];
+    const bool cy1 = ly == pdy - 1 && B.plo[1] + pdy < B.gn[1];
+    const bool cz1 = lz == pdz - 1 && B.plo[2] + pdz < B.gn[2];
+    if (!(cz0 | cy0 | cx0 | cx1 | cy1 | cz1)) {  // only grid faces: no coupling
+        if (want_global) rg_au = stencil7(zm, ym, xm, c, xp, yp, zp, lz > 0, ly > 0, lx > 0);
+        return;
+    }
+    double h[6];
+    h[0] = cz0 ? B.ghost[0][lx + pdx * ly] : 0.0;
+    h[1] = cy0 ? B.ghost[1][lx + pdx * lz] : 0.0;
+    h[2] = cx0 ? B.ghost[2][ly + pdy * lz] : 0.0;
+    h[3] = cx1 ? B.ghost[3][ly + pdy * lz] : 0.0;
+    h[4] = cy1 ? B.ghost[4][lx + pdx * lz] : 0.0;
+    h[5] = cz1 ? B.ghost[5][lx + pdx * ly] : 0.0;
+    const bool cp[6] = {cz0, cy0, cx0, cx1, cy1, cz1};
+    double firstc = 0.0, rest = 0.0;
+    int cnt = 0;
+#pragma unroll
+    for (int d = 0; d < 6; ++d) {
+        if (!cp[d]) continue;
+        if (cnt == 0) firstc = -h[d];
+        else if (cnt == 1) rest = -h[d];
+        else rest = add(rest, -h[d]);
+        ++cnt;
+    }
+    rhs = sub(bv, cnt == 1 ? firstc : add(firstc, rest));
+    if (want_global)
+        rg_au = stencil7(cz0 ? h[0] : zm, cy0 ? h[1] : ym, cx0 ? h[2] : xm, c, cx1 ? h[3] : xp, cy1 ? h[4] : yp,
+                         cz1 ? h[5] : zp, lz > 0 || cz0, ly > 0 || cy0, lx > 0 || cx0);
+}
+
 // ------------------------------------------------------------------ TMA / mbarrier
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -684,31 +755,12 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
                                   lz == pdz - 1;
                 double rhs = bv, rg_au = au;
                 if (face) {
-                    const int ni[6] = {gi, gi, gi - 1, gi + 1, gi, gi};
-                    const int nj[6] = {gj, gj - 1, gj, gj, gj + 1, gj};
-                    const int nk[6] = {gk - 1, gk, gk, gk, gk, gk + 1};
-                    // coupling row sum C*halo (multisplit.py:333-338): entries of
-                    // -1 in ascending column order, reduceat rule first + seq(rest)
-                    double firstc = 0.0, rest = 0.0;
-                    int cnt = 0;
-                    double v[6] = {u_prev[r], ym, xm, xp, yp, u_next[r]};
-                    bool pg[6];
-#pragma unroll
-                    for (int d = 0; d < 6; ++d) {
-                        pg[d] = in_grid(B, ni[d], nj[d], nk[d]);
-                        if (pg[d] && !in_region(B, ni[d], nj[d], nk[d])) {
-                            const double h = ghost_at(B, ni[d], nj[d], nk[d], d);
-                            v[d] = h;  // global operator sees the coupled value
-                            if (cnt == 0) firstc = -h;
-                            else if (cnt == 1) rest = -h;
-                            else rest = add(rest, -h);
-                            ++cnt;
-                        }
-                    }
-                    if (cnt) rhs = sub(bv, cnt == 1 ? firstc : add(firstc, rest));
-                    // global operator row (residual_norms on the gathered iterate)
-                    if (OP == OP_RESID)
-                        rg_au = stencil7(v[0], v[1], v[2], u_cur[r], v[3], v[4], v[5], pg[0], pg[1], pg[2]);
+                    if (BOX)
+                        face_coupling_box(B, lx, ly, lz, bv, u_prev[r], ym, xm, u_cur[r], xp, yp, u_next[r],
+                                          OP == OP_RESID, rhs, rg_au);
+                    else  // out of line: keeps the interior path lean
+                        face_coupling(B, gi, gj, gk, bv, u_prev[r], ym, xm, u_cur[r], xp, yp, u_next[r],
+                                      OP == OP_RESID, rhs, rg_au);
                 }
                 const double rv = sub(rhs, au);
                 if (OP == OP_JAC) {
