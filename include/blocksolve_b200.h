@@ -89,9 +89,15 @@ typedef struct bs_ctx bs_ctx;
 int bs_abi_version(void);
 const char *bs_last_error(void);
 
-/* Create an engine over `nblocks` blocks resident on `device`.  z_chunk = 0
- * picks the z-depth of a CTA tile automatically.  The descriptor table is
- * copied; the buffers stay owned by the caller. */
+/* Create an engine over `nblocks` blocks resident on `device`.  Sweeps tile
+ * each block into 32 x 8 columns; z_chunk = 0 streams full-depth columns
+ * unless the block has too few columns to fill the GPU (then z is split into
+ * chunks of >= 32 planes); z_chunk > 0 forces the chunk depth.  The tiling is
+ * a function of the block alone, so reductions do not depend on which blocks
+ * share a GPU.  The descriptor table is copied; the buffers stay owned by the
+ * caller.  bs_run drives CG solves with one persistent cooperative launch
+ * when every tile fits co-resident (environment BS_PERSIST=0 forces the
+ * CUDA-graph path; both give bitwise-identical results). */
 int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_chunk,
                   bs_ctx **out);
 int bs_ctx_destroy(bs_ctx *ctx);
