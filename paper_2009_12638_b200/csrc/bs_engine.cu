@@ -666,10 +666,11 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
     double *__restrict__ out_w = B.W;
     double *__restrict__ out_p = C.pout;
     double *__restrict__ out_y = C.yout;
-    int s = 1 % NS, sn = 2 % NS;   // stage of plane q and q+1
-    uint32_t par_n = 2 / NS;        // completion parity of stage sn
-
-    auto single_step = [&](int q) {
+    // Plane q sits in stage q % NS and completes phase (q / NS) & 1.  The
+    // loop below is unrolled by NS so both are compile-time per step: `s`
+    // (this plane's stage), `sn` (the next plane's) and `par_n` (the next
+    // plane's parity) are constants or one loop-carried bit.
+    auto single_step = [&](int q, int s, int sn, uint32_t par_n) {
         const int lz = lz0 - 1 + q;
         const unsigned char *st = smem + s * STB;
         const double *cst = reinterpret_cast<const double *>(st + COFF);
@@ -789,13 +790,16 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
-        s = sn;
-        if (++sn == NS) {
-            sn = 0;
-            ++par_n;
-        }
     };
-    for (int q = 1; q <= nplanes - 2; ++q) single_step(q);
+    // q = 1 .. nplanes-2 in rounds of NS aligned to stage 0
+    uint32_t par = 0;  // completion parity of the planes of this round
+    for (int q0 = 0; q0 <= nplanes - 2; q0 += NS, par ^= 1u) {
+#pragma unroll
+        for (int u = 0; u < NS; ++u) {
+            const int q = q0 + u;
+            if (q >= 1 && q <= nplanes - 2) single_step(q, u, (u + 1) % NS, u + 1 == NS ? par ^ 1u : par);
+        }
+    }
     if (tid == 0) BS_STAMP(2);
 }
 
