@@ -13,8 +13,8 @@ from .inner_solvers import InnerSolveReport, InnerSolverSpec, cg_solve, gmres_so
 from .linalg import residual_norms, spmv
 from .multisplit import (TRACE_HEADER, DelayModel, OuterConfig, ResidualTrace, SolveResult,
                          TraceRow, check_termination, combined_residual, outer_solve)
-from .problems import (FACES, BlockDecomposition, DirichletBoundary, Grid3D, LinearProblem,
-                       StencilOperator, build_laplace_3d, decompose, seeded_rhs)
+from .problems import (FACES, BlockDecomposition, BlockOperator, DirichletBoundary, Grid3D, LinearProblem,
+                       StencilOperator, block_system, build_laplace_3d, decompose, seeded_rhs)
 
 __version__ = "0.1.0"
 
@@ -25,5 +25,5 @@ __all__ = [
     "TRACE_HEADER", "TraceRow", "ZeroRhsError", "build_laplace_3d", "cg_solve",
     "check_termination", "combined_residual", "decompose", "gmres_solve", "jacobi_solve", "outer_solve",
     "residual_norms", "seeded_rhs", "solve", "spmv", "SpectralEstimate", "iteration_operator",
-    "jacobi_iteration_operator", "power_iteration",
+    "jacobi_iteration_operator", "power_iteration", "BlockOperator", "block_system",
 ]

@@ -21,7 +21,7 @@ from ._lib import STOP_NAMES
 from .engine import torch
 from .errors import ConfigurationError
 from .engine import launch_bound
-from .linalg import as_device_vector, single_block_engine
+from .linalg import as_device_vector, put_vector, single_block_engine, take_vector
 from .problems import StencilOperator
 
 __all__ = [
@@ -105,8 +105,8 @@ def _fused_solve(kind, a, b, x0, spec, tolerance_basis, batch, out):
     xd, _ = as_device_vector(x0, n, eng.device)
     bb = eng.blocks[0]
     with torch.cuda.device(eng.device):
-        bb.put("b", bd)
-        bb.put("x", xd)
+        put_vector(a, bb, "b", bd)
+        put_vector(a, bb, "x", xd)
         begin = eng.cg_begin if kind == "cg" else eng.jacobi_begin
         begin(spec.max_iterations, spec.tolerance, tolerance_basis)
         eng.run(batch=batch, max_launches=launch_bound(spec.max_iterations, batch))
@@ -114,7 +114,7 @@ def _fused_solve(kind, a, b, x0, spec, tolerance_basis, batch, out):
         rep = eng.reports()[0]
         its = int(rep.iterations_used)
         hist = bb.history[:its].tolist() if its else []
-        x = bb.take("x")  # unpitched copy, never aliased to the engine
+        x = take_vector(a, bb, "x")  # unpitched copy, never aliased to the engine
     report = InnerSolveReport(its, float(rep.final_relative_residual), STOP_NAMES[int(rep.stop_reason)],
                               hist)
     if host:
@@ -149,14 +149,14 @@ def gmres_solve(a: StencilOperator, b, x0, spec: InnerSolverSpec, tolerance_basi
     max_cycles = spec.max_iterations + 2  # every cycle consumes >= 1 iteration
     with torch.cuda.device(eng.device):
         eng.gmres_setup(restart)
-        bb.put("b", bd)
-        bb.put("x", xd)
+        put_vector(a, bb, "b", bd)
+        put_vector(a, bb, "x", xd)
         eng.gmres_begin(spec.max_iterations, spec.tolerance, tolerance_basis)
         eng.gmres_run(max_cycles=max_cycles)
         rep = eng.reports()[0]
         its = int(rep.iterations_used)
         hist = bb.history[:its].tolist() if its else []
-        x = bb.take("x")
+        x = take_vector(a, bb, "x")
     report = InnerSolveReport(its, float(rep.final_relative_residual), STOP_NAMES[int(rep.stop_reason)],
                               hist)
     if host:

@@ -12,18 +12,25 @@ import numpy as np
 
 from .engine import BlockEngine, require_cuda, torch
 from .errors import ZeroRhsError
-from .problems import Box, StencilOperator
+from .problems import BlockOperator, Box, StencilOperator
 
-__all__ = ["spmv", "residual_norms", "as_device_vector", "single_block_engine"]
+__all__ = ["spmv", "residual_norms", "as_device_vector", "single_block_engine", "put_vector", "take_vector"]
 
 _ENGINES: dict = {}
+_MASKS: dict = {}
 
 
-def single_block_engine(a: StencilOperator, device=None, history_cap: int = 1) -> BlockEngine:
-    """Cached one-block engine covering the whole grid (overlap 0)."""
+def single_block_engine(a, device=None, history_cap: int = 1) -> BlockEngine:
+    """Cached one-block engine: the whole grid for a ``StencilOperator``
+    (overlap 0), the block's padded box and region for a ``BlockOperator``."""
     dev = require_cuda(device)
-    shape = (a.nx, a.ny, a.nz)
-    key = (shape, str(dev))
+    if isinstance(a, BlockOperator):
+        key = ("block", a.grid_shape, a.owned.lo, a.owned.hi, a.overlap, str(dev))
+        make = lambda cap: BlockEngine(a.grid_shape, [a.owned], a.overlap, dev, history_cap=cap)  # noqa: E731
+    else:
+        shape = (a.nx, a.ny, a.nz)
+        key = (shape, str(dev))
+        make = lambda cap: BlockEngine(shape, [Box((0, 0, 0), shape)], 0, dev, history_cap=cap)  # noqa: E731
     eng = _ENGINES.get(key)
     if eng is None or eng.blocks[0].history.numel() < history_cap:
         if eng is not None:
@@ -31,9 +38,35 @@ def single_block_engine(a: StencilOperator, device=None, history_cap: int = 1) -
         if len(_ENGINES) >= 4:  # bounded cache: drop the oldest engine
             old = _ENGINES.pop(next(iter(_ENGINES)))
             old.close()
-        eng = BlockEngine(shape, [Box((0, 0, 0), shape)], 0, dev, history_cap=max(history_cap, 1))
+        eng = make(max(history_cap, 1))
         _ENGINES[key] = eng
     return eng
+
+
+def _region_mask(a, device):
+    if not isinstance(a, BlockOperator):
+        return None
+    key = (a, str(device))
+    m = _MASKS.get(key)
+    if m is None:
+        m = _MASKS[key] = torch.from_numpy(a.mask).to(device)
+    return m
+
+
+def put_vector(a, bb, name: str, v) -> None:
+    """Store an operator-ordered vector (whole grid, or a block's region in
+    ascending global index) into the engine buffer ``name``."""
+    m = _region_mask(a, v.device)
+    if m is None:
+        bb.put(name, v)
+    else:
+        bb.view3(getattr(bb, name))[m] = v
+
+
+def take_vector(a, bb, name: str):
+    """Operator-ordered copy of the engine buffer ``name``."""
+    m = _region_mask(a, getattr(bb, name).device)
+    return bb.take(name) if m is None else bb.view3(getattr(bb, name))[m]
 
 
 def as_device_vector(v, n: int, device) -> tuple:
@@ -66,9 +99,13 @@ def spmv(a: StencilOperator, x):
     with torch.cuda.device(eng.device):
         xp = bb.zeros_pitched()
         yp = bb.zeros_pitched()
-        bb.view3(xp).copy_(xd.reshape(a.nz, a.ny, a.nx))
+        m = _region_mask(a, eng.device)
+        if m is None:
+            bb.view3(xp).copy_(xd.reshape(a.nz, a.ny, a.nx))
+        else:
+            bb.view3(xp)[m] = xd
         eng.apply(0, xp, yp)
-        y = bb.view3(yp).contiguous().reshape(-1)
+        y = bb.view3(yp).contiguous().reshape(-1) if m is None else bb.view3(yp)[m]
     return y.cpu().numpy() if host else y
 
 
@@ -80,8 +117,8 @@ def residual_norms(a: StencilOperator, x, b) -> tuple:
     bd, _ = as_device_vector(b, n, eng.device)
     bb = eng.blocks[0]
     with torch.cuda.device(eng.device):
-        bb.put("b", bd)
-        bb.put("x", xd)
+        put_vector(a, bb, "b", bd)
+        put_vector(a, bb, "x", xd)
         eng.residual()
         rep = eng.reports()[0]
     absolute = float(np.sqrt(rep.r_sq))

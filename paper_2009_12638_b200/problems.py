@@ -24,6 +24,8 @@ __all__ = [
     "LinearProblem",
     "StencilOperator",
     "BlockDecomposition",
+    "BlockOperator",
+    "block_system",
     "build_laplace_3d",
     "decompose",
     "seeded_rhs",
@@ -322,3 +324,92 @@ def decompose(grid: Grid3D, block_grid: tuple, overlap: int = 0) -> BlockDecompo
                 neighbors[a].append(b)
                 neighbors[b].append(a)
     return BlockDecomposition(grid, (gx, gy, gz), overlap, owned, neighbors)
+
+
+class BlockOperator:
+    """A block's local operator: the principal submatrix of the 7-point
+    Laplacian on the block's extended region (problems.py:362-406), matrix-free.
+
+    Unknowns are the region's points in ascending global index (the
+    reference's ``extended_indices`` order).  ``spmv`` and the inner solvers
+    accept it like a ``StencilOperator``; they run on a one-block engine of
+    the decomposition's geometry, bit-identical to the reference's CSR
+    ``spmv`` of the extracted ``SparseMatrix``."""
+
+    def __init__(self, grid_shape, owned: Box, overlap: int, padded: Box, mask: np.ndarray, ext: np.ndarray):
+        self.grid_shape = tuple(int(v) for v in grid_shape)
+        self.owned = owned
+        self.overlap = int(overlap)
+        self.padded = padded
+        self.mask = mask  # region mask over the padded box, (z, y, x)
+        self.ext = ext
+
+    @property
+    def num_rows(self) -> int:
+        return int(self.ext.shape[0])
+
+    num_cols = num_rows
+
+    @property
+    def shape(self) -> tuple:
+        return (self.num_rows, self.num_rows)
+
+    @property
+    def nnz(self) -> int:
+        m = self.mask
+        n = int(m.sum())
+        for ax in range(3):
+            sl_a = [slice(None)] * 3
+            sl_b = [slice(None)] * 3
+            sl_a[ax] = slice(1, None)
+            sl_b[ax] = slice(None, -1)
+            n += 2 * int((m[tuple(sl_a)] & m[tuple(sl_b)]).sum())
+        return n
+
+    def __eq__(self, other) -> bool:
+        return (isinstance(other, BlockOperator) and self.grid_shape == other.grid_shape
+                and self.owned == other.owned and self.overlap == other.overlap)
+
+    def __hash__(self):
+        return hash((self.grid_shape, self.owned, self.overlap))
+
+    def __repr__(self) -> str:
+        return (f"BlockOperator(grid={self.grid_shape}, owned={self.owned.lo}..{self.owned.hi}, "
+                f"overlap={self.overlap}, n={self.num_rows})")
+
+
+def block_system(problem: LinearProblem, decomp: BlockDecomposition, block_id: int):
+    """(a_ii, coupling) of one block (problems.py:362-406).
+
+    ``a_ii`` is the principal submatrix on the extended region (a
+    ``BlockOperator``); ``coupling`` lists every (local_row, global_col,
+    coefficient) linking the region to an outside column, by local row and
+    ascending column — the reference's order and values (-1.0)."""
+    if not 0 <= block_id < decomp.num_blocks:
+        raise ValueError(f"block_id {block_id} out of range")
+    nx, ny, nz = problem.grid.shape
+    pad = decomp.padded_box(block_id)
+    mask = decomp.region_mask(block_id)
+    ext = decomp.extended_indices(block_id)
+    k, j, i = np.meshgrid(*(np.arange(pad.lo[d], pad.hi[d]) for d in (2, 1, 0)), indexing="ij")
+    local = np.full(mask.shape, -1, dtype=np.int64)
+    local[mask] = np.arange(int(mask.sum()))
+    rows, cols = [], []
+    # ascending global column order within a row: z-1, y-1, x-1, x+1, y+1, z+1
+    for di, dj, dk in ((0, 0, -1), (0, -1, 0), (-1, 0, 0), (1, 0, 0), (0, 1, 0), (0, 0, 1)):
+        ni, nj, nk = i + di, j + dj, k + dk
+        in_grid = (ni >= 0) & (nj >= 0) & (nk >= 0) & (ni < nx) & (nj < ny) & (nk < nz)
+        li, lj, lk = ni - pad.lo[0], nj - pad.lo[1], nk - pad.lo[2]
+        in_pad = (li >= 0) & (lj >= 0) & (lk >= 0) & (li < mask.shape[2]) & (lj < mask.shape[1]) & \
+            (lk < mask.shape[0])
+        in_region = np.zeros(mask.shape, dtype=bool)
+        in_region[in_pad] = mask[lk[in_pad], lj[in_pad], li[in_pad]]
+        sel = mask & in_grid & ~in_region
+        rows.append(local[sel])
+        cols.append((ni + nx * (nj + ny * nk))[sel])
+    rows = np.concatenate(rows)
+    cols = np.concatenate(cols)
+    order = np.lexsort((cols, rows))
+    coupling = [(int(r), int(c), -1.0) for r, c in zip(rows[order], cols[order])]
+    op = BlockOperator(problem.grid.shape, decomp.owned[block_id], decomp.overlap, pad, mask, ext)
+    return op, coupling

@@ -179,3 +179,31 @@ def test_send_pool_mirrors_the_reference_halo_buffer_pool():
         times.append(got[1])
     assert all(b >= a for a, b in zip(times, times[1:]))
     assert all(t >= k for k, t in enumerate(times))
+
+
+def _blocksys_keys():
+    from golden_io import meta
+
+    return sorted(k for k in meta() if k.startswith("blocksys/"))
+
+
+@pytest.mark.parametrize("key", _blocksys_keys())
+def test_block_system_matches_reference(key):
+    """block_system (problems.py:362-406): region, couplings and size equal the
+    reference's extraction (golden vectors from the unmodified reference)."""
+    from golden_io import arrays, meta
+    from oracle import blocksolve_oracle as O
+
+    A, m = arrays(), meta()[key]
+    shape, bg, ov = tuple(m["shape"]), tuple(m["block_grid"]), m["overlap"]
+    prob = bs.build_laplace_3d(bs.Grid3D(*shape))
+    dec = bs.decompose(prob.grid, bg, ov)
+    _, wss, _, _ = O.build_workspaces(shape, np.zeros(int(np.prod(shape))), bg, ov)
+    for b in range(dec.num_blocks):
+        op, coupling = bs.block_system(prob, dec, b)
+        assert np.array_equal(op.ext, A[f"{key}/{b}/ext"])
+        assert np.array_equal(np.asarray(coupling, dtype=np.float64).reshape(-1, 3), A[f"{key}/{b}/coupling"])
+        assert op.num_rows == op.shape[0] == wss[b].a_ii.num_rows
+        assert op.nnz == wss[b].a_ii.values.shape[0]
+    with pytest.raises(ValueError, match="out of range"):
+        bs.block_system(prob, dec, dec.num_blocks)

@@ -505,3 +505,35 @@ def test_device_seeded_rhs_bit_identical_to_numpy():
     for n, seed in ((1, 0), (1000, 3), (256 ** 3, 0)):
         d = bs.seeded_rhs(n, seed, device="cuda").cpu().numpy()
         assert np.array_equal(d, O.seeded_rhs(n, seed))
+
+
+# ------------------------------------------------------------------ block systems through the public API
+
+
+def test_block_system_spmv_and_solves_public_api():
+    """spmv / cg_solve / gmres_solve on ``block_system`` operators (box and
+    L1-dilated regions) vs the reference's golden SpMV and the oracle."""
+    A, M = arrays(), meta()
+    for key in ("blocksys/8x8x8_222_o2", "blocksys/9x7x6_213_o1", "blocksys/6x6x6_321_o0"):
+        m = M[key]
+        shape, bg, ov = tuple(m["shape"]), tuple(m["block_grid"]), m["overlap"]
+        prob = bs.build_laplace_3d(bs.Grid3D(*shape))
+        dec = bs.decompose(prob.grid, bg, ov)
+        _, wss, _, _ = O.build_workspaces(shape, np.zeros(int(np.prod(shape))), bg, ov)
+        for b in range(dec.num_blocks):
+            op, _ = bs.block_system(prob, dec, b)
+            y = bs.spmv(op, A[f"{key}/{b}/x"])
+            assert np.array_equal(y, A[f"{key}/{b}/y"]), (key, b)
+        op, _ = bs.block_system(prob, dec, 1)
+        rhs = np.random.default_rng(1).uniform(-1, 1, op.num_rows)
+        ap = lambda v, a=wss[1].a_ii: O.csr_spmv(a, v)
+        x, rep = bs.cg_solve(op, rhs, np.zeros(op.num_rows), bs.InnerSolverSpec("cg", 500, 1e-10))
+        xo, ro = O.cg(ap, rhs, np.zeros(op.num_rows), 500, 1e-10)
+        assert rep.iterations_used == ro.iterations_used
+        assert np.linalg.norm(x - xo) <= 1e-9 * np.linalg.norm(xo)
+        x, rep = bs.gmres_solve(op, rhs, np.zeros(op.num_rows), bs.InnerSolverSpec("gmres", 60, 1e-10, 20))
+        xo, ro = O.gmres(ap, rhs, np.zeros(op.num_rows), 60, 1e-10, 20)
+        assert rep.iterations_used == ro.iterations_used
+        assert np.linalg.norm(x - xo) <= 1e-9 * np.linalg.norm(xo)
+        _, rel = bs.residual_norms(op, x, rhs)
+        assert rel <= 1e-9
