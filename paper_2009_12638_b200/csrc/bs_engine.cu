@@ -2080,6 +2080,11 @@ struct bs_ctx {
     // point-Jacobi loop: RESID (serves INIT) ; WHILE(any active) { JAC }
     cudaGraph_t jgraph = nullptr;
     cudaGraphExec_t jgraph_exec = nullptr;
+    // one GMRES(m) restart cycle (all Arnoldi passes, FORM, RESID) captured once
+    cudaGraph_t ggraph = nullptr;
+    cudaGraphExec_t ggraph_exec = nullptr;
+    long long gcycle_kernels = 0;
+    cudaStream_t cap_stream = nullptr;
     int run_kind = KIND_CG;    // solve armed last: bs_run drives its loop
     int pgrid = -1;            // persistent CG grid (co-resident CTAs), -1 = not computed
     bool jac_dirty = false;    // a Jacobi iterate may sit in p[0] (flush before other solves)
@@ -2473,6 +2478,9 @@ int bs_ctx_destroy(bs_ctx *c) {
     if (c->graph) cudaGraphDestroy(c->graph);
     if (c->jgraph_exec) cudaGraphExecDestroy(c->jgraph_exec);
     if (c->jgraph) cudaGraphDestroy(c->jgraph);
+    if (c->ggraph_exec) cudaGraphExecDestroy(c->ggraph_exec);
+    if (c->ggraph) cudaGraphDestroy(c->ggraph);
+    if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
     cudaFree(c->dblocks);
     cudaFree(c->dstates);
     cudaFree(c->dtmaps);
@@ -2756,6 +2764,10 @@ int bs_gmres_setup(bs_ctx *c, int m, const bs_gmres_desc *descs) {
     }
     cudaFree(c->dgmaps);
     c->dgmaps = nullptr;
+    if (c->ggraph_exec) cudaGraphExecDestroy(c->ggraph_exec);  // captured the old maps
+    if (c->ggraph) cudaGraphDestroy(c->ggraph);
+    c->ggraph_exec = nullptr;
+    c->ggraph = nullptr;
     if (!c->dgstates) BS_CU(cudaMalloc(&c->dgstates, sizeof(GState) * c->nblocks));
     BS_CU(cudaMalloc(&c->dgmaps, sizeof(CUtensorMap) * maps.size()));
     BS_CU(cudaMemcpy(c->dgmaps, maps.data(), sizeof(CUtensorMap) * maps.size(), cudaMemcpyHostToDevice));
@@ -2790,16 +2802,35 @@ int bs_gmres_run(bs_ctx *c, int max_cycles, void *stream, int64_t *kernels_out) 
     cudaStream_t st = (cudaStream_t)stream;
     const unsigned long long l0 = g_launches;
     launch_sweep<OP_RESID>(c, st, -1);  // INIT: rhs assembly + r0 (inner_solvers.py:153-159)
+    if (!c->ggraph_exec) {
+        // one restart cycle as a CUDA graph: m Arnoldi steps (NORM, SPMV + h0j,
+        // MGS passes, FINAL), FORM, true residual — 3m + m(m-1)/2 + 2 kernels
+        // replayed per cycle without host launch overhead
+        if (!c->cap_stream) BS_CU(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+        cudaStream_t cs = c->cap_stream;
+        const unsigned long long g0 = g_launches;
+        BS_CU(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        for (int j = 0; j < c->gm; ++j) {  // one Arnoldi step per j; finished blocks skip
+            launch_point<PK_NORM>(c, cs, j, 0);
+            launch_gspmv(c, cs, j);
+            for (int i = 1; i <= j; ++i) launch_point<PK_MGS>(c, cs, j, i);
+            launch_point<PK_FINAL>(c, cs, j, 0);
+        }
+        launch_point<PK_FORM>(c, cs, 0, 0);
+        launch_sweep<OP_RESID>(c, cs, -1);  // true residual -> stop or restart
+        cudaGraph_t g = nullptr;
+        BS_CU(cudaStreamEndCapture(cs, &g));
+        c->gcycle_kernels = (long long)(g_launches - g0);
+        g_launches = g0;  // captured, not launched
+        cudaGraphExec_t ex = nullptr;
+        BS_CU(cudaGraphInstantiate(&ex, g, 0));
+        c->ggraph = g;
+        c->ggraph_exec = ex;
+    }
     int cycles = 0;
     for (;;) {
-        for (int j = 0; j < c->gm; ++j) {  // one Arnoldi step per j; finished blocks skip
-            launch_point<PK_NORM>(c, st, j, 0);
-            launch_gspmv(c, st, j);
-            for (int i = 1; i <= j; ++i) launch_point<PK_MGS>(c, st, j, i);
-            launch_point<PK_FINAL>(c, st, j, 0);
-        }
-        launch_point<PK_FORM>(c, st, 0, 0);
-        launch_sweep<OP_RESID>(c, st, -1);  // true residual -> stop or restart
+        BS_CU(cudaGraphLaunch(c->ggraph_exec, st));
+        g_launches += c->gcycle_kernels;
         BS_CU(cudaGetLastError());
         BS_CU(cudaMemcpyAsync(c->hpinned, c->dnactive, sizeof(int), cudaMemcpyDeviceToHost, st));
         BS_CU(cudaStreamSynchronize(st));
