@@ -537,3 +537,28 @@ def test_block_system_spmv_and_solves_public_api():
         assert np.linalg.norm(x - xo) <= 1e-9 * np.linalg.norm(xo)
         _, rel = bs.residual_norms(op, x, rhs)
         assert rel <= 1e-9
+
+
+def test_full_size_512_size_independent_properties():
+    """BASELINE configs 3/4 grid size (512^3 = 134M unknowns, one block):
+    SpMV bit-identical to the matrix-free oracle on a slab of planes checked
+    in place (stencil rows only see z +- 1), SpMV of a constant = exact face
+    counts, and a CG solve to 1e-8 whose true residual meets the tolerance."""
+    import torch
+
+    n = 512
+    op = bs.StencilOperator(n, n, n)
+    x = bs.seeded_rhs(n ** 3, 7, device="cuda")
+    y = bs.spmv(op, x)
+    xs = x.view(n, n, n)[200:204].cpu().numpy()  # planes 200..203 -> rows 201, 202 are exact
+    ys = O.stencil_apply(np.concatenate([xs], axis=0)).reshape(4, n, n)
+    assert np.array_equal(y.view(n, n, n)[201:203].cpu().numpy(), ys[1:3])
+    ones = torch.ones(n ** 3, dtype=torch.float64, device="cuda")
+    y1 = bs.spmv(op, ones).view(n, n, n)
+    assert float(y1[1:-1, 1:-1, 1:-1].abs().max()) == 0.0  # interior rows of A*1 vanish exactly
+    assert float(y1[0, 0, 0]) == 3.0 and float(y1[0, 5, 5]) == 1.0
+    b = bs.seeded_rhs(n ** 3, 0, device="cuda")
+    xs, rep = bs.cg_solve(op, b, torch.zeros_like(b), bs.InnerSolverSpec("cg", 5000, 1e-8))
+    assert rep.stop_reason == "tolerance_met"
+    _, rel = bs.residual_norms(op, xs, b)
+    assert rel <= 1e-8
