@@ -138,6 +138,10 @@ enum GFlag : int { GF_NONE = 0, GF_HAPPY = 1, GF_CHECK = 2, GF_CYCLE = 3 };
 // Fewer bytes per stage buys a deeper ring in about the same shared memory,
 // so every op keeps ~60 KB of loads in flight per CTA.
 __host__ __device__ constexpr bool op_has_b(int op) { return op == OP_RESID || op == OP_S1; }
+#ifndef BS_REV_S2
+#define BS_REV_S2 1
+#endif
+__host__ __device__ constexpr bool op_rev(int op) { return BS_REV_S2 && op == OP_S2; }
 __host__ __device__ constexpr int op_stages(int op) { return op_has_b(op) ? BS_NSTAGE_AB : BS_NSTAGE_A; }
 __host__ __device__ constexpr int op_coff(int op) { return op_has_b(op) ? 2 * SEG_H : SEG_H; }
 __host__ __device__ constexpr int op_stage_bytes(int op) { return op_coff(op) + SEG_O; }
@@ -556,6 +560,13 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 // BOX (overlap 0, region == padded box): TMA zero-fill supplies the absent
 // neighbours, presence tests are local-coordinate compares and couplings only
 // exist on the box faces.  !BOX evaluates the L1-dilated region analytically.
+//
+// Direction: S2 walks its planes top-down (op_rev).  A CG iteration is S1
+// then S2, so consecutive sweeps always run in opposite z order and the
+// planes one sweep touched last (still in the 126 MB L2) are the first the
+// next one reads.  Per point the arithmetic is the same in both directions
+// (the stencil chain is fixed by column order, not by traversal); only the
+// order of a thread's partial sums moves, deterministically per op.
 template <int OP, bool BOX>
 __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, double (&acc)[NQ]) {
     const DBlock &B = *C.B;
@@ -571,7 +582,10 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
     const int lx0 = ix * TX, ly0 = iy * TY;  // tile origin, padded-box coordinates
     const int lz0 = iz * cz;
     const int lz1 = min(lz0 + cz, pdz);
-    const int nplanes = lz1 - lz0 + 2;       // q = 0..nplanes-1 <-> lz = lz0-1+q
+    const int nplanes = lz1 - lz0 + 2;       // q = 0..nplanes-1 <-> lz = lz0-1+q (lz1-q reversed)
+    constexpr bool REV = op_rev(OP);
+    constexpr int DZ = REV ? -1 : 1;
+    const int lzq0 = REV ? lz1 : lz0 - 1;    // plane of q = 0; plane q is lzq0 + DZ*q
 
     constexpr int NS = op_stages(OP);
     constexpr int STB = op_stage_bytes(OP);
@@ -596,7 +610,7 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
             for (int q = 0; q < nplanes; ++q) {
                 const int s = q % NS;
                 if (q >= NS) mbar_wait(&empty[s], (uint32_t)((q / NS - 1) & 1));
-                const int lz = lz0 - 1 + q;
+                const int lz = lzq0 + DZ * q;
                 const bool epi = use_c && q >= 1 && q <= nplanes - 2;
                 unsigned char *st = smem + s * STB;
                 const uint32_t bytes = (uint32_t)(SC * 8) * (use_b ? 2u : 1u) + (epi ? (uint32_t)SEG_O : 0u);
@@ -618,7 +632,7 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
     const int lx = lx0 + tx, ly_0 = ly0 + ty * RY;
     const int gi = B.plo[0] + lx;
     const long long plane = (long long)B.pitch * pdy;
-    long long sx = (long long)lx + (long long)B.pitch * ((long long)ly_0 + (long long)pdy * lz0);
+    long long sx = (long long)lx + (long long)B.pitch * ((long long)ly_0 + (long long)pdy * (lzq0 + DZ));
     const double beta = C.beta, alpha = C.alpha, alpha_pend = C.alpha_pend;
     const bool pend = C.pend, first = C.first;
     const long long pitch = B.pitch;
@@ -648,10 +662,10 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
     mbar_wait(&full[0], 0u);
     if (tid == 0) BS_STAMP(1);
 #pragma unroll
-    for (int r = 0; r < RY; ++r) u_prev[r] = uval(smem, own[r], 0, gjr[r], lz0 - 1);
+    for (int r = 0; r < RY; ++r) u_prev[r] = uval(smem, own[r], 0, gjr[r], lzq0);
     mbar_wait(&full[1], 0u);
 #pragma unroll
-    for (int r = 0; r < RY; ++r) u_cur[r] = uval(smem + STB, own[r], 0, gjr[r], lz0);
+    for (int r = 0; r < RY; ++r) u_cur[r] = uval(smem + STB, own[r], 0, gjr[r], lzq0 + DZ);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[0]);
 
@@ -670,8 +684,10 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
     // loop below is unrolled by NS so both are compile-time per step: `s`
     // (this plane's stage), `sn` (the next plane's) and `par_n` (the next
     // plane's parity) are constants or one loop-carried bit.
+    // u_prev / u_next are the planes behind / ahead in traversal order: the
+    // z-1 / z+1 neighbours forward, z+1 / z-1 reversed.
     auto single_step = [&](int q, int s, int sn, uint32_t par_n) {
-        const int lz = lz0 - 1 + q;
+        const int lz = lzq0 + DZ * q;
         const unsigned char *st = smem + s * STB;
         const double *cst = reinterpret_cast<const double *>(st + COFF);
         // Phase A, before plane q+1 is waited for: the in-plane neighbours and,
@@ -687,11 +703,13 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
             ym_[r] = r > 0 ? u_cur[r > 0 ? r - 1 : 0] : uval(st, own[r] - SX, 0, gj - 1, lz);
             yp_[r] = r < RY - 1 ? u_cur[r < RY - 1 ? r + 1 : 0] : uval(st, own[r] + SX, 0, gj + 1, lz);
             pre_[r] = fast ? add(add(add(add(-ym_[r], -xm_[r]), mul(6.0, u_cur[r])), -xp_[r]), -yp_[r]) : 0.0;
+            // reversed: z+1 is the plane behind, so it enters the chain now
+            if (REV && fast) pre_[r] = add(pre_[r], -u_prev[r]);
         }
         mbar_wait(&full[sn], par_n & 1u);
         double u_next[RY];
 #pragma unroll
-        for (int r = 0; r < RY; ++r) u_next[r] = uval(smem + sn * STB, own[r], 0, gjr[r], lz + 1);
+        for (int r = 0; r < RY; ++r) u_next[r] = uval(smem + sn * STB, own[r], 0, gjr[r], lz + DZ);
 #pragma unroll
         for (int r = 0; r < RY; ++r) {
             const int ly = ly_0 + r;
@@ -699,12 +717,13 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
             const bool here = BOX ? row_in[r] : (row_in[r] && in_region(B, gi, gj, B.plo[2] + lz));
             if (!here) continue;
             const double xm = xm_[r], xp = xp_[r], ym = ym_[r], yp = yp_[r];
+            const double zm = REV ? u_next[r] : u_prev[r], zp = REV ? u_prev[r] : u_next[r];
             const long long sxr = sx + (long long)r * pitch;
             double au, od = 0.0;
             if (fast) {
-                // = stencil7_interior(u_prev, ym, xm, u_cur, xp, yp, u_next), same association
-                au = add(-u_prev[r], add(pre_[r], -u_next[r]));
-                if (OP == OP_JAC) od = offdiag6(u_prev[r], ym, xm, xp, yp, u_next[r], true, true, true, true, true, true);
+                // = stencil7_interior(zm, ym, xm, u_cur, xp, yp, zp), same association
+                au = REV ? add(-zm, pre_[r]) : add(-zm, add(pre_[r], -zp));
+                if (OP == OP_JAC) od = offdiag6(zm, ym, xm, xp, yp, zp, true, true, true, true, true, true);
             } else {
                 bool pz, py, px;
                 if (BOX) {
@@ -717,7 +736,7 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
                     py = in_region(B, gi, gj - 1, gk);
                     px = in_region(B, gi - 1, gj, gk);
                 }
-                au = stencil7(u_prev[r], ym, xm, u_cur[r], xp, yp, u_next[r], pz, py, px);
+                au = stencil7(zm, ym, xm, u_cur[r], xp, yp, zp, pz, py, px);
                 if (OP == OP_JAC) {
                     bool qz, qy, qx;
                     if (BOX) {
@@ -730,7 +749,7 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
                         qy = in_region(B, gi, gj + 1, gk);
                         qx = in_region(B, gi + 1, gj, gk);
                     }
-                    od = offdiag6(u_prev[r], ym, xm, xp, yp, u_next[r], pz, py, px, qx, qy, qz);
+                    od = offdiag6(zm, ym, xm, xp, yp, zp, pz, py, px, qx, qy, qz);
                 }
             }
             const int ci = (ty * RY + r) * TX + tx;  // bare-tile cell
@@ -757,10 +776,10 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
                 double rhs = bv, rg_au = au;
                 if (face) {
                     if (BOX)
-                        face_coupling_box(B, lx, ly, lz, bv, u_prev[r], ym, xm, u_cur[r], xp, yp, u_next[r],
+                        face_coupling_box(B, lx, ly, lz, bv, zm, ym, xm, u_cur[r], xp, yp, zp,
                                           OP == OP_RESID, rhs, rg_au);
                     else  // out of line: keeps the interior path lean
-                        face_coupling(B, gi, gj, gk, bv, u_prev[r], ym, xm, u_cur[r], xp, yp, u_next[r],
+                        face_coupling(B, gi, gj, gk, bv, zm, ym, xm, u_cur[r], xp, yp, zp,
                                       OP == OP_RESID, rhs, rg_au);
                 }
                 const double rv = sub(rhs, au);
@@ -782,7 +801,7 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
                 }
             }
         }
-        sx += plane;
+        sx += DZ * plane;
 #pragma unroll
         for (int r = 0; r < RY; ++r) {
             u_prev[r] = u_cur[r];
@@ -1172,8 +1191,8 @@ __device__ void finish_block(const KParams &P, int b, int ph, bool served, doubl
 
 template <int NTH, int OPK, bool POINT = false>
 __device__ void finish(const KParams &P, int b, int ph, bool served, double (&acc)[NQ], int nq,
-                       unsigned char *smem) {
-    finish_block<NTH, POINT>(P, b, ph, served, acc, nq, smem, blockIdx.x);
+                       unsigned char *smem, int vcta) {
+    finish_block<NTH, POINT>(P, b, ph, served, acc, nq, smem, vcta);
     // Pointwise (GMRES) passes are host-sequenced and never end a loop: the
     // launch-level bookkeeping (one atomic per CTA on a single counter) is
     // only needed by sweeps.
@@ -1269,7 +1288,11 @@ __host__ __device__ constexpr int op_nq() { return OPK == OP_RESID ? NQ : (OPK =
 template <int OPK, bool BOX>
 __global__ void __launch_bounds__(NTHR, BS_MINBLOCKS) k_sweep(const KParams P) {
     extern __shared__ __align__(1024) unsigned char smem[];
-    const int b = P.cta_block[blockIdx.x];
+    // reversed sweeps also take the tiles in reverse order: with more tiles
+    // than resident CTAs, the last wave of the previous sweep is the first
+    // wave of this one (L2 reuse across the sweep boundary)
+    const int cta = op_rev(OPK) ? P.nctas - 1 - (int)blockIdx.x : (int)blockIdx.x;
+    const int b = P.cta_block[cta];
     const DBlock &B = P.blocks[b];
     const DState S = P.states[b];
     const int ph = S.phase;
@@ -1285,10 +1308,10 @@ __global__ void __launch_bounds__(NTHR, BS_MINBLOCKS) k_sweep(const KParams P) {
 #endif
     if (served) {
         const SweepCtx C = make_ctx<OPK>(P, b, B, S);
-        sweep_tile<OPK, BOX>(C, blockIdx.x - B.cta_begin, smem, acc);
+        sweep_tile<OPK, BOX>(C, cta - B.cta_begin, smem, acc);
         __syncthreads();  // all planes consumed: the stage ring is free for reuse
     }
-    finish<NTHR, OPK>(P, b, ph, served, acc, op_nq<OPK>(), smem);
+    finish<NTHR, OPK>(P, b, ph, served, acc, op_nq<OPK>(), smem, cta);
     if (threadIdx.x == 0) BS_STAMP(3);
 }
 
@@ -1307,7 +1330,8 @@ template <int OPK, bool BOX>
 __device__ void persist_sweep(const KParams &P, unsigned char *smem, const DState *s_states, bool central,
                               int sw) {
     BS_PSTAMP(sw, 0);
-    for (int t = blockIdx.x; t < P.nctas; t += gridDim.x) {
+    for (int t0 = blockIdx.x; t0 < P.nctas; t0 += gridDim.x) {
+        const int t = op_rev(OPK) ? P.nctas - 1 - t0 : t0;  // as k_sweep
         const int b = P.cta_block[t];
         const DBlock &B = P.blocks[b];
         const DState S = central ? ld_state_head(P.states + b) : ld_state(P.states + b);
@@ -1603,7 +1627,7 @@ __global__ void __launch_bounds__(NPT) k_point(const KParams P) {
             }
         }
     }
-    finish<NPT, -1, true>(P, b, ph, served, acc, PKK == PK_OWNRES ? NQ : 1, smem);
+    finish<NPT, -1, true>(P, b, ph, served, acc, PKK == PK_OWNRES ? NQ : 1, smem, blockIdx.x);
 }
 
 // ---- overlapping merge (multisplit.py:341-369), overlap > 0.  Inputs are the
