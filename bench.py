@@ -64,6 +64,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
                     help="cross-GPU halo transport of the sharded outer workloads")
+    ap.add_argument("--max-outer", type=int, default=100000,
+                    help="outer-sweep cap of the supplemental workloads (bounded runs at full size)")
     ap.add_argument("--workload", default="config2", choices=["config2", "config3", "config4", "config5"],
                     help="config2 (default, the bench line); config3/4/5 = outer block-Jacobi solves (supplemental)")
     return ap.parse_args()
@@ -391,6 +393,28 @@ OUTER_WORKLOADS = {
 }
 
 
+def region_sizes(n, block_grid, overlap):
+    """Points of each block's extended region: the owned box dilated `overlap`
+    times by the 7-point stencil (an L1 ball, problems.py:178-190) clipped to
+    the n^3 grid, counted analytically (SURVEY §8 notation N_b)."""
+    from paper_2009_12638_b200.problems import _split_ranges
+
+    sizes = []
+    gx, gy, gz = block_grid
+    for bz in range(gz):
+        for by in range(gy):
+            for bx in range(gx):
+                counts = []
+                for g, bi in ((gx, bx), (gy, by), (gz, bz)):
+                    lo, hi = _split_ranges(n, g)[bi]
+                    # c[k]: coordinates at distance k outside [lo, hi) on this axis
+                    counts.append([hi - lo] + [int(lo - k >= 0) + int(hi - 1 + k < n) for k in range(1, overlap + 1)])
+                cx, cy, cz = counts
+                sizes.append(sum(cx[a] * cy[b] * cz[c] for a in range(overlap + 1) for b in range(overlap + 1)
+                                 for c in range(overlap + 1) if a + b + c <= overlap))
+    return sizes
+
+
 def run_outer_workload(args):
     """Supplemental: time-to-solution of the outer block-Jacobi configs on this
     box (1 GPU: all blocks on one device; torchrun N>1: config3 sharded)."""
@@ -416,7 +440,7 @@ def run_outer_workload(args):
         prob = bs.LinearProblem(bs.StencilOperator(n, n, n), np.random.default_rng(0).uniform(-1.0, 1.0, N), grid)
     kind, its, itol = w["inner"]
     cfg = bs.OuterConfig(block_grid=w["block_grid"], overlap=w["overlap"], inner=bs.InnerSolverSpec(kind, its, itol),
-                         mode=w["mode"], tol=w["tol"], max_outer=100000, tolerance_basis=w["basis"],
+                         mode=w["mode"], tol=w["tol"], max_outer=args.max_outer, tolerance_basis=w["basis"],
                          residual_check_every=w["every"], execution="threads" if w["mode"] == "async" else "replay")
     from paper_2009_12638_b200.distributed import outer_solve_distributed
 
@@ -448,6 +472,17 @@ def run_outer_workload(args):
     if w["overlap"] == 0:
         # sum over sweeps and blocks of N_b (64 its_b + 64)
         alg = sum((N / nb) * (64 * i + 64) for row in res.inner_iterations_per_block for i in row)
+    elif kind == "gmres":
+        # Arnoldi step j of a GMRES(m) cycle moves 32 + 24 (j + 1)
+        # B/pt (SpMV, j + 1 MGS passes, normalisation) over the block's region
+        # (N_b = owned box dilated by the overlap), + 64 B/pt outer overhead
+        sizes = region_sizes(n, w["block_grid"], w["overlap"])
+        m = 30
+
+        def block_bytes(its):
+            return sum(32 + 24 * ((j % m) + 1) for j in range(its)) + 64
+
+        alg = sum(sizes[b] * block_bytes(i) for row in res.inner_iterations_per_block for b, i in enumerate(row))
     else:
         alg = None
     hbm = peaks()[0]
@@ -456,6 +491,8 @@ def run_outer_workload(args):
                 "grid": [n, n, n], "n_gpus": world, "config": {k: (list(v) if isinstance(v, tuple) else v)
                                                              for k, v in w.items()},
                 "time_to_solution_s": tts, "outer_sweeps": res.outer_iterations, "converged": res.converged,
+                "seconds_per_sweep": tts / max(1, res.outer_iterations), "max_outer": args.max_outer,
+                "estimates": [row.estimated_residual for row in res.trace.rows][-3:],
                 "final_true_residual": res.final_true_residual, "inner_iterations_total": total_its,
                 "stencil_gpts_per_s": (pts_its / tts / 1e9) if pts_its else None,
                 "hbm_fraction": (alg / tts / 1e9 / (hbm * world)) if alg else None,

@@ -155,6 +155,15 @@ int bs_gmres_begin(bs_ctx *ctx, int max_iterations, double tolerance, int basis,
  * counter.  Finished blocks skip the remaining launches.  Blocking. */
 int bs_gmres_run(bs_ctx *ctx, int max_cycles, void *stream, int64_t *kernels_out);
 
+/* The same for block `block` alone: every launch covers only that block's
+ * CTAs and only its solve is polled.  Blocks solved one after another this
+ * way may share one V/W workspace (bs_gmres_setup with equal pointers),
+ * which is what lets eight 514^3 blocks of a 1024^3 grid with GMRES(30)
+ * fit one GPU (one basis: 34 GB instead of 270 GB).  Same results, bit
+ * for bit, as the all-block run (multisplit.py:562-580: the sweep-k inner
+ * solves are independent). */
+int bs_gmres_run_block(bs_ctx *ctx, int block, int max_cycles, void *stream, int64_t *kernels_out);
+
 /* Run armed solves to completion with device-side stopping.  Default: one
  * CUDA-graph launch whose WHILE node iterates {CG sweep 1, CG sweep 2,
  * IF(any block verifying) residual sweep} until no block is active — no host

@@ -138,6 +138,9 @@ enum GFlag : int { GF_NONE = 0, GF_HAPPY = 1, GF_CHECK = 2, GF_CYCLE = 3 };
 // Fewer bytes per stage buys a deeper ring in about the same shared memory,
 // so every op keeps ~60 KB of loads in flight per CTA.
 __host__ __device__ constexpr bool op_has_b(int op) { return op == OP_RESID || op == OP_S1; }
+#ifndef BS_EASY
+#define BS_EASY 1  // interior planes of dilated regions take the box logic (sweep_tile)
+#endif
 #ifndef BS_REV_S2
 #define BS_REV_S2 1
 #endif
@@ -228,6 +231,7 @@ struct KParams {
     GState *gstates;
     const CUtensorMap *gmaps;  // per block: V[0..MAXM-1] haloed, [MAXM] = V[0] bare
     int launch_j, launch_i;    // GMRES step served by this launch
+    int cta_base, pcta_base;   // first CTA-table entry of this launch (one-block launches)
 };
 
 // ------------------------------------------------------------------ geometry
@@ -643,10 +647,18 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
         if (OP == OP_S1) return first ? a : add(a, mul(beta, reinterpret_cast<const double *>(st + SEG_H)[cell]));
         return a;
     };
+    // !BOX: a plane is `easy` for a warp when every point it computes lies at
+    // L1 distance <= overlap-1 from the owned box.  Every in-grid neighbour of
+    // such a point is then in the region (distance grows by at most 1 per
+    // step), none sits on the padded box's edge unless the grid ends there,
+    // and no coupling exists: the BOX logic (unmasked values, local-coordinate
+    // presence, no face terms) is exact for it.  Only the outer shell of the
+    // region (about 1% of a 514^3 block) takes the analytic path.
+    bool easy = BOX;
     // u at (row gj_, x + dx) of plane lz (local z), masked to the region for !BOX
     auto uval = [&](const unsigned char *st, int cell, int dx, int gj_, int lz) -> double {
         const double v = val(st, cell);
-        if (BOX) return v;
+        if (BOX || easy) return v;
         return in_region(B, gi + dx, gj_, B.plo[2] + lz) ? v : 0.0;
     };
     int own[RY], gjr[RY];
@@ -672,7 +684,7 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
     const bool px_box = lx > 0;
     // warp-uniform fast path: every lane of this warp has its x-1 and y-1
     // neighbours in the box for all its rows
-    const bool warp_xy_interior = BOX && __all_sync(0xffffffffu, px_box && ly_0 > 0);
+    const bool warp_xy_interior = __all_sync(0xffffffffu, px_box && ly_0 > 0);
     // output pointers hoisted into registers: stores through them cannot alias
     // the block descriptor, so the compiler need not re-load it every plane
     double *__restrict__ out_r = B.r;
@@ -693,7 +705,14 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
         // Phase A, before plane q+1 is waited for: the in-plane neighbours and,
         // on the interior fast path, the reduceat chain up to its last term
         // (z+1 enters second to last), so the wait overlaps the DP latency.
-        const bool fast = BOX && warp_xy_interior && lz > 0;
+        if (!BOX && BS_EASY) {
+            const int gk = B.plo[2] + lz;
+            bool e = true;
+#pragma unroll
+            for (int r = 0; r < RY; ++r) e = e && (!row_in[r] || box_dist1(B, gi, gjr[r], gk) < B.overlap);
+            easy = __all_sync(0xffffffffu, e);
+        }
+        const bool fast = easy && warp_xy_interior && lz > 0;
         double xm_[RY], xp_[RY], ym_[RY], yp_[RY], pre_[RY];
 #pragma unroll
         for (int r = 0; r < RY; ++r) {
@@ -714,7 +733,7 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
         for (int r = 0; r < RY; ++r) {
             const int ly = ly_0 + r;
             const int gj = gjr[r];
-            const bool here = BOX ? row_in[r] : (row_in[r] && in_region(B, gi, gj, B.plo[2] + lz));
+            const bool here = (BOX || easy) ? row_in[r] : (row_in[r] && in_region(B, gi, gj, B.plo[2] + lz));
             if (!here) continue;
             const double xm = xm_[r], xp = xp_[r], ym = ym_[r], yp = yp_[r];
             const double zm = REV ? u_next[r] : u_prev[r], zp = REV ? u_prev[r] : u_next[r];
@@ -726,7 +745,7 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
                 if (OP == OP_JAC) od = offdiag6(zm, ym, xm, xp, yp, zp, true, true, true, true, true, true);
             } else {
                 bool pz, py, px;
-                if (BOX) {
+                if (BOX || easy) {
                     pz = lz > 0;
                     py = ly > 0;
                     px = px_box;
@@ -739,7 +758,7 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
                 au = stencil7(zm, ym, xm, u_cur[r], xp, yp, zp, pz, py, px);
                 if (OP == OP_JAC) {
                     bool qz, qy, qx;
-                    if (BOX) {
+                    if (BOX || easy) {
                         qz = lz < pdz - 1;
                         qy = ly < pdy - 1;
                         qx = lx < pdx - 1;
@@ -771,8 +790,9 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
             } else {  // OP_RESID: r = (b - C*halo) - A_ii u ; OP_JAC: also the Jacobi update
                 const double bv = cst[ci];
                 const int gk = B.plo[2] + lz;
-                const bool face = !BOX || lx == 0 || ly == 0 || lz == 0 || lx == pdx - 1 || ly == pdy - 1 ||
-                                  lz == pdz - 1;
+                const bool face = BOX ? (lx == 0 || ly == 0 || lz == 0 || lx == pdx - 1 || ly == pdy - 1 ||
+                                         lz == pdz - 1)
+                                      : !easy;
                 double rhs = bv, rg_au = au;
                 if (face) {
                     if (BOX)
@@ -1203,7 +1223,7 @@ __device__ void finish(const KParams &P, int b, int ph, bool served, double (&ac
     if (tid == 0) {
         __threadfence();
         const unsigned prev = atomicAdd(P.launch_counter, 1u);
-        *flag = (prev == (unsigned)nctas - 1u);
+        *flag = (prev == gridDim.x - 1u);
     }
     __syncthreads();
     if (!*flag || tid != 0) return;
@@ -1291,7 +1311,7 @@ __global__ void __launch_bounds__(NTHR, BS_MINBLOCKS) k_sweep(const KParams P) {
     // reversed sweeps also take the tiles in reverse order: with more tiles
     // than resident CTAs, the last wave of the previous sweep is the first
     // wave of this one (L2 reuse across the sweep boundary)
-    const int cta = op_rev(OPK) ? P.nctas - 1 - (int)blockIdx.x : (int)blockIdx.x;
+    const int cta = P.cta_base + (op_rev(OPK) ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x);
     const int b = P.cta_block[cta];
     const DBlock &B = P.blocks[b];
     const DState S = P.states[b];
@@ -1497,7 +1517,8 @@ __global__ void __launch_bounds__(NTHR, 2) k_cg_persistent(const KParams P) {
 template <int PKK, bool BOX>
 __global__ void __launch_bounds__(NPT) k_point(const KParams P) {
     extern __shared__ __align__(1024) unsigned char smem[];
-    const int b = P.pcta_block[blockIdx.x];
+    const int pc = P.pcta_base + (int)blockIdx.x;
+    const int b = P.pcta_block[pc];
     const DBlock &B = P.blocks[b];
     const DState S = P.states[b];
     const int ph = S.phase;
@@ -1512,7 +1533,7 @@ __global__ void __launch_bounds__(NPT) k_point(const KParams P) {
         const GState &G = P.gstates[b];
         const int tid = threadIdx.x;
         const long long n = (long long)B.pitch * B.pdim[1] * B.pdim[2];
-        const long long base = (long long)(blockIdx.x - B.pcta_begin) * PCHUNK;
+        const long long base = (long long)(pc - B.pcta_begin) * PCHUNK;
         const int j = S.gj, i = S.gi;
         const long long vs = B.vstride;
         double *__restrict__ W = B.W;
@@ -1627,7 +1648,7 @@ __global__ void __launch_bounds__(NPT) k_point(const KParams P) {
             }
         }
     }
-    finish<NPT, -1, true>(P, b, ph, served, acc, PKK == PK_OWNRES ? NQ : 1, smem, blockIdx.x);
+    finish<NPT, -1, true>(P, b, ph, served, acc, PKK == PK_OWNRES ? NQ : 1, smem, pc);
 }
 
 // ---- overlapping merge (multisplit.py:341-369), overlap > 0.  Inputs are the
@@ -2107,6 +2128,7 @@ struct bs_ctx {
     // one GMRES(m) restart cycle (all Arnoldi passes, FORM, RESID) captured once
     cudaGraph_t ggraph = nullptr;
     cudaGraphExec_t ggraph_exec = nullptr;
+    std::vector<cudaGraphExec_t> ggraph_blk;  // the same per block (one-block runs)
     long long gcycle_kernels = 0;
     cudaStream_t cap_stream = nullptr;
     int run_kind = KIND_CG;    // solve armed last: bs_run drives its loop
@@ -2163,29 +2185,49 @@ KParams make_params(bs_ctx *c, bool graph, cudaGraphConditionalHandle hl = 0,
     P.gmaps = c->dgmaps;
     P.launch_j = 0;
     P.launch_i = 0;
+    P.cta_base = 0;
+    P.pcta_base = 0;
     return P;
 }
 
+// Grid of a sweep (pointwise) launch over every block (blk < 0) or only
+// block blk's CTA range, with the matching CTA-table base in P.
+int sweep_grid(bs_ctx *c, KParams &P, int blk) {
+    if (blk < 0) return c->nctas;
+    const DBlock &B = c->hblocks[blk];
+    P.cta_base = B.cta_begin;
+    return B.cta_end - B.cta_begin;
+}
+
+int point_grid(bs_ctx *c, KParams &P, int blk) {
+    if (blk < 0) return c->npctas;
+    const DBlock &B = c->hblocks[blk];
+    P.pcta_base = B.pcta_begin;
+    return B.pcta_end - B.pcta_begin;
+}
+
 template <int PKK>
-void launch_point(bs_ctx *c, cudaStream_t st, int j, int i) {
+void launch_point(bs_ctx *c, cudaStream_t st, int j, int i, int blk = -1) {
     KParams P = make_params(c, false);
     P.launch_j = j;
     P.launch_i = i;
+    const int grid = point_grid(c, P, blk);
     constexpr int smem = (NQ * (NPT / 32) + 256 + 8) * 8;
     if (c->box)
-        k_point<PKK, true><<<c->npctas, NPT, smem, st>>>(P);
+        k_point<PKK, true><<<grid, NPT, smem, st>>>(P);
     else
-        k_point<PKK, false><<<c->npctas, NPT, smem, st>>>(P);
+        k_point<PKK, false><<<grid, NPT, smem, st>>>(P);
     ++g_launches;
 }
 
-void launch_gspmv(bs_ctx *c, cudaStream_t st, int j) {
+void launch_gspmv(bs_ctx *c, cudaStream_t st, int j, int blk = -1) {
     KParams P = make_params(c, false);
     P.launch_j = j;
+    const int grid = sweep_grid(c, P, blk);
     if (c->box)
-        k_sweep<OP_GSPMV, true><<<c->nctas, NTHR, op_smem(OP_GSPMV), st>>>(P);
+        k_sweep<OP_GSPMV, true><<<grid, NTHR, op_smem(OP_GSPMV), st>>>(P);
     else
-        k_sweep<OP_GSPMV, false><<<c->nctas, NTHR, op_smem(OP_GSPMV), st>>>(P);
+        k_sweep<OP_GSPMV, false><<<grid, NTHR, op_smem(OP_GSPMV), st>>>(P);
     ++g_launches;
 }
 
@@ -2195,13 +2237,14 @@ void *sweep_fn(bool box) {
 }
 
 template <int OPK>
-void launch_sweep(bs_ctx *c, cudaStream_t st, int slot) {
-    const KParams P = make_params(c, false);
+void launch_sweep(bs_ctx *c, cudaStream_t st, int slot, int blk = -1) {
+    KParams P = make_params(c, false);
+    const int grid = sweep_grid(c, P, blk);
     if (c->timing && slot >= 0) cudaEventRecord(c->ev[2 * slot], st);
     if (c->box)
-        k_sweep<OPK, true><<<c->nctas, NTHR, op_smem(OPK), st>>>(P);
+        k_sweep<OPK, true><<<grid, NTHR, op_smem(OPK), st>>>(P);
     else
-        k_sweep<OPK, false><<<c->nctas, NTHR, op_smem(OPK), st>>>(P);
+        k_sweep<OPK, false><<<grid, NTHR, op_smem(OPK), st>>>(P);
     if (c->timing && slot >= 0) cudaEventRecord(c->ev[2 * slot + 1], st);
     ++g_launches;
 }
@@ -2504,6 +2547,8 @@ int bs_ctx_destroy(bs_ctx *c) {
     if (c->jgraph) cudaGraphDestroy(c->jgraph);
     if (c->ggraph_exec) cudaGraphExecDestroy(c->ggraph_exec);
     if (c->ggraph) cudaGraphDestroy(c->ggraph);
+    for (cudaGraphExec_t e : c->ggraph_blk)
+        if (e) cudaGraphExecDestroy(e);
     if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
     cudaFree(c->dblocks);
     cudaFree(c->dstates);
@@ -2792,6 +2837,10 @@ int bs_gmres_setup(bs_ctx *c, int m, const bs_gmres_desc *descs) {
     if (c->ggraph) cudaGraphDestroy(c->ggraph);
     c->ggraph_exec = nullptr;
     c->ggraph = nullptr;
+    for (cudaGraphExec_t &e : c->ggraph_blk) {
+        if (e) cudaGraphExecDestroy(e);
+        e = nullptr;
+    }
     if (!c->dgstates) BS_CU(cudaMalloc(&c->dgstates, sizeof(GState) * c->nblocks));
     BS_CU(cudaMalloc(&c->dgmaps, sizeof(CUtensorMap) * maps.size()));
     BS_CU(cudaMemcpy(c->dgmaps, maps.data(), sizeof(CUtensorMap) * maps.size(), cudaMemcpyHostToDevice));
@@ -2819,14 +2868,23 @@ int bs_gmres_begin(bs_ctx *c, int max_iterations, double tolerance, int basis, c
     return BS_OK;
 }
 
-int bs_gmres_run(bs_ctx *c, int max_cycles, void *stream, int64_t *kernels_out) {
-    if (!c) return fail(BS_EINVAL, "bs_gmres_run: null context");
-    if (!c->gm) return fail(BS_ESTATE, "bs_gmres_run: call bs_gmres_setup first");
-    if (int e = set_dev(c)) return e;
-    cudaStream_t st = (cudaStream_t)stream;
+namespace {
+// Restart cycles of the armed GMRES solves of every block (blk < 0) or of
+// block blk alone (launches cover only its CTAs; its cycle graph is
+// captured once per block).  The one-block form lets blocks share one
+// Krylov basis, solved one after another.
+int gmres_run(bs_ctx *c, int blk, int max_cycles, cudaStream_t st, int64_t *kernels_out) {
     const unsigned long long l0 = g_launches;
-    launch_sweep<OP_RESID>(c, st, -1);  // INIT: rhs assembly + r0 (inner_solvers.py:153-159)
-    if (!c->ggraph_exec) {
+    if (blk >= 0) {
+        // W may hold another block's values (shared workspace): off-region
+        // cells and row padding must read as exact zeros (see k_point)
+        const DBlock &B = c->hblocks[blk];
+        BS_CU(cudaMemsetAsync(B.W, 0, sizeof(double) * (size_t)B.vstride, st));
+    }
+    launch_sweep<OP_RESID>(c, st, -1, blk);  // INIT: rhs assembly + r0 (inner_solvers.py:153-159)
+    if (blk >= 0 && c->ggraph_blk.size() != (size_t)c->nblocks) c->ggraph_blk.assign(c->nblocks, nullptr);
+    cudaGraphExec_t &exec = blk < 0 ? c->ggraph_exec : c->ggraph_blk[blk];
+    if (!exec) {
         // one restart cycle as a CUDA graph: m Arnoldi steps (NORM, SPMV + h0j,
         // MGS passes, FINAL), FORM, true residual — 3m + m(m-1)/2 + 2 kernels
         // replayed per cycle without host launch overhead
@@ -2835,31 +2893,33 @@ int bs_gmres_run(bs_ctx *c, int max_cycles, void *stream, int64_t *kernels_out) 
         const unsigned long long g0 = g_launches;
         BS_CU(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
         for (int j = 0; j < c->gm; ++j) {  // one Arnoldi step per j; finished blocks skip
-            launch_point<PK_NORM>(c, cs, j, 0);
-            launch_gspmv(c, cs, j);
-            for (int i = 1; i <= j; ++i) launch_point<PK_MGS>(c, cs, j, i);
-            launch_point<PK_FINAL>(c, cs, j, 0);
+            launch_point<PK_NORM>(c, cs, j, 0, blk);
+            launch_gspmv(c, cs, j, blk);
+            for (int i = 1; i <= j; ++i) launch_point<PK_MGS>(c, cs, j, i, blk);
+            launch_point<PK_FINAL>(c, cs, j, 0, blk);
         }
-        launch_point<PK_FORM>(c, cs, 0, 0);
-        launch_sweep<OP_RESID>(c, cs, -1);  // true residual -> stop or restart
+        launch_point<PK_FORM>(c, cs, 0, 0, blk);
+        launch_sweep<OP_RESID>(c, cs, -1, blk);  // true residual -> stop or restart
         cudaGraph_t g = nullptr;
         BS_CU(cudaStreamEndCapture(cs, &g));
         c->gcycle_kernels = (long long)(g_launches - g0);
         g_launches = g0;  // captured, not launched
-        cudaGraphExec_t ex = nullptr;
-        BS_CU(cudaGraphInstantiate(&ex, g, 0));
-        c->ggraph = g;
-        c->ggraph_exec = ex;
+        BS_CU(cudaGraphInstantiate(&exec, g, 0));
+        BS_CU(cudaGraphDestroy(g));
     }
     int cycles = 0;
     for (;;) {
-        BS_CU(cudaGraphLaunch(c->ggraph_exec, st));
+        BS_CU(cudaGraphLaunch(exec, st));
         g_launches += c->gcycle_kernels;
         BS_CU(cudaGetLastError());
-        BS_CU(cudaMemcpyAsync(c->hpinned, c->dnactive, sizeof(int), cudaMemcpyDeviceToHost, st));
+        if (blk < 0)
+            BS_CU(cudaMemcpyAsync(c->hpinned, c->dnactive, sizeof(int), cudaMemcpyDeviceToHost, st));
+        else
+            BS_CU(cudaMemcpyAsync(c->hpinned, &c->dstates[blk].phase, sizeof(int), cudaMemcpyDeviceToHost, st));
         BS_CU(cudaStreamSynchronize(st));
         ++cycles;
-        if (c->hpinned[0] == 0) break;
+        const bool done = blk < 0 ? c->hpinned[0] == 0 : (c->hpinned[0] == PH_DONE || c->hpinned[0] == PH_IDLE);
+        if (done) break;
         if (max_cycles > 0 && cycles >= max_cycles) {
             if (kernels_out) *kernels_out = (int64_t)(g_launches - l0);
             return fail(BS_ESTATE, "bs_gmres_run: solves still active after max_cycles restart cycles");
@@ -2867,6 +2927,23 @@ int bs_gmres_run(bs_ctx *c, int max_cycles, void *stream, int64_t *kernels_out) 
     }
     if (kernels_out) *kernels_out = (int64_t)(g_launches - l0);
     return BS_OK;
+}
+
+}  // namespace
+
+int bs_gmres_run(bs_ctx *c, int max_cycles, void *stream, int64_t *kernels_out) {
+    if (!c) return fail(BS_EINVAL, "bs_gmres_run: null context");
+    if (!c->gm) return fail(BS_ESTATE, "bs_gmres_run: call bs_gmres_setup first");
+    if (int e = set_dev(c)) return e;
+    return gmres_run(c, -1, max_cycles, (cudaStream_t)stream, kernels_out);
+}
+
+int bs_gmres_run_block(bs_ctx *c, int block, int max_cycles, void *stream, int64_t *kernels_out) {
+    if (!c) return fail(BS_EINVAL, "bs_gmres_run_block: null context");
+    if (!c->gm) return fail(BS_ESTATE, "bs_gmres_run_block: call bs_gmres_setup first");
+    if (block < 0 || block >= c->nblocks) return fail(BS_EINVAL, "bs_gmres_run_block: block out of range");
+    if (int e = set_dev(c)) return e;
+    return gmres_run(c, block, max_cycles, (cudaStream_t)stream, kernels_out);
 }
 
 int bs_overlap_merge(bs_ctx *c, void *stream) {

@@ -265,22 +265,51 @@ class BlockEngine:
         _lib.check(self.lib.bs_flush(self.ctx, self.stream))
 
     # -- GMRES(m) workspace ----------------------------------------------
-    def gmres_setup(self, m: int) -> None:
-        """Allocate m Krylov vectors + the work vector per block (idempotent)."""
-        if getattr(self, "_gm", 0) == m:
+    def gmres_setup(self, m: int, shared=None) -> None:
+        """Allocate the GMRES(m) workspace: m Krylov vectors + the work vector.
+
+        Per block by default.  ``shared=True`` (or automatically, when the
+        per-block bases would take more than half of the free device memory)
+        allocates ONE basis for all blocks; ``gmres_run`` then solves the
+        blocks one after another (``bs_gmres_run_block``), which gives the
+        same numbers — a block's passes only touch its own state — and is what
+        lets config 5 at 1024^3 (eight 514^3 padded blocks, 31 vectors each)
+        run on one GPU.  Idempotent.
+        """
+        n_max = max(bb.x.numel() for bb in self.blocks)
+        if shared is None:
+            env = os.environ.get("BS_GMRES_SHARED")
+            if env is not None:
+                shared = env == "1"
+            else:
+                per_block = sum((m + 1) * bb.x.numel() * 8 for bb in self.blocks)
+                free, _ = torch.cuda.mem_get_info(self.device)
+                shared = self.nblocks > 1 and per_block > free // 2
+        shared = bool(shared) and self.nblocks > 1
+        if getattr(self, "_gm", 0) == m and getattr(self, "_gshared", False) == shared:
             return
+        self._gbufs = []  # release an earlier workspace before allocating the new one
         descs = (_lib.GmresDesc * self.nblocks)()
-        self._gbufs = []
-        for i, bb in enumerate(self.blocks):
-            n = bb.x.numel()
-            V = torch.zeros(m, n, dtype=torch.float64, device=self.device)
-            W = torch.zeros(n, dtype=torch.float64, device=self.device)
+        if shared:
+            V = torch.zeros(m, n_max, dtype=torch.float64, device=self.device)
+            W = torch.zeros(n_max, dtype=torch.float64, device=self.device)
             self._gbufs.append((V, W))
+        for i, bb in enumerate(self.blocks):
+            if not shared:
+                n = bb.x.numel()
+                V = torch.zeros(m, n, dtype=torch.float64, device=self.device)
+                W = torch.zeros(n, dtype=torch.float64, device=self.device)
+                self._gbufs.append((V, W))
             descs[i].V = V.data_ptr()
-            descs[i].vstride = n
+            descs[i].vstride = V.shape[1]
             descs[i].W = W.data_ptr()
         _lib.check(self.lib.bs_gmres_setup(self.ctx, int(m), descs))
         self._gm = m
+        self._gshared = shared
+
+    @property
+    def gmres_shared(self) -> bool:
+        return bool(getattr(self, "_gshared", False))
 
     def gmres_begin(self, max_iterations: int, tolerance: float, basis: str = "rhs", active=None) -> None:
         m = self._mask(active)
@@ -288,9 +317,16 @@ class BlockEngine:
                                            _lib.BASIS[basis], m[0] if m else None, self.stream))
 
     def gmres_run(self, max_cycles: int = 0) -> int:
+        """Run the armed GMRES solves; one block at a time with a shared basis."""
         n = ctypes.c_int64(0)
-        _lib.check(self.lib.bs_gmres_run(self.ctx, int(max_cycles), self.stream, ctypes.byref(n)))
-        return n.value
+        if not self.gmres_shared:
+            _lib.check(self.lib.bs_gmres_run(self.ctx, int(max_cycles), self.stream, ctypes.byref(n)))
+            return n.value
+        total = 0
+        for b in range(self.nblocks):
+            _lib.check(self.lib.bs_gmres_run_block(self.ctx, b, int(max_cycles), self.stream, ctypes.byref(n)))
+            total += n.value
+        return total
 
     def halo_pack(self, plan: np.ndarray) -> None:
         plan = np.ascontiguousarray(plan, dtype=np.int32)

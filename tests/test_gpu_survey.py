@@ -91,3 +91,21 @@ def test_degeneration_point_blocks_equal_point_jacobi():
     for _, snap in r.snapshots:
         x = (prob.rhs - O.csr_spmv(off, x)) / 6.0
         assert np.array_equal(snap, x)
+
+
+@pytest.mark.parametrize("overlap,block_grid", [(2, (2, 2, 2)), (0, (1, 1, 4))])
+def test_shared_gmres_basis_equals_per_block(monkeypatch, overlap, block_grid):
+    """One Krylov basis shared by all blocks, solved one block at a time
+    (bs_gmres_run_block: how config 5 at 1024^3 fits one GPU) gives the
+    per-block-basis run's numbers bit for bit."""
+    prob = bs.LinearProblem(bs.StencilOperator(24, 24, 24), O.seeded_rhs(24 ** 3, 1), bs.Grid3D(24, 24, 24))
+    cfg = dict(block_grid=block_grid, overlap=overlap, inner=bs.InnerSolverSpec("gmres", 30, 1e-3, 30), tol=1e-8,
+               tolerance_basis="initial", max_outer=40)
+    runs = []
+    for shared in ("0", "1"):
+        monkeypatch.setenv("BS_GMRES_SHARED", shared)
+        r = bs.outer_solve(prob, bs.OuterConfig(**cfg))
+        runs.append((r, [(row.inner_iterations, row.estimated_residual) for row in r.trace.rows]))
+    (a, ta), (b, tb) = runs
+    assert a.outer_iterations == b.outer_iterations and ta == tb
+    assert np.array_equal(a.solution, b.solution)
