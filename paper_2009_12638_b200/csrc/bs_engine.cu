@@ -141,6 +141,9 @@ __host__ __device__ constexpr bool op_has_b(int op) { return op == OP_RESID || o
 #ifndef BS_EASY
 #define BS_EASY 1  // interior planes of dilated regions take the box logic (sweep_tile)
 #endif
+#ifndef BS_REV_PASSES
+#define BS_REV_PASSES 1
+#endif
 #ifndef BS_REV_S2
 #define BS_REV_S2 1
 #endif
@@ -1517,7 +1520,20 @@ __global__ void __launch_bounds__(NTHR, 2) k_cg_persistent(const KParams P) {
 template <int PKK, bool BOX>
 __global__ void __launch_bounds__(NPT) k_point(const KParams P) {
     extern __shared__ __align__(1024) unsigned char smem[];
-    const int pc = P.pcta_base + (int)blockIdx.x;
+    // Chunk order: consecutive passes of an Arnoldi step alternate direction
+    // (MGS pass i reversed when i is odd, FINAL opposite to the last MGS
+    // pass, NORM opposite to the FINAL before it), so each pass starts on
+    // the chunks the previous one touched last (still in L2).  Partials are
+    // indexed by chunk, so the reduction order (and every result) is the
+    // same either way.
+    bool rev = false;
+    if (BS_REV_PASSES) {
+        // GSPMV (a z-ascending sweep) precedes MGS pass 1 and FINAL of step 0
+        if (PKK == PK_MGS) rev = P.launch_i & 1;
+        else if (PKK == PK_FINAL) rev = !(P.launch_j & 1);
+        else if (PKK == PK_NORM) rev = P.launch_j > 0 && !(P.launch_j & 1);
+    }
+    const int pc = P.pcta_base + (rev ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x);
     const int b = P.pcta_block[pc];
     const DBlock &B = P.blocks[b];
     const DState S = P.states[b];
