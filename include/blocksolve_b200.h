@@ -67,6 +67,10 @@ typedef struct bs_block_desc {
                                 where the face lies on the global boundary) */
     double *history;         /* device residual history, history_cap entries */
     int32_t history_cap;
+    int32_t remote;          /* 1: phantom of a block another process owns —
+                                geometry + r (its snapshot, peer-mapped) only;
+                                read by the overlap merge, never solved
+                                (multi-process overlap > 0, config 5) */
 } bs_block_desc;
 
 /* Per-block solver report, host side (InnerSolveReport, inner_solvers.py:60-67,
@@ -205,6 +209,15 @@ int bs_halo_pack(bs_ctx *ctx, int nplan, const int32_t *plan, void *stream);
  * x at shared points, and the average over covering blocks into the halo
  * cells (x cells outside the region, face planes). */
 int bs_overlap_merge(bs_ctx *ctx, void *stream);
+
+/* The two halves of bs_overlap_merge, for blocks spread over processes: every
+ * process snapshots its blocks, a host barrier orders the snapshots before
+ * any read, then the combine step reads the neighbours' snapshots — through
+ * the peer-mapped pointers of their phantom descriptors (remote = 1, r = the
+ * owner's snapshot opened with bs_ipc_open) — over NVLink, in the same
+ * order and with the same arithmetic as the single-process merge. */
+int bs_overlap_snapshot(bs_ctx *ctx, void *stream);
+int bs_overlap_combine(bs_ctx *ctx, void *stream);
 
 /* a7 (overlap > 0): local residual with owner-canonical values
  * (multisplit.py:372-396) = b - A x_gathered on each block's owned rows,

@@ -35,6 +35,7 @@ class BlockDesc(ctypes.Structure):
         ("ghost", ctypes.c_void_p * NDIR),
         ("history", ctypes.c_void_p),
         ("history_cap", ctypes.c_int32),
+        ("remote", ctypes.c_int32),
     ]
 
 
@@ -93,6 +94,8 @@ _SIGS = {
     "bs_gmres_setup": ([_P, _I, ctypes.POINTER(GmresDesc)], _I),
     "bs_gmres_begin": ([_P, _I, ctypes.c_double, _I, _P, _P], _I),
     "bs_gmres_run": ([_P, _I, _P, ctypes.POINTER(ctypes.c_int64)], _I),
+    "bs_overlap_snapshot": ([_P, _P], _I),
+    "bs_overlap_combine": ([_P, _P], _I),
     "bs_gmres_run_block": ([_P, _I, _I, _P, ctypes.POINTER(ctypes.c_int64)], _I),
     "bs_timing": ([_P, _I, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_longlong)], _I),
 }

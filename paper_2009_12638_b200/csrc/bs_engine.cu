@@ -177,6 +177,8 @@ struct DBlock {
     double *V;          // GMRES basis: V[j] = V + j * vstride (pitched padded box)
     long long vstride;
     double *W;          // GMRES work vector w
+    int remote;         // phantom of a block owned by another process: only its
+                        // snapshot (r, peer-mapped) is read, by the merge kernels
     int nnbr;           // neighbours, ascending ids (problems.py:343-349)
     int nbr[MAXNBR];
 };
@@ -1676,6 +1678,7 @@ __global__ void __launch_bounds__(NPT) k_point(const KParams P) {
 // r, W and V must stay zero off the region for the unmasked pointwise passes)
 __global__ void k_snapshot(const DBlock *__restrict__ blocks) {
     const DBlock &B = blocks[blockIdx.y];
+    if (B.remote) return;
     const long long n = (long long)B.pitch * B.pdim[1] * B.pdim[2];
     for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < n;
          c += (long long)gridDim.x * blockDim.x) {
@@ -1704,6 +1707,7 @@ __device__ __forceinline__ double merged_value(const DBlock *blocks, const DBloc
 
 __global__ void k_merge(const DBlock *__restrict__ blocks) {
     const DBlock &T = blocks[blockIdx.y];
+    if (T.remote) return;
     const long long n = (long long)T.pitch * T.pdim[1] * T.pdim[2];
     for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < n;
          c += (long long)gridDim.x * blockDim.x) {
@@ -1724,7 +1728,7 @@ __global__ void k_merge(const DBlock *__restrict__ blocks) {
 __global__ void k_merge_faces(const DBlock *__restrict__ blocks) {
     const DBlock &T = blocks[blockIdx.y];
     const int dir = blockIdx.z;
-    if (!T.ghost[dir]) return;
+    if (T.remote || !T.ghost[dir]) return;
     int nu, nv;
     if (dir == 0 || dir == 5) {
         nu = T.pdim[0];
@@ -1772,11 +1776,11 @@ __global__ void __launch_bounds__(NTHR, BS_MINBLOCKS) k_apply(const DBlock *__re
 }
 
 // Arm solves / residual sweeps.
-__global__ void k_arm(DState *states, const int *active, int nblocks, int phase, int max_its, double tol,
-                      int basis, int kind, int gm) {
+__global__ void k_arm(const DBlock *blocks, DState *states, const int *active, int nblocks, int phase, int max_its,
+                      double tol, int basis, int kind, int gm) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= nblocks) return;
-    if (active && !active[b]) return;
+    if ((active && !active[b]) || blocks[b].remote) return;  // phantoms stay idle
     DState &S = states[b];
     S.phase = phase;
     if (phase == PH_INIT) {
@@ -2426,6 +2430,21 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
         for (int q = 0; q < BS_NDIR; ++q) B.ghost[q] = d.ghost[q];
         B.hist = d.history;
         B.hist_cap = d.history_cap;
+        B.remote = d.remote != 0;
+        if (B.remote) {
+            // phantom: geometry + snapshot pointer only; no tiles, no chunks
+            if (!B.r || d.overlap == 0 || reinterpret_cast<uintptr_t>(B.r) % 16) {
+                delete c;
+                return fail(BS_EINVAL, "bs_ctx_create: remote block " + std::to_string(b) +
+                                           " needs overlap > 0 and a 16-byte aligned snapshot pointer");
+            }
+            for (int q = 0; q < BS_NDIR; ++q) B.ghost[q] = nullptr;
+            B.tiles_x = B.tiles_y = B.tiles_z = 0;
+            B.cz = 1;
+            B.cta_begin = B.cta_end = (int)cta_block.size();
+            c->hblocks.push_back(B);
+            continue;
+        }
         if (!B.x || !B.r || !B.p[0] || !B.p[1] || !B.b) {
             delete c;
             return fail(BS_EINVAL, "bs_ctx_create: null vector pointer for block " + std::to_string(b));
@@ -2480,7 +2499,8 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
         DBlock &B = c->hblocks[b];
         const long long n = (long long)B.pitch * B.pdim[1] * B.pdim[2];
         B.pcta_begin = (int)pcta_block.size();
-        for (long long t = 0; t < (n + PCHUNK - 1) / PCHUNK; ++t) pcta_block.push_back(b);
+        if (!B.remote)
+            for (long long t = 0; t < (n + PCHUNK - 1) / PCHUNK; ++t) pcta_block.push_back(b);
         B.pcta_end = (int)pcta_block.size();
     }
     c->npctas = (int)pcta_block.size();
@@ -2643,7 +2663,7 @@ int bs_cg_begin(bs_ctx *c, int max_iterations, double tolerance, int basis, cons
     if (int e = upload_active(c, active, st, &dact)) return e;
     if (c->jac_dirty) launch_flush(c, st);
     ++g_launches;
-    k_arm<<<(c->nblocks + 127) / 128, 128, 0, st>>>(c->dstates, dact, c->nblocks, PH_INIT, max_iterations,
+    k_arm<<<(c->nblocks + 127) / 128, 128, 0, st>>>(c->dblocks, c->dstates, dact, c->nblocks, PH_INIT, max_iterations,
                                                    tolerance, basis, KIND_CG, 0);
     BS_CU(cudaGetLastError());
     c->run_kind = KIND_CG;
@@ -2662,7 +2682,7 @@ int bs_jacobi_begin(bs_ctx *c, int max_iterations, double tolerance, int basis, 
     if (int e = upload_active(c, active, st, &dact)) return e;
     launch_flush(c, st);  // sweep 0 reads x itself: apply any pending CG update / Jacobi copy
     ++g_launches;
-    k_arm<<<(c->nblocks + 127) / 128, 128, 0, st>>>(c->dstates, dact, c->nblocks, PH_INIT, max_iterations,
+    k_arm<<<(c->nblocks + 127) / 128, 128, 0, st>>>(c->dblocks, c->dstates, dact, c->nblocks, PH_INIT, max_iterations,
                                                    tolerance, basis, KIND_JACOBI, 0);
     BS_CU(cudaGetLastError());
     c->run_kind = KIND_JACOBI;
@@ -2685,7 +2705,7 @@ int bs_cancel(bs_ctx *c, const int32_t *active, void *stream) {
     const int *dact = nullptr;
     if (int e = upload_active(c, active, st, &dact)) return e;
     ++g_launches;
-    k_arm<<<(c->nblocks + 127) / 128, 128, 0, st>>>(c->dstates, dact, c->nblocks, PH_DONE, 0, 0.0, 0, 0, 0);
+    k_arm<<<(c->nblocks + 127) / 128, 128, 0, st>>>(c->dblocks, c->dstates, dact, c->nblocks, PH_DONE, 0, 0.0, 0, 0, 0);
     BS_CU(cudaGetLastError());
     return BS_OK;
 }
@@ -2697,7 +2717,7 @@ int bs_residual(bs_ctx *c, const int32_t *active, void *stream) {
     const int *dact = nullptr;
     if (int e = upload_active(c, active, st, &dact)) return e;
     ++g_launches;
-    k_arm<<<(c->nblocks + 127) / 128, 128, 0, st>>>(c->dstates, dact, c->nblocks, PH_RESID, 0, 0.0, 0, 0, 0);
+    k_arm<<<(c->nblocks + 127) / 128, 128, 0, st>>>(c->dblocks, c->dstates, dact, c->nblocks, PH_RESID, 0, 0.0, 0, 0, 0);
     launch_sweep<OP_RESID>(c, st, -1);
     BS_CU(cudaGetLastError());
     return BS_OK;
@@ -2837,6 +2857,7 @@ int bs_gmres_setup(bs_ctx *c, int m, const bs_gmres_desc *descs) {
     for (int b = 0; b < c->nblocks; ++b) {
         DBlock &B = c->hblocks[b];
         const bs_gmres_desc &d = descs[b];
+        if (B.remote) continue;  // phantoms never solve
         if (!d.V || !d.W) return fail(BS_EINVAL, "bs_gmres_setup: null V or W");
         const long long n = (long long)B.pitch * B.pdim[1] * B.pdim[2];
         if (d.vstride < n || (d.vstride * 8) % 16) return fail(BS_EINVAL, "bs_gmres_setup: bad V stride");
@@ -2878,7 +2899,7 @@ int bs_gmres_begin(bs_ctx *c, int max_iterations, double tolerance, int basis, c
     if (int e = upload_active(c, active, st, &dact)) return e;
     if (c->jac_dirty) launch_flush(c, st);
     ++g_launches;
-    k_arm<<<(c->nblocks + 127) / 128, 128, 0, st>>>(c->dstates, dact, c->nblocks, PH_INIT, max_iterations,
+    k_arm<<<(c->nblocks + 127) / 128, 128, 0, st>>>(c->dblocks, c->dstates, dact, c->nblocks, PH_INIT, max_iterations,
                                                    tolerance, basis, KIND_GMRES, c->gm);
     BS_CU(cudaGetLastError());
     return BS_OK;
@@ -2964,10 +2985,25 @@ int bs_gmres_run_block(bs_ctx *c, int block, int max_cycles, void *stream, int64
 
 int bs_overlap_merge(bs_ctx *c, void *stream) {
     if (!c) return fail(BS_EINVAL, "bs_overlap_merge: null context");
+    if (int e = bs_overlap_snapshot(c, stream)) return e;
+    return bs_overlap_combine(c, stream);
+}
+
+int bs_overlap_snapshot(bs_ctx *c, void *stream) {
+    if (!c) return fail(BS_EINVAL, "bs_overlap_snapshot: null context");
     if (int e = set_dev(c)) return e;
     cudaStream_t st = (cudaStream_t)stream;
-    g_launches += 3;
+    g_launches += 1;
     k_snapshot<<<dim3(296, c->nblocks), 256, 0, st>>>(c->dblocks);
+    BS_CU(cudaGetLastError());
+    return BS_OK;
+}
+
+int bs_overlap_combine(bs_ctx *c, void *stream) {
+    if (!c) return fail(BS_EINVAL, "bs_overlap_combine: null context");
+    if (int e = set_dev(c)) return e;
+    cudaStream_t st = (cudaStream_t)stream;
+    g_launches += 2;
     k_merge<<<dim3(296, c->nblocks), 256, 0, st>>>(c->dblocks);
     k_merge_faces<<<dim3(64, c->nblocks, BS_NDIR), 256, 0, st>>>(c->dblocks);
     BS_CU(cudaGetLastError());
@@ -2979,7 +3015,7 @@ int bs_owner_residual(bs_ctx *c, void *stream) {
     if (int e = set_dev(c)) return e;
     cudaStream_t st = (cudaStream_t)stream;
     ++g_launches;
-    k_arm<<<(c->nblocks + 127) / 128, 128, 0, st>>>(c->dstates, nullptr, c->nblocks, PH_OWNRES, 0, 0.0, 0, 0, 0);
+    k_arm<<<(c->nblocks + 127) / 128, 128, 0, st>>>(c->dblocks, c->dstates, nullptr, c->nblocks, PH_OWNRES, 0, 0.0, 0, 0, 0);
     launch_point<PK_OWNRES>(c, st, 0, 0);
     BS_CU(cudaGetLastError());
     return BS_OK;

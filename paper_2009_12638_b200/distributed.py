@@ -18,6 +18,15 @@ reference (comm.py:332-365 and 422-453):
   ``comm.py:442-445``; iteration counts are therefore identical at 1/2/4/8
   GPUs (the fixed-order per-block reductions do not depend on the GPU count).
 
+Overlap > 0 (config 5: 2x2x2 cubes with a 2-plane overlap, one per GPU):
+every rank's engine holds all blocks — its own, plus *phantoms* of the others
+whose only buffer is the owner's snapshot vector, opened once through CUDA
+IPC.  Per sweep: flush, snapshot, host barrier, then the merge and the
+owner-canonical residual read the neighbours' snapshots straight from their
+GPUs' memory (NVLink loads inside the merge kernels — no packing, no staging
+copy, the reference's index-list payloads are the kernels' reads), and the
+scalar all-reduce is the barrier before the next inner solve overwrites them.
+
 ``engine_factory`` lets CPU tests (gloo, world_size 2) drive the same host
 logic with an oracle-backed stand-in engine; production uses ``BlockEngine``
 on ``cuda:LOCAL_RANK``.
@@ -167,8 +176,8 @@ def outer_solve_distributed(problem: LinearProblem, config: OuterConfig, group=N
     dist = torch.distributed
     if not dist.is_initialized():
         raise ConfigurationError("distributed: torch.distributed is not initialised")
-    if config.mode != "sync" or config.overlap != 0:
-        raise ConfigurationError("distributed: sharded runs are sync with overlap 0")
+    if config.mode != "sync":
+        raise ConfigurationError("distributed: sharded runs are synchronous")
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     grid = problem.grid
     nx, ny, nz = grid.shape
@@ -186,6 +195,10 @@ def outer_solve_distributed(problem: LinearProblem, config: OuterConfig, group=N
     for box in decomp.owned:
         d = float(np.linalg.norm(b3[box.lo[2]:box.hi[2], box.lo[1]:box.hi[1], box.lo[0]:box.hi[0]].ravel()))
         dens.append(d if d != 0.0 else (bnorm if bnorm != 0.0 else 1.0))
+    if config.overlap != 0:
+        if engine_factory is not None:
+            raise ConfigurationError("distributed: overlap > 0 runs on the device engine")
+        return _solve_overlap(config, group, grid, decomp, local_ids, owner, rank, world, b3, bnorm, dens)
     factory = engine_factory or _default_factory
     eng = factory(grid.shape, [decomp.owned[g] for g in local_ids], config.overlap, local_ids)
     eng.load_host("b", b3)
@@ -211,6 +224,83 @@ def outer_solve_distributed(problem: LinearProblem, config: OuterConfig, group=N
     finally:
         exchange.close()
         eng.close()
+    rows = [TraceRow(k, t, est, tr, inner, 0) for k, t, est, tr, inner in trace]
+    if rows and rows[-1].true_residual is None:
+        rows[-1].true_residual = final_true
+    return SolveResult(solution=sol.reshape(-1).cpu().numpy(), trace=ResidualTrace(rows), converged=converged,
+                       outer_iterations=len(rows), final_true_residual=final_true,
+                       inner_iterations_per_block=per_block, wall_seconds=time.perf_counter() - t_start)
+
+
+def _open_snapshots(eng, group, world, opened):
+    """resolve_remote for the phantom engine: export every local block's
+    snapshot buffer (its r) as a CUDA IPC handle, gather all ranks' handles,
+    open the ones of the phantoms (once per solve)."""
+    import ctypes
+
+    lib = _lib.load()
+    mine = {}
+    for i in eng.local_indices:
+        handle = (ctypes.c_ubyte * 64)()
+        off = ctypes.c_uint64(0)
+        _lib.check(lib.bs_ipc_export(ctypes.c_void_p(eng.blocks[i].r.data_ptr()), handle, ctypes.byref(off)))
+        mine[i] = (bytes(handle), off.value)
+    gathered = [None] * world
+    torch.distributed.all_gather_object(gathered, mine, group=group)
+    table = {k: v for part in gathered for k, v in part.items()}
+    ptrs = {}
+    for i in sorted(eng.remote):
+        handle, off = table[i]
+        ptr = ctypes.c_void_p()
+        _lib.check(lib.bs_ipc_open((ctypes.c_ubyte * 64).from_buffer_copy(handle), off, ctypes.byref(ptr)))
+        opened.append(ptr.value - off)
+        ptrs[i] = ptr.value
+    return ptrs
+
+
+def _solve_overlap(config, group, grid, decomp, local_ids, owner, rank, world, b3, bnorm, dens):
+    """Sharded sync sweep with overlap > 0 over peer-mapped snapshots (module doc)."""
+    dist = torch.distributed
+    nx, ny, nz = grid.shape
+    nb = decomp.num_blocks
+    dev = require_cuda(f"cuda:{int(os.environ.get('LOCAL_RANK', torch.cuda.current_device()))}")
+    opened = []
+    remote = [g for g in range(nb) if owner[g] != rank]
+    with torch.cuda.device(dev):
+        eng = BlockEngine(grid.shape, decomp.owned, config.overlap, dev, history_cap=1, remote=remote,
+                          resolve_remote=lambda e: _open_snapshots(e, group, world, opened))
+        host_comm = dist.get_backend(group) == "gloo"
+        comm_dev = torch.device("cpu") if host_comm else dev
+
+        def merge():
+            eng.overlap_snapshot()
+            eng.synchronize()
+            dist.barrier(group=group)  # every snapshot of this sweep is complete before any read
+            eng.overlap_combine()
+
+        def allreduce_rows(table: np.ndarray) -> np.ndarray:
+            t = torch.from_numpy(table).to(comm_dev)
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)  # also: nobody still reads a snapshot
+            return t.cpu().numpy()
+
+        t_start = time.perf_counter()
+        try:
+            eng.load_host("b", b3)
+            trace, per_block, converged, final_true = run_sync(
+                eng, config, dens, bnorm, nb, local_ids, lambda: None, allreduce_rows, t_start,
+                merge=merge, eng_index=local_ids)
+            eng.flush()
+            sol = torch.zeros(nz, ny, nx, dtype=torch.float64, device=dev)
+            eng.gather_owned(sol)
+            sol = sol.to(comm_dev)
+            dist.all_reduce(sol, op=dist.ReduceOp.SUM, group=group)  # disjoint owned boxes: exact
+        finally:
+            eng.synchronize()
+            dist.barrier(group=group)  # no peer reads our snapshots any more
+            eng.close()
+            lib = _lib.load()
+            for base in opened:
+                lib.bs_ipc_close(base)
     rows = [TraceRow(k, t, est, tr, inner, 0) for k, t, est, tr, inner in trace]
     if rows and rows[-1].true_residual is None:
         rows[-1].true_residual = final_true

@@ -89,18 +89,35 @@ class BlockEngine:
     """All blocks of one decomposition that live on one device."""
 
     def __init__(self, grid_shape, owned: list, overlap: int, device=None,
-                 history_cap: int = 0, z_chunk: int = 0, block_ids=None):
+                 history_cap: int = 0, z_chunk: int = 0, block_ids=None, remote=None, resolve_remote=None):
+        """``remote``: indices of ``owned`` that another process owns (overlap
+        > 0 only).  They become phantom descriptors — geometry plus the
+        owner's snapshot buffer, peer-mapped — that the overlap merge reads;
+        ``resolve_remote(engine)`` is called once the local buffers exist and
+        returns {index: device pointer of that block's snapshot}."""
         self.lib = _lib.load()
         self.device = require_cuda(device)
         self.grid_shape = tuple(int(v) for v in grid_shape)
         self.overlap = int(overlap)
         self.block_ids = list(block_ids) if block_ids is not None else list(range(len(owned)))
+        self.remote = set(int(i) for i in (remote or ()))
+        if self.remote and self.overlap == 0:
+            raise DeviceError("phantom blocks are only used by the overlap > 0 merge")
         self.blocks: list = []
         nx, ny, nz = self.grid_shape
         descs = (_lib.BlockDesc * len(owned))()
         opts = dict(dtype=torch.float64, device=self.device)
         cap = max(1, int(history_cap))
         for i, box in enumerate(owned):
+            d = descs[i]
+            d.global_dims[:] = [nx, ny, nz]
+            d.owned_lo[:] = list(box.lo)
+            d.owned_hi[:] = list(box.hi)
+            d.overlap = overlap
+            if i in self.remote:
+                self.blocks.append(None)
+                d.remote = 1
+                continue
             lo = tuple(max(0, box.lo[d] - overlap) for d in range(3))
             hi = tuple(min(self.grid_shape[d], box.hi[d] + overlap) for d in range(3))
             pad = Box(lo, hi)
@@ -118,17 +135,16 @@ class BlockEngine:
                 p0=torch.zeros(n, **opts), p1=torch.zeros(n, **opts), b=torch.zeros(n, **opts),
                 ghost=ghosts, history=torch.zeros(cap, **opts))
             self.blocks.append(bb)
-            d = descs[i]
-            d.global_dims[:] = [nx, ny, nz]
-            d.owned_lo[:] = list(box.lo)
-            d.owned_hi[:] = list(box.hi)
-            d.overlap = overlap
             d.x, d.r, d.p0, d.p1, d.b = (bb.x.data_ptr(), bb.r.data_ptr(), bb.p0.data_ptr(),
                                          bb.p1.data_ptr(), bb.b.data_ptr())
             for q in range(_lib.NDIR):
                 d.ghost[q] = ghosts[q].data_ptr() if ghosts[q] is not None else None
             d.history = bb.history.data_ptr()
             d.history_cap = cap
+        if self.remote:
+            ptrs = resolve_remote(self)
+            for i in self.remote:
+                descs[i].r = int(ptrs[i])
         self._descs = descs
         if not z_chunk:
             z_chunk = int(os.environ.get("BS_ZCHUNK", "0"))
@@ -139,7 +155,7 @@ class BlockEngine:
         self.ctx = ctx
         self.nblocks = len(owned)
         for i, bb in enumerate(self.blocks):
-            if self.lib.bs_block_pitch(ctx, i) != bb.pitch:
+            if bb is not None and self.lib.bs_block_pitch(ctx, i) != bb.pitch:
                 raise DeviceError("row pitch mismatch between host and engine")
         self._reports = (_lib.BlockReport * self.nblocks)()
 
@@ -159,7 +175,13 @@ class BlockEngine:
     def stream(self) -> ctypes.c_void_p:
         return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
 
+    @property
+    def local_indices(self) -> list:
+        return [i for i, bb in enumerate(self.blocks) if bb is not None]
+
     def _mask(self, active):
+        if active is None and self.remote:
+            active = [bb is not None for bb in self.blocks]  # phantoms are never armed
         if active is None:
             return None
         arr = (ctypes.c_int32 * self.nblocks)(*[1 if a else 0 for a in active])
@@ -173,12 +195,16 @@ class BlockEngine:
     def load_global(self, name: str, g3: "torch.Tensor") -> None:
         """Scatter a global (nz, ny, nx) device tensor into every block's padded box."""
         for bb in self.blocks:
+            if bb is None:
+                continue
             (x0, y0, z0), (x1, y1, z1) = bb.padded.lo, bb.padded.hi
             bb.view3(getattr(bb, name)).copy_(g3[z0:z1, y0:y1, x0:x1])
 
     def load_host(self, name: str, g3: np.ndarray) -> None:
         """Scatter a global (nz, ny, nx) host array into every block's padded box."""
         for bb in self.blocks:
+            if bb is None:
+                continue
             (x0, y0, z0), (x1, y1, z1) = bb.padded.lo, bb.padded.hi
             src = torch.from_numpy(np.ascontiguousarray(g3[z0:z1, y0:y1, x0:x1])).to(self.device)
             bb.view3(getattr(bb, name)).copy_(src)
@@ -219,11 +245,15 @@ class BlockEngine:
     def gather_owned(self, out3: "torch.Tensor", name: str = "x") -> None:
         """Write every block's owned values of ``name`` into a global (nz, ny, nx) tensor."""
         for bb in self.blocks:
+            if bb is None:
+                continue
             (x0, y0, z0), (x1, y1, z1) = bb.owned.lo, bb.owned.hi
             out3[z0:z1, y0:y1, x0:x1].copy_(bb.view3(getattr(bb, name))[bb.owned_slices()])
 
     def zero(self, *names) -> None:
         for bb in self.blocks:
+            if bb is None:
+                continue
             for name in names:
                 getattr(bb, name).zero_()
             if "ghost" in names:
@@ -276,16 +306,17 @@ class BlockEngine:
         lets config 5 at 1024^3 (eight 514^3 padded blocks, 31 vectors each)
         run on one GPU.  Idempotent.
         """
-        n_max = max(bb.x.numel() for bb in self.blocks)
+        live = [bb for bb in self.blocks if bb is not None]
+        n_max = max(bb.x.numel() for bb in live)
         if shared is None:
             env = os.environ.get("BS_GMRES_SHARED")
             if env is not None:
                 shared = env == "1"
             else:
-                per_block = sum((m + 1) * bb.x.numel() * 8 for bb in self.blocks)
+                per_block = sum((m + 1) * bb.x.numel() * 8 for bb in live)
                 free, _ = torch.cuda.mem_get_info(self.device)
-                shared = self.nblocks > 1 and per_block > free // 2
-        shared = bool(shared) and self.nblocks > 1
+                shared = len(live) > 1 and per_block > free // 2
+        shared = bool(shared) and len(live) > 1
         if getattr(self, "_gm", 0) == m and getattr(self, "_gshared", False) == shared:
             return
         self._gbufs = []  # release an earlier workspace before allocating the new one
@@ -295,6 +326,8 @@ class BlockEngine:
             W = torch.zeros(n_max, dtype=torch.float64, device=self.device)
             self._gbufs.append((V, W))
         for i, bb in enumerate(self.blocks):
+            if bb is None:  # phantom: no workspace (the C side skips it)
+                continue
             if not shared:
                 n = bb.x.numel()
                 V = torch.zeros(m, n, dtype=torch.float64, device=self.device)
@@ -323,7 +356,7 @@ class BlockEngine:
             _lib.check(self.lib.bs_gmres_run(self.ctx, int(max_cycles), self.stream, ctypes.byref(n)))
             return n.value
         total = 0
-        for b in range(self.nblocks):
+        for b in self.local_indices:
             _lib.check(self.lib.bs_gmres_run_block(self.ctx, b, int(max_cycles), self.stream, ctypes.byref(n)))
             total += n.value
         return total
@@ -337,6 +370,12 @@ class BlockEngine:
 
     def overlap_merge(self) -> None:
         _lib.check(self.lib.bs_overlap_merge(self.ctx, self.stream))
+
+    def overlap_snapshot(self) -> None:
+        _lib.check(self.lib.bs_overlap_snapshot(self.ctx, self.stream))
+
+    def overlap_combine(self) -> None:
+        _lib.check(self.lib.bs_overlap_combine(self.ctx, self.stream))
 
     def owner_residual(self) -> None:
         _lib.check(self.lib.bs_owner_residual(self.ctx, self.stream))

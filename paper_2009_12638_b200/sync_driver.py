@@ -34,7 +34,7 @@ def make_inner(eng, spec, config):
         # _make_inner_solver (multisplit.py:532-536): one cycle of the configured
         # length unless a restart is given; gmres_solve caps it at n (162)
         restart = spec.restart if spec.restart is not None else spec.max_iterations
-        restart = min(restart, min(bb.padded.size for bb in eng.blocks))
+        restart = min(restart, min(bb.padded.size for bb in eng.blocks if bb is not None))
         eng.gmres_setup(restart)
 
         def arm():
@@ -54,16 +54,21 @@ def make_inner(eng, spec, config):
 
 
 def run_sync(eng, config, dens, bnorm, nblocks, local_ids, exchange, allreduce_rows, t_start,
-             on_sweep=None):
+             on_sweep=None, merge=None, eng_index=None):
     """Run sweeps until the reference's termination rule fires.
 
     ``exchange()`` performs the overlap-0 halo exchange; ``allreduce_rows(a)``
     sums an (nblocks, 4) array whose rows only the owning rank fills (exact:
-    every entry is nonzero on one rank).  Returns (rows, per_block, converged,
+    every entry is nonzero on one rank).  ``merge()`` performs the overlap > 0
+    merge (default: ``eng.overlap_merge``); ``eng_index[li]`` is the engine
+    slot of ``local_ids[li]`` (default: li).  Returns (rows, per_block, converged,
     final_true) with rows = (k, time, estimate, true_or_None, inner_total).
     """
     spec = config.inner
     overlap = eng.overlap
+    if merge is None and overlap:
+        merge = eng.overlap_merge
+    eng_index = list(eng_index) if eng_index is not None else list(range(len(local_ids)))
     arm, solve = make_inner(eng, spec, config)
     arm()
     solve()  # sweep 0: rhs = b (zero halos), x0 = 0
@@ -79,13 +84,14 @@ def run_sync(eng, config, dens, bnorm, nblocks, local_ids, exchange, allreduce_r
             eng.sweep_resid()
         else:
             eng.flush()
-            eng.overlap_merge()
+            merge()
             eng.owner_residual()
         reps = eng.reports()
         table = np.zeros((nblocks, 4))
         for li, gid in enumerate(local_ids):
-            table[gid] = (its_reps[li].iterations_used, 1.0 if int(its_reps[li].stop_reason) == 3 else 0.0,
-                          reps[li].r_owned_sq, reps[li].rglob_owned_sq)
+            e = eng_index[li]
+            table[gid] = (its_reps[e].iterations_used, 1.0 if int(its_reps[e].stop_reason) == 3 else 0.0,
+                          reps[e].r_owned_sq, reps[e].rglob_owned_sq)
         table = allreduce_rows(table)
         broken = np.nonzero(table[:, 1])[0]
         if broken.size:

@@ -69,3 +69,57 @@ def test_p2p_ipc_halo_puts_two_processes_equal_single_process():
             assert np.array_equal(got["counts"], np.asarray(ref.inner_iterations_per_block))
             assert np.array_equal(got["est"], np.asarray([r.estimated_residual for r in ref.trace.rows]))
             assert np.array_equal(got["solution"], ref.solution)
+
+
+def _cfg5(bs):
+    n = 24
+    prob = bs.build_laplace_3d(bs.Grid3D(n, n, n, bs.DirichletBoundary({"z_lo": 1.0})))
+    cfg = bs.OuterConfig(block_grid=(2, 2, 2), overlap=2, inner=bs.InnerSolverSpec("gmres", 30, 1e-3, 30),
+                         tol=1e-8, tolerance_basis="initial", max_outer=60)
+    return prob, cfg
+
+
+def _worker_overlap(rank, world, port, out_dir):
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    os.environ["LOCAL_RANK"] = "0"
+    import torch
+
+    import paper_2009_12638_b200 as bs
+    from paper_2009_12638_b200.distributed import outer_solve_distributed
+
+    torch.cuda.set_device(0)
+    torch.distributed.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                                         world_size=world)
+    prob, cfg = _cfg5(bs)
+    res = outer_solve_distributed(prob, cfg)
+    np.savez(os.path.join(out_dir, f"ov_{rank}.npz"), solution=res.solution,
+             counts=np.asarray(res.inner_iterations_per_block),
+             est=np.asarray([r.estimated_residual for r in res.trace.rows]),
+             true=np.asarray([res.final_true_residual]))
+    torch.distributed.destroy_process_group()
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("world", [2, 4])
+def test_overlap_merge_over_peer_snapshots_equals_single_process(world):
+    """Config-5 shape (2x2x2 cubes, overlap 2, GMRES(30)) split over processes:
+    each engine holds phantoms of the other ranks' blocks whose snapshot
+    buffers are IPC-mapped; the merge and owner residual read them in place.
+    Bitwise equal to the single-process solve."""
+    import torch.multiprocessing as mp
+
+    import paper_2009_12638_b200 as bs
+
+    with tempfile.TemporaryDirectory() as tmp:
+        mp.spawn(_worker_overlap, args=(world, _port(), tmp), nprocs=world, join=True)
+        prob, cfg = _cfg5(bs)
+        ref = bs.outer_solve(prob, cfg)
+        for rank in range(world):
+            got = np.load(os.path.join(tmp, f"ov_{rank}.npz"))
+            assert np.array_equal(got["counts"], np.asarray(ref.inner_iterations_per_block))
+            assert np.array_equal(got["est"], np.asarray([r.estimated_residual for r in ref.trace.rows]))
+            assert np.array_equal(got["solution"], ref.solution)
+            assert got["true"][0] == ref.final_true_residual
