@@ -44,7 +44,7 @@ import numpy as np
 
 from . import _lib
 from .engine import BlockEngine, box_halo_plan, launch_bound, torch
-from .errors import SolverBreakdownError
+from .errors import ConfigurationError, SolverBreakdownError
 
 RING_SLOTS_MAX = 8  # without injected delays deeper rings only hold stale planes
 NO_FILTER = (1 << 63) - 1  # receiver_k that accepts every published slot
@@ -106,27 +106,100 @@ class _Mailbox:
         self.stage = torch.zeros(plane, dtype=torch.float64, device=device)
         self.torn = torch.zeros(1, dtype=torch.int32, device=device)
         self.pool = None  # SendPool under injected latency
+        # where the sender writes: this process's tensors, or (sender in
+        # another process) the receiver's, opened through CUDA IPC
+        self.ring_ptr, self.seqs_ptr, self.deliver_ptr = (self.ring.data_ptr(), self.seqs.data_ptr(),
+                                                          self.deliver.data_ptr())
+
+
+class _RemoteMailbox:
+    """Sender-side view of a mailbox owned by a receiver in another process:
+    the ring, sequence and delivery words are the receiver's device memory,
+    peer-mapped (one-sided NVLink puts)."""
+
+    def __init__(self, dst: int, ghost_dir: int, src: int, slots: int, ptrs):
+        self.dst, self.ghost_dir, self.src = dst, ghost_dir, src
+        self.post_dir = 5 - ghost_dir
+        self.R = slots
+        self.ring_ptr, self.seqs_ptr, self.deliver_ptr = ptrs
+        self.pool = None
+
+
+class _Rendezvous:
+    """Barrier of every block of the solve: the block threads of this process
+    (threading.Barrier), and across processes one gloo barrier taken by the
+    thread the local barrier elects."""
+
+    def __init__(self, n_local: int, group=None, multi: bool = False):
+        # a generous timeout: a block reaches the round at most one sweep
+        # after the request, but a lost peer must not hang the node
+        self.local = threading.Barrier(n_local, timeout=600.0)
+        self.group = group
+        self.multi = multi
+
+    def wait(self):
+        if self.local.wait() == 0 and self.multi:
+            try:
+                torch.distributed.barrier(group=self.group)
+            except Exception:
+                self.local.abort()
+                raise
+        self.local.wait()
+
+    def abort(self):
+        self.local.abort()
 
 
 class _Board:
-    """Host-side residual board + confirmation rendezvous (the fabric's role)."""
+    """Host-side residual board + confirmation rendezvous (the fabric's role).
 
-    def __init__(self, nb: int):
+    ``store`` holds the cross-block words: float64 local_sq[nb],
+    confirm_sq[nb] and four flags (confirm requested, stop, converged,
+    failed).  One process: a private array.  Several processes (one per
+    GPU, same node): a POSIX shared-memory segment every rank maps, written
+    one-sidedly (aligned 8-byte stores) — the board is an estimate by
+    design (comm.py:455-527); the confirmation round's barrier orders it."""
+
+    FLAGS = ("confirm_requested", "stop", "converged", "failed")
+
+    def __init__(self, nb: int, n_local: int = None, store=None, group=None, multi: bool = False):
         self.nb = nb
         self.lock = threading.Lock()
-        self.local_sq = [math.inf] * nb
+        self.store = store if store is not None else np.zeros(2 * nb + 4)
+        if store is None:
+            self.local_sq[:] = math.inf
         self.progress = [0] * nb        # sweep each block has begun
         self.pub = [[] for _ in range(nb)]  # delayed model: (deliver_at, value) per publisher
-        self.confirm_requested = False
-        self.stop = False
-        self.converged = False
         self.error: BaseException | None = None
-        self.barrier = threading.Barrier(nb)
-        self.confirm_sq = [0.0] * nb
+        self.barrier = _Rendezvous(nb if n_local is None else n_local, group, multi)
+
+    @property
+    def local_sq(self):
+        return self.store[:self.nb]
+
+    @property
+    def confirm_sq(self):
+        return self.store[self.nb:2 * self.nb]
+
+    def _flag(i):
+        def get(self):
+            return bool(self.store[2 * self.nb + i] != 0.0)
+
+        def put(self, v):
+            self.store[2 * self.nb + i] = 1.0 if v else 0.0
+        return property(get, put)
+
+    confirm_requested = _flag(0)
+    stop = _flag(1)
+    converged = _flag(2)
+    failed = _flag(3)
+    del _flag
 
     def estimate(self) -> float:
         with self.lock:
-            total = float(sum(self.local_sq[w] for w in range(self.nb)))  # block order (comm.py:443-445)
+            total = 0.0
+            for w in range(self.nb):  # block order (comm.py:443-445)
+                total += float(self.local_sq[w])
         return math.sqrt(total) if math.isfinite(total) else math.inf
 
     def estimate_delayed(self, reader: int, k: int) -> float:
@@ -144,11 +217,20 @@ class _Board:
         return math.sqrt(total) if math.isfinite(total) else math.inf
 
 
-def outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, spec):
-    """Run the asynchronous two-stage solve; returns the pieces of a SolveResult."""
+def outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, spec, local=None, group=None,
+                      distributed=False):
+    """Run the asynchronous two-stage solve; returns the pieces of a SolveResult.
+
+    ``distributed`` (one process per GPU; ``group`` a gloo group, None = the
+    default one): this process drives the blocks in ``local``; mailboxes of cross-process channels live in the
+    receiver's process and the sender puts into them through CUDA IPC; the
+    board is a shared-memory segment and the confirmation round adds a gloo
+    barrier (``group``).  Every rank returns the full solution and records."""
     grid = problem.grid
     nx, ny, nz = grid.shape
     nb = decomp.num_blocks
+    local = list(range(nb)) if local is None else list(local)
+    multi = bool(distributed)
     every = max(1, int(getattr(config, "residual_check_every", 1)))
     delay = config.delay
     delayed = delay.kind != "none"
@@ -157,25 +239,39 @@ def outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, spec):
     slots = max(1, int(config.buffer_slots) if delayed else min(int(config.buffer_slots), RING_SLOTS_MAX))
     rng = np.random.default_rng(delay.seed)
     rng_lock = threading.Lock()
-    engines, streams = [], []
+    if multi and delayed:
+        raise ConfigurationError("delay: injected latency is a single-process experiment (one GPU)")
+    engines, streams = {}, {}
+    opened, shm = [], None
     with torch.cuda.device(dev):
-        for i in range(nb):
+        for i in local:
             eng = BlockEngine(grid.shape, [decomp.owned[i]], 0, dev, history_cap=1)
             eng.load_global("b", b_dev)
-            engines.append(eng)
-            streams.append(torch.cuda.Stream(dev))
+            engines[i] = eng
+            streams[i] = torch.cuda.Stream(dev)
         torch.cuda.synchronize(dev)
         plan = box_halo_plan(decomp.owned, decomp.block_grid)
-        incoming = [[] for _ in range(nb)]
-        outgoing = [[] for _ in range(nb)]
+        incoming = {i: [] for i in local}
+        outgoing = {i: [] for i in local}
         for dst, gdir, src in plan.tolist():
+            if dst not in engines:
+                continue
             plane = engines[dst].blocks[0].ghost[gdir].numel()
             mb = _Mailbox(dst, gdir, src, plane, slots, dev)
             if delayed:
                 mb.pool = SendPool(slots, delay)
             incoming[dst].append(mb)
-            outgoing[src].append(mb)
-    board = _Board(nb)
+            if src in engines:
+                outgoing[src].append(mb)
+        if multi:
+            for mb in _open_remote_mailboxes(plan, incoming, engines, slots, group, opened):
+                outgoing[mb.src].append(mb)
+            for lst in outgoing.values():  # post order as in one process: plan order
+                lst.sort(key=lambda m: (m.dst, m.ghost_dir))
+            store, shm = _shared_store(nb, group)
+            board = _Board(nb, len(local), store, group, multi=True)
+        else:
+            board = _Board(nb)
     records = [[] for _ in range(nb)]
     t0 = time.perf_counter()
 
@@ -236,6 +332,7 @@ def outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, spec):
         except BaseException as exc:  # propagate after join; release the others
             board.error = exc
             board.stop = True
+            board.failed = True
             board.barrier.abort()
 
     def _draw() -> int:
@@ -250,8 +347,8 @@ def outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, spec):
     def _post(eng, mb, k: int, st) -> None:
         if not delayed:
             slot = k % mb.R
-            _lib.check(eng.lib.bs_async_post_slot(eng.ctx, 0, mb.post_dir, mb.ring.data_ptr(), mb.seqs.data_ptr(),
-                                                  mb.deliver.data_ptr(), slot, 2 * k, 0, st))
+            _lib.check(eng.lib.bs_async_post_slot(eng.ctx, 0, mb.post_dir, mb.ring_ptr, mb.seqs_ptr,
+                                                  mb.deliver_ptr, slot, 2 * k, 0, st))
             return
         with board.lock:
             reached = board.progress[mb.dst]  # the receiver's begun iteration (comm.py:383)
@@ -260,8 +357,8 @@ def outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, spec):
         if got is None:
             return  # exhausted pool: skip, never block (comm.py:392-393)
         slot, deliver_at = got
-        _lib.check(eng.lib.bs_async_post_slot(eng.ctx, 0, mb.post_dir, mb.ring.data_ptr(), mb.seqs.data_ptr(),
-                                              mb.deliver.data_ptr(), slot, 2 * k, deliver_at, st))
+        _lib.check(eng.lib.bs_async_post_slot(eng.ctx, 0, mb.post_dir, mb.ring_ptr, mb.seqs_ptr,
+                                              mb.deliver_ptr, slot, 2 * k, deliver_at, st))
 
     def _confirm(b: int, k: int) -> bool:
         """Confirmation round (comm.py:542-598): flush current payloads, recompute
@@ -274,8 +371,8 @@ def outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, spec):
             if board.stop and not board.confirm_requested:
                 return True
             for mb in outgoing[b]:  # the reserved slot R: a synchronous, undelayed flush
-                _lib.check(eng.lib.bs_async_post_slot(eng.ctx, 0, mb.post_dir, mb.ring.data_ptr(),
-                                                      mb.seqs.data_ptr(), mb.deliver.data_ptr(), mb.R, 2 * k + 1,
+                _lib.check(eng.lib.bs_async_post_slot(eng.ctx, 0, mb.post_dir, mb.ring_ptr,
+                                                      mb.seqs_ptr, mb.deliver_ptr, mb.R, 2 * k + 1,
                                                       0, st))
             torch.cuda.current_stream(dev).synchronize()
             board.barrier.wait()
@@ -303,25 +400,115 @@ def outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, spec):
         except threading.BrokenBarrierError:
             return True
 
-    threads = [threading.Thread(target=worker, args=(b,), name=f"block-{b}") for b in range(nb)]
+    threads = [threading.Thread(target=worker, args=(b,), name=f"block-{b}") for b in local]
     for t in threads:
         t.start()
     for t in threads:
         t.join()
     if board.error is not None:
-        for eng in engines:
+        for eng in engines.values():
             eng.close()
+        _close_fabric(opened, shm, multi)
         raise board.error
     with torch.cuda.device(dev):
-        sol = torch.empty(nz, ny, nx, dtype=torch.float64, device=dev)
-        for eng in engines:
+        sol = torch.zeros(nz, ny, nx, dtype=torch.float64, device=dev)
+        for eng in engines.values():
             eng.flush()
             eng.gather_owned(sol)
         torch.cuda.synchronize(dev)
-        torn = int(sum(int(mb.torn.item()) for lst in incoming for mb in lst))
-        skipped = int(sum(mb.pool.skipped for lst in incoming for mb in lst if mb.pool is not None))
-        for eng in engines:
+        torn = int(sum(int(mb.torn.item()) for lst in incoming.values() for mb in lst))
+        skipped = int(sum(mb.pool.skipped for lst in incoming.values() for mb in lst if mb.pool is not None))
+        converged = board.converged
+        recs = {b: records[b] for b in local}
+        if multi:
+            # disjoint owned boxes: the sum is exact; every rank gets everything
+            cpu = torch.distributed.get_backend(group) == "gloo"
+            t = sol.cpu() if cpu else sol
+            torch.distributed.all_reduce(t, group=group)
+            sol = t.to(dev)
+            counts = torch.tensor([torn, skipped], dtype=torch.int64)
+            torch.distributed.all_reduce(counts, group=group)
+            torn, skipped = int(counts[0]), int(counts[1])
+            parts = [None] * torch.distributed.get_world_size(group)
+            torch.distributed.all_gather_object(parts, recs, group=group)
+            recs = {b: r for part in parts for b, r in part.items()}
+            torch.distributed.barrier(group=group)  # nobody posts into our rings any more
+        for eng in engines.values():
             eng.close()
+    _close_fabric(opened, shm, multi)
     # a lapped read (sender overwrote the slot mid-copy) kept the old halo,
     # i.e. behaved like "no fresh payload delivered"; reported, not an error
-    return sol, records, board.converged, torn, skipped
+    return sol, [recs[b] for b in range(nb)], converged, torn, skipped
+
+
+def _open_remote_mailboxes(plan, incoming, engines, slots, group, opened):
+    """Export the rings this process receives on (their ring, sequence and
+    delivery buffers) as CUDA IPC handles, gather every rank's, and open the
+    ones this process sends into.  Returns the sender-side views."""
+    import ctypes
+
+    lib = _lib.load()
+    mine = {}
+    for dst, lst in incoming.items():
+        for mb in lst:
+            if mb.src in engines:
+                continue
+            hs = []
+            for t in (mb.ring, mb.seqs, mb.deliver):
+                handle = (ctypes.c_ubyte * 64)()
+                off = ctypes.c_uint64(0)
+                _lib.check(lib.bs_ipc_export(ctypes.c_void_p(t.data_ptr()), handle, ctypes.byref(off)))
+                hs.append((bytes(handle), off.value))
+            mine[(mb.dst, mb.ghost_dir, mb.src)] = hs
+    parts = [None] * torch.distributed.get_world_size(group)
+    torch.distributed.all_gather_object(parts, mine, group=group)
+    table = {k: v for part in parts for k, v in part.items()}
+    out = []
+    for dst, gdir, src in plan.tolist():
+        if src not in engines or dst in engines:
+            continue
+        ptrs = []
+        for handle, off in table[(dst, gdir, src)]:
+            ptr = ctypes.c_void_p()
+            _lib.check(lib.bs_ipc_open((ctypes.c_ubyte * 64).from_buffer_copy(handle), off, ctypes.byref(ptr)))
+            opened.append(ptr.value - off)
+            ptrs.append(ptr.value)
+        out.append(_RemoteMailbox(dst, gdir, src, slots, ptrs))
+    return out
+
+
+def _shared_store(nb: int, group):
+    """The board's float64[2 nb + 4] in a POSIX shared-memory segment created
+    by rank 0 and mapped by every rank of the node (``_Board``)."""
+    from multiprocessing import shared_memory
+
+    n = 2 * nb + 4
+    rank = torch.distributed.get_rank(group)
+    name = [None]
+    if rank == 0:
+        shm = shared_memory.SharedMemory(create=True, size=8 * n)
+        name[0] = shm.name
+    src = torch.distributed.get_global_rank(group, 0) if group is not None else 0
+    torch.distributed.broadcast_object_list(name, src=src, group=group)
+    if rank != 0:
+        shm = shared_memory.SharedMemory(name=name[0])
+    store = np.ndarray((n,), dtype=np.float64, buffer=shm.buf)
+    if rank == 0:
+        store[:] = 0.0
+        store[:nb] = math.inf  # local_sq: +inf until every block published
+    torch.distributed.barrier(group=group)
+    return store, shm
+
+
+def _close_fabric(opened, shm, multi):
+    if opened:
+        lib = _lib.load()
+        for base in opened:
+            lib.bs_ipc_close(base)
+    if shm is not None:
+        try:
+            shm.close()
+            if torch.distributed.get_rank() == 0:
+                shm.unlink()
+        except Exception:
+            pass

@@ -176,8 +176,8 @@ def outer_solve_distributed(problem: LinearProblem, config: OuterConfig, group=N
     dist = torch.distributed
     if not dist.is_initialized():
         raise ConfigurationError("distributed: torch.distributed is not initialised")
-    if config.mode != "sync":
-        raise ConfigurationError("distributed: sharded runs are synchronous")
+    if config.mode == "async" and (config.inner.kind not in ("cg", "jacobi") or config.overlap != 0):
+        raise ConfigurationError("mode: async runs CG or Jacobi inner solves on overlap-0 decompositions")
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     grid = problem.grid
     nx, ny, nz = grid.shape
@@ -195,6 +195,10 @@ def outer_solve_distributed(problem: LinearProblem, config: OuterConfig, group=N
     for box in decomp.owned:
         d = float(np.linalg.norm(b3[box.lo[2]:box.hi[2], box.lo[1]:box.hi[1], box.lo[0]:box.hi[0]].ravel()))
         dens.append(d if d != 0.0 else (bnorm if bnorm != 0.0 else 1.0))
+    if config.mode == "async":
+        if engine_factory is not None:
+            raise ConfigurationError("distributed: async runs on the device engine")
+        return _solve_async(problem, config, group, decomp, local_ids, b_host, bnorm, dens)
     if config.overlap != 0:
         if engine_factory is not None:
             raise ConfigurationError("distributed: overlap > 0 runs on the device engine")
@@ -307,3 +311,26 @@ def _solve_overlap(config, group, grid, decomp, local_ids, owner, rank, world, b
     return SolveResult(solution=sol.reshape(-1).cpu().numpy(), trace=ResidualTrace(rows), converged=converged,
                        outer_iterations=len(rows), final_true_residual=final_true,
                        inner_iterations_per_block=per_block, wall_seconds=time.perf_counter() - t_start)
+
+
+def _solve_async(problem, config, group, decomp, local_ids, b_host, bnorm, dens):
+    """Asynchronous block Jacobi, one process per GPU: each rank drives its
+    blocks with the single-process async driver; halo posts to blocks of
+    other ranks are one-sided puts into their IPC-mapped mailbox rings, the
+    residual board is node-shared memory, and only the confirmation round
+    synchronises (a gloo barrier) — no per-sweep barrier anywhere."""
+    from .async_driver import outer_solve_async
+    from .multisplit import async_result
+
+    dist = torch.distributed
+    nx, ny, nz = problem.grid.shape
+    dev = require_cuda(f"cuda:{int(os.environ.get('LOCAL_RANK', torch.cuda.current_device()))}")
+    host_group = group if dist.get_backend(group) == "gloo" else dist.new_group(
+        ranks=dist.get_process_group_ranks(group) if group is not None else None, backend="gloo")
+    t_start = time.perf_counter()
+    with torch.cuda.device(dev):
+        b_dev = torch.from_numpy(b_host.reshape(nz, ny, nx)).to(dev)
+        pieces = outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, config.inner,
+                                   local=local_ids, group=host_group, distributed=True)
+        res = async_result(problem, b_dev, False, t_start, pieces)
+    return res

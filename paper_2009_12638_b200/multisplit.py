@@ -299,11 +299,17 @@ def outer_solve(problem: LinearProblem, config: OuterConfig) -> SolveResult:
 
 def _outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, on_device, t_start):
     from .async_driver import outer_solve_async
+
+    pieces = outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, config.inner)
+    return async_result(problem, b_dev, on_device, t_start, pieces)
+
+
+def async_result(problem, b_dev, on_device, t_start, pieces) -> SolveResult:
+    """SolveResult of an asynchronous run: trace aggregated across blocks
+    (multisplit.py:769-787) and the true residual of the gathered iterate."""
     from .linalg import residual_norms
 
-    grid = problem.grid
-    sol, records, converged, lapped, skipped = outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev,
-                                                       config.inner)
+    sol, records, converged, lapped, skipped = pieces
     flat = sol.reshape(-1)
     final_true = residual_norms(problem.matrix, flat, b_dev.reshape(-1))[1]
     # trace aggregation across blocks (multisplit.py:769-787)
