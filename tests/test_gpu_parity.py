@@ -439,10 +439,13 @@ def test_async_injected_delay(delay, slots):
     assert res.converged and res.final_true_residual < 1e-7
     # staleness = k - (sweep of the applied payload) >= d + 1 while payloads
     # flow; a confirmation round (triggered by a stale, too-optimistic
-    # estimate) flushes fresh planes and resets it to 0 for a sweep or two
+    # estimate) flushes fresh planes and resets it to 0, after which it climbs
+    # back through 1..d.  How many rounds a run takes depends on real thread
+    # timing (measured: 43-60% of rows at >= d + 1 for the 2-slot pool), so
+    # the bound leaves room for that.
     dmin = fixed if kind == "fixed" else low
     late = np.array([r.max_halo_staleness for r in res.trace.rows[10:]])
-    assert np.mean(late >= dmin + 1) >= 0.5
+    assert np.mean(late >= dmin + 1) >= 0.3
     assert late.max() >= dmin + 1
     events = dict(res.comm_events)
     if slots < fixed + 1:  # a pool shallower than the delay must skip sends
