@@ -986,7 +986,10 @@ __device__ __noinline__ void gmres_transition(const DBlock &B, DState &S, GState
     }
 }
 
-__device__ __noinline__ void cg_transition(const DBlock &B, DState &S, int ph, const double *q) {
+// rec = false: a redundant copy of the transition (the persistent kernel's
+// non-recording CTAs) that must not write the block's history.
+__device__ __noinline__ void cg_transition(const DBlock &B, DState &S, int ph, const double *q, bool rec = true) {
+    const int hist_cap = rec ? B.hist_cap : 0;
     switch (ph) {
         case PH_INIT: {
             for (int i = 0; i < NQ; ++i) S.q[i] = q[i];
@@ -1027,7 +1030,7 @@ __device__ __noinline__ void cg_transition(const DBlock &B, DState &S, int ph, c
             S.alpha_pend = S.alpha;
             const double rel = sqrt(rr_new) / S.scale;
             S.rel = rel;
-            if (S.it - 1 < B.hist_cap) B.hist[S.it - 1] = rel;
+            if (S.it - 1 < hist_cap) B.hist[S.it - 1] = rel;
             if (!isfinite(rel)) {
                 S.stop = BS_STOP_BREAKDOWN;
                 S.phase = PH_DONE;
@@ -1049,14 +1052,14 @@ __device__ __noinline__ void cg_transition(const DBlock &B, DState &S, int ph, c
             const double rel_true = sqrt(q[1]) / S.scale;
             if (rel_true <= S.tol_eff) {
                 S.rel = rel_true;
-                if (S.it - 1 < B.hist_cap) B.hist[S.it - 1] = rel_true;
+                if (S.it - 1 < hist_cap) B.hist[S.it - 1] = rel_true;
                 S.stop = BS_STOP_TOLERANCE_MET;
                 S.phase = PH_DONE;
             } else {
                 const double rr_new = q[1];  // r = r_true
                 const double rel = sqrt(rr_new) / S.scale;
                 S.rel = rel;
-                if (S.it - 1 < B.hist_cap) B.hist[S.it - 1] = rel;
+                if (S.it - 1 < hist_cap) B.hist[S.it - 1] = rel;
                 S.beta = rr_new / S.rr;
                 S.rr = rr_new;
                 if (S.it >= S.max_its) {
@@ -1122,14 +1125,14 @@ __device__ __noinline__ void jacobi_transition(const DBlock &B, DState &S, int p
     }
 }
 
-__device__ void transition(const DBlock &B, DState &S, GState *G, int ph, const double *q) {
+__device__ void transition(const DBlock &B, DState &S, GState *G, int ph, const double *q, bool rec = true) {
     if (ph == PH_JAC || (ph == PH_INIT && S.kind == KIND_JACOBI)) {
         jacobi_transition(B, S, ph, q);
         return;
     }
     const bool gm = (ph >= PH_G_NORM && ph <= PH_G_RESID) || (ph == PH_INIT && S.kind == KIND_GMRES);
     if (gm) gmres_transition(B, S, *G, ph, q);
-    else cg_transition(B, S, ph, q);
+    else cg_transition(B, S, ph, q, rec);
 }
 
 // Does a launch of sweep op OPK (or pointwise pass PK when OPK < 0) serve this block?
@@ -1353,13 +1356,13 @@ constexpr int CENTRAL_MAX = 4;
 
 template <int OPK, bool BOX>
 __device__ void persist_sweep(const KParams &P, unsigned char *smem, const DState *s_states, bool central,
-                              int sw) {
+                              int sw, double *part, bool local = false) {
     BS_PSTAMP(sw, 0);
     for (int t0 = blockIdx.x; t0 < P.nctas; t0 += gridDim.x) {
         const int t = op_rev(OPK) ? P.nctas - 1 - t0 : t0;  // as k_sweep
         const int b = P.cta_block[t];
         const DBlock &B = P.blocks[b];
-        const DState S = central ? ld_state_head(P.states + b) : ld_state(P.states + b);
+        const DState S = local ? s_states[b] : central ? ld_state_head(P.states + b) : ld_state(P.states + b);
         const int ph = S.phase;
         const bool served = serves<OPK, -1>(S, P);
         double acc[NQ] = {0.0, 0.0, 0.0, 0.0};
@@ -1382,7 +1385,7 @@ __device__ void persist_sweep(const KParams &P, unsigned char *smem, const DStat
                 cta_sum<NTHR>(acc, reinterpret_cast<double *>(smem));
                 if (threadIdx.x == 0) {
 #pragma unroll
-                    for (int q = 0; q < NQ; ++q) P.partials[(size_t)q * P.nctas + t] = acc[q];
+                    for (int q = 0; q < NQ; ++q) part[(size_t)q * P.nctas + t] = acc[q];
                 }
                 BS_PSTAMP(sw, 2);
             }
@@ -1493,25 +1496,145 @@ __device__ void grid_sync(const KParams &P, unsigned char *smem, DState *s_state
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+#ifndef BS_BAR_LOCAL
+#define BS_BAR_LOCAL 1
+#endif
+
+// Loop conditions of the local-decision barrier, one copy per CTA.
+struct LocalCtl {
+    int active, verify, cycles, resid_runs, stalled, max_cycles;
+};
+
+// Local-decision grid barrier (central mode): every CTA arrives once on a
+// monotonic counter and, when all have, reduces the sweep's tile partials
+// ITSELF (range_sum in tile order: the same numbers in every CTA) and
+// advances its own shared-memory copy of the block states and loop
+// conditions.  Nothing is published on the critical path — one L2 round trip
+// and a state re-read fewer than the last-arriver barrier.  Partials
+// alternate between two buffers by sweep parity: a CTA overwrites a buffer
+// only after the NEXT barrier, which every CTA reaches after reading it.
+// Only CTA 0 records the residual history (the others' transitions are
+// redundant copies).
+template <int OPK>
+__device__ void grid_sync_local(const KParams &P, unsigned char *smem, DState *s_states, const double *part,
+                                unsigned &target, LocalCtl &L, int sw) {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __syncthreads();
+    target += gridDim.x;
+    if (threadIdx.x == 0) {
+        unsigned prev;
+        asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&P.ctl->bar_count) : "memory");
+        unsigned cur = prev + 1u;
+        while ((int)(cur - target) < 0)
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(&P.ctl->bar_count) : "memory");
+    }
+    __syncthreads();
+    BS_PSTAMP(sw, 3);
+    double *scratch = reinterpret_cast<double *>(smem);
+    for (int b = 0; b < P.nblocks; ++b) {
+        if (serves<OPK, -1>(s_states[b], P)) {
+            double q[NQ];
+#pragma unroll
+            for (int i = 0; i < NQ; ++i)
+                q[i] = i < op_nq<OPK>() ? range_sum<NTHR>(part + (size_t)i * P.nctas, P.blocks[b].cta_begin,
+                                                         P.blocks[b].cta_end, scratch)
+                                        : 0.0;
+            if (threadIdx.x == 0)
+                transition(P.blocks[b], s_states[b], nullptr, s_states[b].phase, q, blockIdx.x == 0);
+        }
+    }
+    if (threadIdx.x == 0) {
+        int active = 0, verify = 0;
+        for (int bb = 0; bb < P.nblocks; ++bb) {
+            const int p2 = s_states[bb].phase;
+            if (p2 != PH_DONE && p2 != PH_IDLE) ++active;
+            if (p2 == PH_VERIFY || p2 == PH_INIT || p2 == PH_RESID) ++verify;
+        }
+        if (OPK == OP_S2) {
+            L.cycles += 1;
+            if (L.max_cycles > 0 && L.cycles > L.max_cycles && active) {
+                for (int bb = 0; bb < P.nblocks; ++bb) {
+                    DState &Sb = s_states[bb];
+                    if (Sb.phase != PH_DONE && Sb.phase != PH_IDLE) {
+                        Sb.phase = PH_DONE;
+                        Sb.stop = STOP_STALLED;
+                    }
+                }
+                L.stalled = 1;
+                active = 0;
+                verify = 0;
+            }
+        }
+        if (OPK == OP_RESID) L.resid_runs += 1;
+        L.active = active;
+        L.verify = verify;
+    }
+    __syncthreads();
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+template <bool BOX>
+__device__ void cg_persistent_local(const KParams &P, unsigned char *smem, DState *s_states) {
+    __shared__ LocalCtl L;
+    if (threadIdx.x < P.nblocks) s_states[threadIdx.x] = ld_state(P.states + threadIdx.x);
+    if (threadIdx.x == 0) L = LocalCtl{0, 0, 0, 0, 0, *(volatile int *)&P.ctl->max_cycles};
+    __syncthreads();
+    double *part[2] = {P.partials, P.partials + (size_t)NQ * P.nctas};
+    unsigned target = 0;  // bar_count is zeroed by k_reset_control before the launch
+    int sw = 0;
+    persist_sweep<OP_RESID, BOX>(P, smem, s_states, true, sw, part[sw & 1], true);
+    grid_sync_local<OP_RESID>(P, smem, s_states, part[sw & 1], target, L, sw);
+    ++sw;
+    while (L.active) {
+        persist_sweep<OP_S1, BOX>(P, smem, s_states, true, sw, part[sw & 1], true);
+        grid_sync_local<OP_S1>(P, smem, s_states, part[sw & 1], target, L, sw);
+        ++sw;
+        persist_sweep<OP_S2, BOX>(P, smem, s_states, true, sw, part[sw & 1], true);
+        grid_sync_local<OP_S2>(P, smem, s_states, part[sw & 1], target, L, sw);
+        ++sw;
+        if (L.verify) {
+            persist_sweep<OP_RESID, BOX>(P, smem, s_states, true, sw, part[sw & 1], true);
+            grid_sync_local<OP_RESID>(P, smem, s_states, part[sw & 1], target, L, sw);
+            ++sw;
+        }
+    }
+    if (blockIdx.x == 0) {
+        if (threadIdx.x < P.nblocks) P.states[threadIdx.x] = s_states[threadIdx.x];
+        if (threadIdx.x == 0) {
+            Control *ctl = P.ctl;
+            ctl->cycles = L.cycles;
+            ctl->stalled = L.stalled;
+            ctl->resid_runs = L.resid_runs;
+            ctl->active = L.active;
+            ctl->verify = L.verify;
+            *P.n_active = L.active;
+        }
+    }
+}
+
 template <bool BOX>
 __global__ void __launch_bounds__(NTHR, 2) k_cg_persistent(const KParams P) {
     extern __shared__ __align__(1024) unsigned char smem[];
     __shared__ DState s_states[CENTRAL_MAX];
     __shared__ unsigned s_gen0;
     const bool central = P.nblocks <= CENTRAL_MAX;
+    if (BS_BAR_LOCAL && central) {
+        cg_persistent_local<BOX>(P, smem, s_states);
+        return;
+    }
     if (threadIdx.x == 0) s_gen0 = *(volatile unsigned *)&P.ctl->bar_gen;  // no barrier completes before all read it
     __syncthreads();
     unsigned gen = s_gen0;
     int sw = 0;  // sweep counter (tracing only)
-    persist_sweep<OP_RESID, BOX>(P, smem, s_states, central, sw);  // INIT (and any armed residual sweep)
+    persist_sweep<OP_RESID, BOX>(P, smem, s_states, central, sw, P.partials);  // INIT (and any armed residual sweep)
     grid_sync<OP_RESID>(P, smem, s_states, central, gen, sw++);
     while (*(volatile int *)&P.ctl->active) {
-        persist_sweep<OP_S1, BOX>(P, smem, s_states, central, sw);
+        persist_sweep<OP_S1, BOX>(P, smem, s_states, central, sw, P.partials);
         grid_sync<OP_S1>(P, smem, s_states, central, gen, sw++);
-        persist_sweep<OP_S2, BOX>(P, smem, s_states, central, sw);
+        persist_sweep<OP_S2, BOX>(P, smem, s_states, central, sw, P.partials);
         grid_sync<OP_S2>(P, smem, s_states, central, gen, sw++);
         if (*(volatile int *)&P.ctl->verify) {
-            persist_sweep<OP_RESID, BOX>(P, smem, s_states, central, sw);
+            persist_sweep<OP_RESID, BOX>(P, smem, s_states, central, sw, P.partials);
             grid_sync<OP_RESID>(P, smem, s_states, central, gen, sw++);
         }
     }
@@ -2530,7 +2653,7 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
     if (e == cudaSuccess) e = cudaMalloc(&c->dstates, sizeof(DState) * nblocks);
     if (e == cudaSuccess) e = cudaMalloc(&c->dtmaps, sizeof(CUtensorMap) * maps.size());
     if (e == cudaSuccess) e = cudaMalloc(&c->dcta_block, sizeof(int) * c->nctas);
-    if (e == cudaSuccess) e = cudaMalloc(&c->dpartials, sizeof(double) * NQ * std::max(c->nctas, c->npctas));
+    if (e == cudaSuccess) e = cudaMalloc(&c->dpartials, 2 * sizeof(double) * NQ * std::max(c->nctas, c->npctas));  // x2: persistent parity buffers
     if (e == cudaSuccess) e = cudaMalloc(&c->dpcta_block, sizeof(int) * c->npctas);
     if (e == cudaSuccess)
         e = cudaMemcpy(c->dpcta_block, pcta_block.data(), sizeof(int) * c->npctas, cudaMemcpyHostToDevice);
