@@ -515,14 +515,20 @@ __device__ double range_sum(const double *part, int begin, int end, double *scra
 constexpr int TRACE_CTAS = 4096;
 __device__ unsigned long long g_trace[5][TRACE_CTAS];  // [4] = SM id
 // persistent kernel: [sweep][stamp][cta] for the first PT_SWEEPS sweeps:
-// 0 sweep start, 1 tiles done, 2 partials written, 3 barrier released
+// 0 sweep start, 1 tiles done, 2 partials written, 3 barrier released,
+// 4 = SM clock at stamp 0 (low 48 bits) | SM id << 48
 constexpr int PT_SWEEPS = 2048, PT_CTAS = 296;
+__device__ __forceinline__ unsigned smid() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
 __device__ unsigned long long g_ptrace[PT_SWEEPS][5][PT_CTAS];  // [4]: SM clock at stamp 0
 #define BS_PSTAMP(sw, i)                                                             \
     do {                                                                             \
         if (threadIdx.x == 0 && blockIdx.x < PT_CTAS) {                              \
             g_ptrace[(sw) % PT_SWEEPS][(i)][blockIdx.x] = global_ns();               \
-            if ((i) == 0) g_ptrace[(sw) % PT_SWEEPS][4][blockIdx.x] = clock64();     \
+            if ((i) == 0) g_ptrace[(sw) % PT_SWEEPS][4][blockIdx.x] = (clock64() & 0xFFFFFFFFFFFFull) | ((unsigned long long)smid() << 48); \
         }                                                                            \
     } while (0)
 #define BS_STAMP(i)                                                                  \

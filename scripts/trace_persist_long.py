@@ -27,7 +27,8 @@ t = np.frombuffer(buf, dtype=np.uint64).reshape(SW, 5, CT)[:, :, :nctas].astype(
 nsw = 1 + 2 * 856 + 1
 t = t[:nsw]
 st, done, part, rel = (t[:, i] / 1e3 for i in range(4))
-clk = t[:, 4, 0]
+clk = t[:, 4, 0] & ((1 << 48) - 1)
+sm = t[0, 4] >> 48
 mhz = np.diff(clk) / np.diff(t[:, 0, 0]) * 1e3
 for lo in range(1, nsw - 2, 200):
     idx = np.arange(lo, min(lo + 200, nsw - 2))
@@ -36,5 +37,21 @@ for lo in range(1, nsw - 2, 200):
         tail = done[sel].max(axis=1) - np.median(done[sel], axis=1)
         bar = rel[sel].min(axis=1) - part[sel].max(axis=1)
         spread = st[sel].max(axis=1) - st[sel].min(axis=1)
+        epi = part[sel].max(axis=1) - done[sel].max(axis=1)
+        red = st[sel + 1].min(axis=1) - rel[sel].max(axis=1)
+        period = st[sel + 1].max(axis=1) - st[sel].max(axis=1)
         print(f"sweeps {lo:4d}-{idx[-1]:4d} {kind}: fill->done {fd.mean():6.1f}  tail {tail.mean():5.1f}  "
-              f"barrier {bar.mean():5.1f}  start-spread {spread.mean():4.1f}  SM MHz {mhz[sel].mean():6.0f}")
+              f"barrier {bar.mean():5.1f}  start-spread {spread.mean():4.1f}  epi {epi.mean():4.1f}  reduce {red.mean():4.1f}  "
+              f"period {period.mean():6.1f}  SM MHz {mhz[sel].mean():6.0f}")
+
+# which CTAs finish late: lateness vs. how many CTAs share the SM
+sel = np.arange(1, nsw - 2)
+late = (done[sel] - np.median(done[sel], axis=1, keepdims=True)).mean(axis=0)
+share = np.array([(sm == s).sum() for s in sm])
+for c in (1, 2):
+    m = share == c
+    if m.any():
+        print(f"CTAs sharing an SM with {c - 1} other: {m.sum():3d}  mean lateness {late[m].mean():5.2f} us  "
+              f"max {late[m].max():5.2f}")
+order = np.argsort(late)[::-1][:12]
+print("latest CTAs (cta, sm, share, lateness):", [(int(i), int(sm[i]), int(share[i]), round(float(late[i]), 2)) for i in order])
