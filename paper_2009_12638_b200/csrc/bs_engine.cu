@@ -148,14 +148,29 @@ __host__ __device__ constexpr bool op_has_b(int op) { return op == OP_RESID || o
 #define BS_REV_S2 1
 #endif
 __host__ __device__ constexpr bool op_rev(int op) { return BS_REV_S2 && op == OP_S2; }
-__host__ __device__ constexpr int op_stages(int op) { return op_has_b(op) ? BS_NSTAGE_AB : BS_NSTAGE_A; }
-__host__ __device__ constexpr int op_coff(int op) { return op_has_b(op) ? 2 * SEG_H : SEG_H; }
-__host__ __device__ constexpr int op_stage_bytes(int op) { return op_coff(op) + SEG_O; }
+// Planes per ring stage: CG sweep 2 stages its planes in pairs (one TMA box of
+// depth 2 per operand): half the TMA issues and mbarrier round trips per byte
+// of the lightest sweep.
+#ifndef BS_ZP_S2
+#define BS_ZP_S2 2
+#endif
+__host__ __device__ constexpr int op_zp(int op) { return op == OP_S2 ? BS_ZP_S2 : 1; }
+__host__ __device__ constexpr int op_stages(int op) {
+    return op_has_b(op) ? BS_NSTAGE_AB : (BS_NSTAGE_A + op_zp(op) - 1) / op_zp(op);
+}
+// stage layout: [A: zp haloed planes][B: zp haloed planes, if any][C: zp bare planes]
+__host__ __device__ constexpr int op_sega(int op) { return ((op_zp(op) * SC * 8 + 127) / 128) * 128; }
+__host__ __device__ constexpr int op_coff(int op) { return op_has_b(op) ? 2 * op_sega(op) : op_sega(op); }
+__host__ __device__ constexpr int op_stage_bytes(int op) { return op_coff(op) + op_zp(op) * SEG_O; }
 __host__ __device__ constexpr int op_smem(int op) { return op_stages(op) * (op_stage_bytes(op) + 16); }
 constexpr int SMEM_MAX = op_smem(OP_S1) > op_smem(OP_S2) ? op_smem(OP_S1) : op_smem(OP_S2);
 
 // tensor maps per block
-enum Tm : int { TM_XH = 0, TM_P0H = 1, TM_P1H = 2, TM_RH = 3, TM_XO = 4, TM_RO = 5, TM_BO = 6, NTM = 7 };
+// (suffix 2: boxes two planes deep, for sweeps staging plane pairs)
+enum Tm : int {
+    TM_XH = 0, TM_P0H = 1, TM_P1H = 2, TM_RH = 3, TM_XO = 4, TM_RO = 5, TM_BO = 6,
+    TM_P0H2 = 7, TM_P1H2 = 8, TM_RO2 = 9, NTM = 10
+};
 
 constexpr int STOP_STALLED = 4;
 
@@ -605,10 +620,14 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
     constexpr int NS = op_stages(OP);
     constexpr int STB = op_stage_bytes(OP);
     constexpr int COFF = op_coff(OP);
+    constexpr int ZP = op_zp(OP);     // planes per stage
+    constexpr int BOFF = op_sega(OP); // B operand of a plane, from its A plane
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + NS * STB);
     uint64_t *empty = full + NS;
     const bool use_b = C.map_b != nullptr;
     const bool use_c = C.map_c != nullptr;
+    // slot of plane q inside its stage's box (boxes run upwards in z)
+    auto slot = [](int qq) { return REV ? ZP - 1 - qq % ZP : qq % ZP; };
 
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) {
@@ -622,16 +641,19 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
 
     if (warp == NCW) {  // ---------------- TMA producer warp
         if (lane == 0) {
-            for (int q = 0; q < nplanes; ++q) {
-                const int s = q % NS;
-                if (q >= NS) mbar_wait(&empty[s], (uint32_t)((q / NS - 1) & 1));
-                const int lz = lzq0 + DZ * q;
-                const bool epi = use_c && q >= 1 && q <= nplanes - 2;
+            const int nst = (nplanes + ZP - 1) / ZP;
+            for (int k = 0; k < nst; ++k) {  // stage k holds planes ZP*k .. ZP*k+ZP-1
+                const int s = k % NS;
+                if (k >= NS) mbar_wait(&empty[s], (uint32_t)((k / NS - 1) & 1));
+                const int lz = REV ? lzq0 - ZP * k - (ZP - 1) : lzq0 + ZP * k;  // lowest plane of the box
+                // ZP == 1: the bare operand only for computed planes; ZP > 1: always
+                const bool epi = use_c && (ZP > 1 || (k >= 1 && k <= nplanes - 2));
                 unsigned char *st = smem + s * STB;
-                const uint32_t bytes = (uint32_t)(SC * 8) * (use_b ? 2u : 1u) + (epi ? (uint32_t)SEG_O : 0u);
+                const uint32_t bytes =
+                    (uint32_t)(ZP * SC * 8) * (use_b ? 2u : 1u) + (epi ? (uint32_t)(ZP * SEG_O) : 0u);
                 mbar_expect_tx(&full[s], bytes);
                 tma_load3(st, C.map_a, lx0 - 2, ly0 - 1, lz, &full[s]);
-                if (use_b) tma_load3(st + SEG_H, C.map_b, lx0 - 2, ly0 - 1, lz, &full[s]);
+                if (use_b) tma_load3(st + BOFF, C.map_b, lx0 - 2, ly0 - 1, lz, &full[s]);
                 if (epi) tma_load3(st + COFF, C.map_c, lx0, ly0, lz, &full[s]);
             }
         }
@@ -654,8 +676,8 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
 
     auto val = [&](const unsigned char *st, int cell) -> double {
         const double a = reinterpret_cast<const double *>(st)[cell];
-        if (OP == OP_RESID) return pend ? add(a, mul(alpha_pend, reinterpret_cast<const double *>(st + SEG_H)[cell])) : a;
-        if (OP == OP_S1) return first ? a : add(a, mul(beta, reinterpret_cast<const double *>(st + SEG_H)[cell]));
+        if (OP == OP_RESID) return pend ? add(a, mul(alpha_pend, reinterpret_cast<const double *>(st + BOFF)[cell])) : a;
+        if (OP == OP_S1) return first ? a : add(a, mul(beta, reinterpret_cast<const double *>(st + BOFF)[cell]));
         return a;
     };
     // !BOX: a plane is `easy` for a warp when every point it computes lies at
@@ -685,12 +707,15 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
     mbar_wait(&full[0], 0u);
     if (tid == 0) BS_STAMP(1);
 #pragma unroll
-    for (int r = 0; r < RY; ++r) u_prev[r] = uval(smem, own[r], 0, gjr[r], lzq0);
-    mbar_wait(&full[1], 0u);
+    for (int r = 0; r < RY; ++r) u_prev[r] = uval(smem + slot(0) * (SC * 8), own[r], 0, gjr[r], lzq0);
+    if (ZP == 1) mbar_wait(&full[1], 0u);
+    const unsigned char *st1 = smem + (ZP == 1 ? STB : 0) + slot(1) * (SC * 8);
 #pragma unroll
-    for (int r = 0; r < RY; ++r) u_cur[r] = uval(smem + STB, own[r], 0, gjr[r], lzq0 + DZ);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[0]);
+    for (int r = 0; r < RY; ++r) u_cur[r] = uval(st1, own[r], 0, gjr[r], lzq0 + DZ);
+    if (ZP == 1) {  // plane 0 is never computed: its stage is free (ZP > 1: plane 1 shares it)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[0]);
+    }
 
     const bool px_box = lx > 0;
     // warp-uniform fast path: every lane of this warp has its x-1 and y-1
@@ -709,10 +734,13 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
     // plane's parity) are constants or one loop-carried bit.
     // u_prev / u_next are the planes behind / ahead in traversal order: the
     // z-1 / z+1 neighbours forward, z+1 / z-1 reversed.
-    auto single_step = [&](int q, int s, int sn, uint32_t par_n) {
+    // plane q: stage s, slot sl; the next plane: stage sn, slot sln, waited
+    // for only when it opens a new stage; the stage is released after its
+    // last plane.
+    auto single_step = [&](int q, int s, int sl, int sn, int sln, bool wait_next, uint32_t par_n, bool release) {
         const int lz = lzq0 + DZ * q;
-        const unsigned char *st = smem + s * STB;
-        const double *cst = reinterpret_cast<const double *>(st + COFF);
+        const unsigned char *st = smem + s * STB + sl * (SC * 8);
+        const double *cst = reinterpret_cast<const double *>(smem + s * STB + COFF + sl * SEG_O);
         // Phase A, before plane q+1 is waited for: the in-plane neighbours and,
         // on the interior fast path, the reduceat chain up to its last term
         // (z+1 enters second to last), so the wait overlaps the DP latency.
@@ -736,10 +764,10 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
             // reversed: z+1 is the plane behind, so it enters the chain now
             if (REV && fast) pre_[r] = add(pre_[r], -u_prev[r]);
         }
-        mbar_wait(&full[sn], par_n & 1u);
+        if (wait_next) mbar_wait(&full[sn], par_n & 1u);
         double u_next[RY];
 #pragma unroll
-        for (int r = 0; r < RY; ++r) u_next[r] = uval(smem + sn * STB, own[r], 0, gjr[r], lz + DZ);
+        for (int r = 0; r < RY; ++r) u_next[r] = uval(smem + sn * STB + sln * (SC * 8), own[r], 0, gjr[r], lz + DZ);
 #pragma unroll
         for (int r = 0; r < RY; ++r) {
             const int ly = ly_0 + r;
@@ -796,7 +824,7 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
             } else if (OP == OP_S1) {
                 out_p[sxr] = u_cur[r];
                 if (pend)
-                    out_x[sxr] = add(cst[ci], mul(alpha_pend, reinterpret_cast<const double *>(st + SEG_H)[own[r]]));
+                    out_x[sxr] = add(cst[ci], mul(alpha_pend, reinterpret_cast<const double *>(st + BOFF)[own[r]]));
                 acc[0] = add(acc[0], mul(u_cur[r], au));
             } else {  // OP_RESID: r = (b - C*halo) - A_ii u ; OP_JAC: also the Jacobi update
                 const double bv = cst[ci];
@@ -838,16 +866,21 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
             u_prev[r] = u_cur[r];
             u_cur[r] = u_next[r];
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
+        if (release) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
     };
-    // q = 1 .. nplanes-2 in rounds of NS aligned to stage 0
-    uint32_t par = 0;  // completion parity of the planes of this round
-    for (int q0 = 0; q0 <= nplanes - 2; q0 += NS, par ^= 1u) {
+    // q = 1 .. nplanes-2 in rounds of NS stages (NS*ZP planes) aligned to stage 0
+    uint32_t par = 0;  // completion parity of the stages of this round
+    for (int q0 = 0; q0 <= nplanes - 2; q0 += NS * ZP, par ^= 1u) {
 #pragma unroll
-        for (int u = 0; u < NS; ++u) {
+        for (int u = 0; u < NS * ZP; ++u) {
             const int q = q0 + u;
-            if (q >= 1 && q <= nplanes - 2) single_step(q, u, (u + 1) % NS, u + 1 == NS ? par ^ 1u : par);
+            const int un = u + 1;
+            if (q >= 1 && q <= nplanes - 2)
+                single_step(q, u / ZP, slot(u), (un / ZP) % NS, slot(un), un % ZP == 0,
+                            un == NS * ZP ? par ^ 1u : par, u % ZP == ZP - 1);
         }
     }
     if (tid == 0) BS_STAMP(2);
@@ -1303,9 +1336,9 @@ __device__ __forceinline__ SweepCtx make_ctx(const KParams &P, int b, const DBlo
             C.map_b = (!C.first || C.pend) ? tm_p : nullptr;
             C.map_c = C.pend ? tm + TM_XO : nullptr;
         } else if (OPK == OP_S2) {
-            C.map_a = tm_p;
+            C.map_a = op_zp(OP_S2) == 2 ? tm + (S.pcur ? TM_P1H2 : TM_P0H2) : tm_p;
             C.map_b = nullptr;
-            C.map_c = tm + TM_RO;
+            C.map_c = tm + (op_zp(OP_S2) == 2 ? TM_RO2 : TM_RO);
         } else {  // OP_GSPMV: u = v_j (haloed), epilogue operand v_0 (bare)
             const CUtensorMap *gm = P.gmaps + (size_t)b * (MAXM + 1);
             C.first = S.gj == 0;
@@ -2220,11 +2253,11 @@ int get_encoder() {
 
 // 3-D map over a block's pitched padded box; haloed (TX+4 x TY+2) or bare (TX x TY) plane boxes.
 // Box starts are 16-byte aligned in x: tile origins are multiples of TX, haloed boxes start at x0-2.
-int encode_map(CUtensorMap *m, const void *ptr, const DBlock &B, bool halo) {
+int encode_map(CUtensorMap *m, const void *ptr, const DBlock &B, bool halo, int depth = 1) {
     if (int e = get_encoder()) return e;
     cuuint64_t dims[3] = {(cuuint64_t)B.pdim[0], (cuuint64_t)B.pdim[1], (cuuint64_t)B.pdim[2]};
     cuuint64_t strides[2] = {(cuuint64_t)B.pitch * 8, (cuuint64_t)B.pitch * B.pdim[1] * 8};
-    cuuint32_t box[3] = {(cuuint32_t)(halo ? SX : TX), (cuuint32_t)(halo ? HY : TY), 1};
+    cuuint32_t box[3] = {(cuuint32_t)(halo ? SX : TX), (cuuint32_t)(halo ? HY : TY), (cuuint32_t)depth};
     cuuint32_t es[3] = {1, 1, 1};
     CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void *>(ptr), dims, strides, box, es,
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -2613,6 +2646,9 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
         if (!e) e = encode_map(&m[TM_XO], B.x, B, false);
         if (!e) e = encode_map(&m[TM_RO], B.r, B, false);
         if (!e) e = encode_map(&m[TM_BO], B.b, B, false);
+        if (!e) e = encode_map(&m[TM_P0H2], B.p[0], B, true, 2);
+        if (!e) e = encode_map(&m[TM_P1H2], B.p[1], B, true, 2);
+        if (!e) e = encode_map(&m[TM_RO2], B.r, B, false, 2);
         if (e) {
             delete c;
             return e;
