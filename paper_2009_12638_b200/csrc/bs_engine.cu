@@ -154,22 +154,28 @@ __host__ __device__ constexpr bool op_rev(int op) { return BS_REV_S2 && op == OP
 #ifndef BS_ZP_S2
 #define BS_ZP_S2 2
 #endif
-__host__ __device__ constexpr int op_zp(int op) { return op == OP_S2 ? BS_ZP_S2 : 1; }
+#ifndef BS_ZP_S1
+#define BS_ZP_S1 1
+#endif
+__host__ __device__ constexpr int op_zp(int op) { return op == OP_S2 ? BS_ZP_S2 : (op == OP_S1 ? BS_ZP_S1 : 1); }
 __host__ __device__ constexpr int op_stages(int op) {
-    return op_has_b(op) ? BS_NSTAGE_AB : (BS_NSTAGE_A + op_zp(op) - 1) / op_zp(op);
+    return ((op_has_b(op) ? BS_NSTAGE_AB : BS_NSTAGE_A) + op_zp(op) - 1) / op_zp(op);
 }
 // stage layout: [A: zp haloed planes][B: zp haloed planes, if any][C: zp bare planes]
 __host__ __device__ constexpr int op_sega(int op) { return ((op_zp(op) * SC * 8 + 127) / 128) * 128; }
 __host__ __device__ constexpr int op_coff(int op) { return op_has_b(op) ? 2 * op_sega(op) : op_sega(op); }
 __host__ __device__ constexpr int op_stage_bytes(int op) { return op_coff(op) + op_zp(op) * SEG_O; }
 __host__ __device__ constexpr int op_smem(int op) { return op_stages(op) * (op_stage_bytes(op) + 16); }
-constexpr int SMEM_MAX = op_smem(OP_S1) > op_smem(OP_S2) ? op_smem(OP_S1) : op_smem(OP_S2);
+constexpr int cmax(int a, int b) { return a > b ? a : b; }
+constexpr int SMEM_MAX = cmax(cmax(cmax(op_smem(OP_RESID), op_smem(OP_S1)), cmax(op_smem(OP_S2), op_smem(OP_APPLY))),
+                              cmax(op_smem(OP_GSPMV), op_smem(OP_JAC)));
 
 // tensor maps per block
-// (suffix 2: boxes two planes deep, for sweeps staging plane pairs)
+// (suffixes _S1/_S2: boxes op_zp(OP_S1/OP_S2) planes deep, for the CG sweeps)
 enum Tm : int {
     TM_XH = 0, TM_P0H = 1, TM_P1H = 2, TM_RH = 3, TM_XO = 4, TM_RO = 5, TM_BO = 6,
-    TM_P0H2 = 7, TM_P1H2 = 8, TM_RO2 = 9, NTM = 10
+    TM_P0H_S2 = 7, TM_P1H_S2 = 8, TM_RO_S2 = 9,
+    TM_RH_S1 = 10, TM_P0H_S1 = 11, TM_P1H_S1 = 12, TM_XO_S1 = 13, NTM = 14
 };
 
 constexpr int STOP_STALLED = 4;
@@ -1322,6 +1328,7 @@ __device__ __forceinline__ SweepCtx make_ctx(const KParams &P, int b, const DBlo
         C.yout = nullptr;
         C.pout = B.p[S.pcur ^ 1];
         const CUtensorMap *tm_p = tm + (S.pcur ? TM_P1H : TM_P0H);
+        const CUtensorMap *tm_p1 = tm + (S.pcur ? TM_P1H_S1 : TM_P0H_S1);
         if (OPK == OP_RESID) {
             C.map_a = tm + (S.xin ? TM_P0H : TM_XH);
             C.map_b = C.pend ? tm_p : nullptr;
@@ -1332,13 +1339,13 @@ __device__ __forceinline__ SweepCtx make_ctx(const KParams &P, int b, const DBlo
             C.map_c = tm + TM_BO;
             C.pout = S.xin ? B.x : B.p[0];
         } else if (OPK == OP_S1) {
-            C.map_a = tm + TM_RH;
-            C.map_b = (!C.first || C.pend) ? tm_p : nullptr;
-            C.map_c = C.pend ? tm + TM_XO : nullptr;
+            C.map_a = tm + TM_RH_S1;
+            C.map_b = (!C.first || C.pend) ? tm_p1 : nullptr;
+            C.map_c = C.pend ? tm + TM_XO_S1 : nullptr;
         } else if (OPK == OP_S2) {
-            C.map_a = op_zp(OP_S2) == 2 ? tm + (S.pcur ? TM_P1H2 : TM_P0H2) : tm_p;
+            C.map_a = tm + (S.pcur ? TM_P1H_S2 : TM_P0H_S2);
             C.map_b = nullptr;
-            C.map_c = tm + (op_zp(OP_S2) == 2 ? TM_RO2 : TM_RO);
+            C.map_c = tm + TM_RO_S2;
         } else {  // OP_GSPMV: u = v_j (haloed), epilogue operand v_0 (bare)
             const CUtensorMap *gm = P.gmaps + (size_t)b * (MAXM + 1);
             C.first = S.gj == 0;
@@ -2646,9 +2653,13 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
         if (!e) e = encode_map(&m[TM_XO], B.x, B, false);
         if (!e) e = encode_map(&m[TM_RO], B.r, B, false);
         if (!e) e = encode_map(&m[TM_BO], B.b, B, false);
-        if (!e) e = encode_map(&m[TM_P0H2], B.p[0], B, true, 2);
-        if (!e) e = encode_map(&m[TM_P1H2], B.p[1], B, true, 2);
-        if (!e) e = encode_map(&m[TM_RO2], B.r, B, false, 2);
+        if (!e) e = encode_map(&m[TM_P0H_S2], B.p[0], B, true, op_zp(OP_S2));
+        if (!e) e = encode_map(&m[TM_P1H_S2], B.p[1], B, true, op_zp(OP_S2));
+        if (!e) e = encode_map(&m[TM_RO_S2], B.r, B, false, op_zp(OP_S2));
+        if (!e) e = encode_map(&m[TM_RH_S1], B.r, B, true, op_zp(OP_S1));
+        if (!e) e = encode_map(&m[TM_P0H_S1], B.p[0], B, true, op_zp(OP_S1));
+        if (!e) e = encode_map(&m[TM_P1H_S1], B.p[1], B, true, op_zp(OP_S1));
+        if (!e) e = encode_map(&m[TM_XO_S1], B.x, B, false, op_zp(OP_S1));
         if (e) {
             delete c;
             return e;
