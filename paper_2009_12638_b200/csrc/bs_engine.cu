@@ -724,9 +724,6 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
     }
 
     const bool px_box = lx > 0;
-    // warp-uniform fast path: every lane of this warp has its x-1 and y-1
-    // neighbours in the box for all its rows
-    const bool warp_xy_interior = __all_sync(0xffffffffu, px_box && ly_0 > 0);
     // output pointers hoisted into registers: stores through them cannot alias
     // the block descriptor, so the compiler need not re-load it every plane
     double *__restrict__ out_r = B.r;
@@ -757,7 +754,13 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
             for (int r = 0; r < RY; ++r) e = e && (!row_in[r] || box_dist1(B, gi, gjr[r], gk) < B.overlap);
             easy = __all_sync(0xffffffffu, e);
         }
-        const bool fast = easy && warp_xy_interior && lz > 0;
+        // Fast path = stencil7's z-present branch, which never tests the x / y
+        // flags: an absent x-1 / y-1 neighbour of a box (or easy) row lies
+        // outside the padded box, where TMA zero-fills, and an exact zero
+        // inside the chain leaves every partial sum unchanged.  So only the
+        // z-1 presence selects it — tiles on the low x / y faces stream as
+        // fast as interior ones (they used to finish each sweep last).
+        const bool fast = easy && lz > 0;
         double xm_[RY], xp_[RY], ym_[RY], yp_[RY], pre_[RY];
 #pragma unroll
         for (int r = 0; r < RY; ++r) {

@@ -55,3 +55,12 @@ for c in (1, 2):
               f"max {late[m].max():5.2f}")
 order = np.argsort(late)[::-1][:12]
 print("latest CTAs (cta, sm, share, lateness):", [(int(i), int(sm[i]), int(share[i]), round(float(late[i]), 2)) for i in order])
+# lateness by tile column (ix = tile % tiles_x; S2 walks the tiles in reverse order)
+tx = 256 // 32 if n == 256 else None
+if tx:
+    for kind, sel in (("S1", np.arange(1, nsw - 2, 2)), ("S2", np.arange(2, nsw - 2, 2))):
+        lt = (done[sel] - np.median(done[sel], axis=1, keepdims=True)).mean(axis=0)
+        tiles = np.arange(nctas) if kind == "S1" else nctas - 1 - np.arange(nctas)
+        print(kind, "lateness by tile ix:", [round(float(lt[tiles % tx == i].mean()), 2) for i in range(tx)])
+        iy = tiles // tx
+        print(kind, "lateness by tile iy (first/last 4):", [round(float(lt[iy == i].mean()), 2) for i in (0, 1, 2, 3, 28, 29, 30, 31)])
