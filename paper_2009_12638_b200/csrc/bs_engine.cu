@@ -507,24 +507,39 @@ __device__ __forceinline__ void cta_sum(double (&acc)[NQ], double *red) {
     }
 }
 
-// Sum of partials[begin:end) with a fixed strided + tree order (whole CTA,
-// NTH >= 256 threads); scratch holds 256 doubles.
+// Sum of partials[begin:end) in a fixed order: 256 virtual lanes, lane l
+// sums part[begin + l + 256 k] (k ascending), then a binary tree pairing
+// l with l + w for w = 128, 64, ..., 1.  The lane sums are spread over the
+// CTA (all loads in flight at once); warp 0 then folds the tree levels
+// 128 / 64 / 32 in registers (lane t holds virtual lanes t + 32 m) and the
+// last five with shuffles — the same tree, so the same bits, as a
+// shared-memory tree over 256 threads, with three CTA barriers instead of
+// ten.  All NTH threads call it and get the sum (scratch: 256 doubles).
 template <int NTH>
 __device__ double range_sum(const double *part, int begin, int end, double *scratch) {
+    static_assert(NTH >= 32, "range_sum needs a full warp");
     const int tid = threadIdx.x;
-    // 256 virtual lanes whatever the CTA size, so the order is the same in
-    // every kernel: lane l sums part[begin + l + 256 k], then a binary tree
     for (int l = tid; l < 256; l += NTH) {
         double s = 0.0;
         for (int c = begin + l; c < end; c += 256) s = add(s, __ldcg(part + c));
         scratch[l] = s;
     }
     __syncthreads();
-    for (int w = 128; w > 0; w >>= 1) {
-        if (tid < w) scratch[tid] = add(scratch[tid], scratch[tid + w]);
-        __syncthreads();
+    if (tid < 32) {
+        double v[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) v[m] = scratch[tid + 32 * m];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) v[m] = add(v[m], v[m + 4]);  // w = 128
+        v[0] = add(v[0], v[2]);                                    // w = 64
+        v[1] = add(v[1], v[3]);
+        double t = add(v[0], v[1]);                                // w = 32
+#pragma unroll
+        for (int w = 16; w > 0; w >>= 1) t = add(t, __shfl_down_sync(0xffffffffu, t, w));
+        if (tid == 0) scratch[0] = t;
     }
-    double out = scratch[0];
+    __syncthreads();
+    const double out = scratch[0];
     __syncthreads();
     return out;
 }
