@@ -157,7 +157,13 @@ __host__ __device__ constexpr bool op_rev(int op) { return BS_REV_S2 && op == OP
 #ifndef BS_ZP_S1
 #define BS_ZP_S1 1
 #endif
-__host__ __device__ constexpr int op_zp(int op) { return op == OP_S2 ? BS_ZP_S2 : (op == OP_S1 ? BS_ZP_S1 : 1); }
+#ifndef BS_ZP_LIGHT
+#define BS_ZP_LIGHT 2  // SpMV, point-Jacobi and GMRES-SpMV sweeps (one haloed operand)
+#endif
+__host__ __device__ constexpr int op_zp(int op) {
+    return op == OP_S2 ? BS_ZP_S2
+                       : op == OP_S1 ? BS_ZP_S1 : (op == OP_APPLY || op == OP_JAC || op == OP_GSPMV) ? BS_ZP_LIGHT : 1;
+}
 __host__ __device__ constexpr int op_stages(int op) {
     return ((op_has_b(op) ? BS_NSTAGE_AB : BS_NSTAGE_A) + op_zp(op) - 1) / op_zp(op);
 }
@@ -175,7 +181,8 @@ constexpr int SMEM_MAX = cmax(cmax(cmax(op_smem(OP_RESID), op_smem(OP_S1)), cmax
 enum Tm : int {
     TM_XH = 0, TM_P0H = 1, TM_P1H = 2, TM_RH = 3, TM_XO = 4, TM_RO = 5, TM_BO = 6,
     TM_P0H_S2 = 7, TM_P1H_S2 = 8, TM_RO_S2 = 9,
-    TM_RH_S1 = 10, TM_P0H_S1 = 11, TM_P1H_S1 = 12, TM_XO_S1 = 13, NTM = 14
+    TM_RH_S1 = 10, TM_P0H_S1 = 11, TM_P1H_S1 = 12, TM_XO_S1 = 13,
+    TM_XH_J = 14, TM_P0H_J = 15, TM_BO_J = 16, NTM = 17  // _J: point-Jacobi sweeps
 };
 
 constexpr int STOP_STALLED = 4;
@@ -1352,9 +1359,9 @@ __device__ __forceinline__ SweepCtx make_ctx(const KParams &P, int b, const DBlo
             C.map_b = C.pend ? tm_p : nullptr;
             C.map_c = tm + TM_BO;
         } else if (OPK == OP_JAC) {  // x_k haloed from buf[xin], b bare; x_{k+1} -> other buffer
-            C.map_a = tm + (S.xin ? TM_P0H : TM_XH);
+            C.map_a = tm + (S.xin ? TM_P0H_J : TM_XH_J);
             C.map_b = nullptr;
-            C.map_c = tm + TM_BO;
+            C.map_c = tm + TM_BO_J;
             C.pout = S.xin ? B.x : B.p[0];
         } else if (OPK == OP_S1) {
             C.map_a = tm + TM_RH_S1;
@@ -2678,6 +2685,9 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
         if (!e) e = encode_map(&m[TM_P0H_S1], B.p[0], B, true, op_zp(OP_S1));
         if (!e) e = encode_map(&m[TM_P1H_S1], B.p[1], B, true, op_zp(OP_S1));
         if (!e) e = encode_map(&m[TM_XO_S1], B.x, B, false, op_zp(OP_S1));
+        if (!e) e = encode_map(&m[TM_XH_J], B.x, B, true, op_zp(OP_JAC));
+        if (!e) e = encode_map(&m[TM_P0H_J], B.p[0], B, true, op_zp(OP_JAC));
+        if (!e) e = encode_map(&m[TM_BO_J], B.b, B, false, op_zp(OP_JAC));
         if (e) {
             delete c;
             return e;
@@ -2835,7 +2845,7 @@ int bs_stencil_apply(bs_ctx *c, int block, const double *x, double *y, void *str
     if (int e = set_dev(c)) return e;
     const DBlock &B = c->hblocks[block];
     CUtensorMap xmap;
-    if (int e = encode_map(&xmap, x, B, true)) return e;
+    if (int e = encode_map(&xmap, x, B, true, op_zp(OP_APPLY))) return e;
     ++g_launches;
     if (B.overlap == 0)
         k_apply<true><<<B.cta_end - B.cta_begin, NTHR, op_smem(OP_APPLY), (cudaStream_t)stream>>>(c->dblocks, block, xmap, y);
@@ -3059,8 +3069,10 @@ int bs_gmres_setup(bs_ctx *c, int m, const bs_gmres_desc *descs) {
         B.vstride = d.vstride;
         B.W = d.W;
         for (int j = 0; j < m; ++j)
-            if (int e = encode_map(&maps[(size_t)b * (MAXM + 1) + j], B.V + (size_t)j * d.vstride, B, true)) return e;
-        if (int e = encode_map(&maps[(size_t)b * (MAXM + 1) + MAXM], B.V, B, false)) return e;
+            if (int e = encode_map(&maps[(size_t)b * (MAXM + 1) + j], B.V + (size_t)j * d.vstride, B, true,
+                                   op_zp(OP_GSPMV)))
+                return e;
+        if (int e = encode_map(&maps[(size_t)b * (MAXM + 1) + MAXM], B.V, B, false, op_zp(OP_GSPMV))) return e;
     }
     cudaFree(c->dgmaps);
     c->dgmaps = nullptr;

@@ -43,3 +43,8 @@ def jac():
 
 t = ev_time(jac, 3)
 print(f"jacobi: {t / (K + 1):.1f} us per sweep ({24 * N / (t / (K + 1)) / 1e3:.0f} GB/s at 24 B/pt)")
+
+xp, yp = bb.zeros_pitched(), bb.zeros_pitched()
+xp.copy_(torch.rand_like(xp))
+t = ev_time(lambda: eng.apply(0, xp, yp), 50)
+print(f"spmv: {t:.1f} us  ({16 * N / t / 1e3:.0f} GB/s at 16 B/pt)")
