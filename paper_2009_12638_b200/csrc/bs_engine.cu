@@ -164,8 +164,12 @@ __host__ __device__ constexpr int op_zp(int op) {
     return op == OP_S2 ? BS_ZP_S2
                        : op == OP_S1 ? BS_ZP_S1 : (op == OP_APPLY || op == OP_JAC || op == OP_GSPMV) ? BS_ZP_LIGHT : 1;
 }
+#ifndef BS_NSTAGE_APPLY
+#define BS_NSTAGE_APPLY 20  // ring depth (planes) of the standalone SpMV: nothing but the stencil per plane
+#endif
 __host__ __device__ constexpr int op_stages(int op) {
-    return ((op_has_b(op) ? BS_NSTAGE_AB : BS_NSTAGE_A) + op_zp(op) - 1) / op_zp(op);
+    return ((op_has_b(op) ? BS_NSTAGE_AB : op == OP_APPLY ? BS_NSTAGE_APPLY : BS_NSTAGE_A) + op_zp(op) - 1) /
+           op_zp(op);
 }
 // stage layout: [A: zp haloed planes][B: zp haloed planes, if any][C: zp bare planes]
 __host__ __device__ constexpr int op_sega(int op) { return ((op_zp(op) * SC * 8 + 127) / 128) * 128; }
