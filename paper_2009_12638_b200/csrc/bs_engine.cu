@@ -160,9 +160,15 @@ __host__ __device__ constexpr bool op_rev(int op) { return BS_REV_S2 && op == OP
 #ifndef BS_ZP_LIGHT
 #define BS_ZP_LIGHT 2  // SpMV, point-Jacobi and GMRES-SpMV sweeps (one haloed operand)
 #endif
+#ifndef BS_ZP_RESID
+#define BS_ZP_RESID 2
+#endif
 __host__ __device__ constexpr int op_zp(int op) {
-    return op == OP_S2 ? BS_ZP_S2
-                       : op == OP_S1 ? BS_ZP_S1 : (op == OP_APPLY || op == OP_JAC || op == OP_GSPMV) ? BS_ZP_LIGHT : 1;
+    return op == OP_S2      ? BS_ZP_S2
+           : op == OP_S1    ? BS_ZP_S1
+           : op == OP_RESID ? BS_ZP_RESID
+           : (op == OP_APPLY || op == OP_JAC || op == OP_GSPMV) ? BS_ZP_LIGHT
+                                                                : 1;
 }
 #ifndef BS_NSTAGE_APPLY
 #define BS_NSTAGE_APPLY 20  // ring depth (planes) of the standalone SpMV: nothing but the stencil per plane
@@ -180,13 +186,14 @@ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 constexpr int SMEM_MAX = cmax(cmax(cmax(op_smem(OP_RESID), op_smem(OP_S1)), cmax(op_smem(OP_S2), op_smem(OP_APPLY))),
                               cmax(op_smem(OP_GSPMV), op_smem(OP_JAC)));
 
-// tensor maps per block
-// (suffixes _S1/_S2: boxes op_zp(OP_S1/OP_S2) planes deep, for the CG sweeps)
+// Tensor maps per block, one set per sweep op: each op's boxes are op_zp(op)
+// planes deep (H: haloed (TX+4) x (TY+2) box, O: bare TX x TY tile).
 enum Tm : int {
-    TM_XH = 0, TM_P0H = 1, TM_P1H = 2, TM_RH = 3, TM_XO = 4, TM_RO = 5, TM_BO = 6,
-    TM_P0H_S2 = 7, TM_P1H_S2 = 8, TM_RO_S2 = 9,
-    TM_RH_S1 = 10, TM_P0H_S1 = 11, TM_P1H_S1 = 12, TM_XO_S1 = 13,
-    TM_XH_J = 14, TM_P0H_J = 15, TM_BO_J = 16, NTM = 17  // _J: point-Jacobi sweeps
+    TM_RH_S1 = 0, TM_P0H_S1, TM_P1H_S1, TM_XO_S1,  // CG sweep 1
+    TM_P0H_S2, TM_P1H_S2, TM_RO_S2,                // CG sweep 2
+    TM_XH_J, TM_P0H_J, TM_BO_J,                    // point-Jacobi sweeps
+    TM_XH_R, TM_P0H_R, TM_P1H_R, TM_BO_R,          // residual sweeps
+    NTM
 };
 
 constexpr int STOP_STALLED = 4;
@@ -1356,12 +1363,11 @@ __device__ __forceinline__ SweepCtx make_ctx(const KParams &P, int b, const DBlo
         C.beta = S.beta;
         C.yout = nullptr;
         C.pout = B.p[S.pcur ^ 1];
-        const CUtensorMap *tm_p = tm + (S.pcur ? TM_P1H : TM_P0H);
         const CUtensorMap *tm_p1 = tm + (S.pcur ? TM_P1H_S1 : TM_P0H_S1);
         if (OPK == OP_RESID) {
-            C.map_a = tm + (S.xin ? TM_P0H : TM_XH);
-            C.map_b = C.pend ? tm_p : nullptr;
-            C.map_c = tm + TM_BO;
+            C.map_a = tm + (S.xin ? TM_P0H_R : TM_XH_R);
+            C.map_b = C.pend ? tm + (S.pcur ? TM_P1H_R : TM_P0H_R) : nullptr;
+            C.map_c = tm + TM_BO_R;
         } else if (OPK == OP_JAC) {  // x_k haloed from buf[xin], b bare; x_{k+1} -> other buffer
             C.map_a = tm + (S.xin ? TM_P0H_J : TM_XH_J);
             C.map_b = nullptr;
@@ -2675,13 +2681,6 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
         B.cta_end = (int)cta_block.size();
         CUtensorMap *m = &maps[(size_t)b * NTM];
         int e = 0;
-        if (!e) e = encode_map(&m[TM_XH], B.x, B, true);
-        if (!e) e = encode_map(&m[TM_P0H], B.p[0], B, true);
-        if (!e) e = encode_map(&m[TM_P1H], B.p[1], B, true);
-        if (!e) e = encode_map(&m[TM_RH], B.r, B, true);
-        if (!e) e = encode_map(&m[TM_XO], B.x, B, false);
-        if (!e) e = encode_map(&m[TM_RO], B.r, B, false);
-        if (!e) e = encode_map(&m[TM_BO], B.b, B, false);
         if (!e) e = encode_map(&m[TM_P0H_S2], B.p[0], B, true, op_zp(OP_S2));
         if (!e) e = encode_map(&m[TM_P1H_S2], B.p[1], B, true, op_zp(OP_S2));
         if (!e) e = encode_map(&m[TM_RO_S2], B.r, B, false, op_zp(OP_S2));
@@ -2692,6 +2691,10 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
         if (!e) e = encode_map(&m[TM_XH_J], B.x, B, true, op_zp(OP_JAC));
         if (!e) e = encode_map(&m[TM_P0H_J], B.p[0], B, true, op_zp(OP_JAC));
         if (!e) e = encode_map(&m[TM_BO_J], B.b, B, false, op_zp(OP_JAC));
+        if (!e) e = encode_map(&m[TM_XH_R], B.x, B, true, op_zp(OP_RESID));
+        if (!e) e = encode_map(&m[TM_P0H_R], B.p[0], B, true, op_zp(OP_RESID));
+        if (!e) e = encode_map(&m[TM_P1H_R], B.p[1], B, true, op_zp(OP_RESID));
+        if (!e) e = encode_map(&m[TM_BO_R], B.b, B, false, op_zp(OP_RESID));
         if (e) {
             delete c;
             return e;
