@@ -35,6 +35,10 @@ for its in (3, 4):  # odd/even: the last launch is S2 after 3 its... read after 
     print(f"nz={nz} its={its} ctas={nctas}")
     for i, nm in enumerate(names):
         print(f"  {nm:11s} min {rel[i].min():7.2f}  med {np.median(rel[i]):7.2f}  max {rel[i].max():7.2f} us")
+    d_fill, d_stream, d_epi = rel[1] - rel[0], rel[2] - rel[1], rel[3] - rel[2]
+    print(f"  per CTA (median): fill {np.median(d_fill):6.2f}  stream {np.median(d_stream):7.2f}  "
+          f"epilogue {np.median(d_epi):6.2f} us;  SM-time busy {(rel[3] - rel[0]).sum():.0f} us "
+          f"over {len(set(t[0].tolist()) and set(sm.tolist()))} SMs x {rel[3].max():.1f} us span")
     tiles_x = (nx + 31) // 32
     ix = np.arange(nctas) % tiles_x
     iy = np.arange(nctas) // tiles_x
