@@ -1,7 +1,8 @@
 """The persistent cooperative CG kernel and the CUDA-graph launch path are
 the same computation: identical tile partials summed in the same order, so
-their results must be bitwise identical — for one block (central reduction
-in the barrier's last arriver) and for many blocks (per-block last tile)."""
+their results must be bitwise identical — for up to four blocks (every CTA
+reduces the tile partials itself after the local-decision barrier) and for
+many blocks (per-block last tile, last-arriver barrier)."""
 
 import os
 
