@@ -44,6 +44,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -276,6 +277,8 @@ struct KParams {
     const CUtensorMap *gmaps;  // per block: V[0..MAXM-1] haloed, [MAXM] = V[0] bare
     int launch_j, launch_i;    // GMRES step served by this launch
     int cta_base, pcta_base;   // first CTA-table entry of this launch (one-block launches)
+    int ntiles;                // tiles of this sweep launch (CTA-table entries from cta_base)
+    unsigned *tile_counter;    // next tile of a sweep launch (rewound by its last CTA)
 };
 
 // ------------------------------------------------------------------ geometry
@@ -533,16 +536,25 @@ __device__ __forceinline__ void cta_sum(double (&acc)[NQ], double *red) {
 // last five with shuffles — the same tree, so the same bits, as a
 // shared-memory tree over 256 threads, with three CTA barriers instead of
 // ten.  All NTH threads call it and get the sum (scratch: 256 doubles).
-template <int NTH>
+// Consumer-warps-only CTA barrier (named barrier 1): in multi-tile sweeps the
+// producer warp is already streaming the next tile meanwhile.
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); }
+
+template <int NTH, bool CONSUMERS = false>
 __device__ double range_sum(const double *part, int begin, int end, double *scratch) {
     static_assert(NTH >= 32, "range_sum needs a full warp");
+    static_assert(!CONSUMERS || NTH == NT, "the consumer-only form runs on the NT consumer threads");
+    auto sync = [] {
+        if (CONSUMERS) consumer_sync();
+        else __syncthreads();
+    };
     const int tid = threadIdx.x;
     for (int l = tid; l < 256; l += NTH) {
         double s = 0.0;
         for (int c = begin + l; c < end; c += 256) s = add(s, __ldcg(part + c));
         scratch[l] = s;
     }
-    __syncthreads();
+    sync();
     if (tid < 32) {
         double v[8];
 #pragma unroll
@@ -556,9 +568,9 @@ __device__ double range_sum(const double *part, int begin, int end, double *scra
         for (int w = 16; w > 0; w >>= 1) t = add(t, __shfl_down_sync(0xffffffffu, t, w));
         if (tid == 0) scratch[0] = t;
     }
-    __syncthreads();
+    sync();
     const double out = scratch[0];
-    __syncthreads();
+    sync();
     return out;
 }
 
@@ -636,8 +648,14 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 // next one reads.  Per point the arithmetic is the same in both directions
 // (the stencil chain is fixed by column order, not by traversal); only the
 // order of a thread's partial sums moves, deterministically per op.
+// round0 < 0: the tile owns the ring (initialised here, one tile per ring).
+// round0 >= 0: the ring is shared by a sequence of tiles (multi-tile CTAs):
+// initialised once, and this tile's stages are rounds round0, round0+1, ...
+// of NS stages each — the producer pads the last round with empty stages, so
+// every tile starts on stage 0 and the compile-time stage schedule below
+// holds.  Returns the rounds the tile used (0 for round0 < 0).
 template <int OP, bool BOX>
-__device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, double (&acc)[NQ]) {
+__device__ int sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, double (&acc)[NQ], int round0 = -1) {
     const DBlock &B = *C.B;
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
@@ -668,22 +686,28 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
     // slot of plane q inside its stage's box (boxes run upwards in z)
     auto slot = [](int qq) { return REV ? ZP - 1 - qq % ZP : qq % ZP; };
 
-    if (tid == 0) {
-        for (int s = 0; s < NS; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], NCW);
+    const bool shared_ring = round0 >= 0;
+    const int nst = (nplanes + ZP - 1) / ZP;   // stages with data
+    const int rounds = (nst + NS - 1) / NS;    // rounds this tile occupies (shared ring)
+    const int k0 = shared_ring ? round0 * NS : 0;  // ring-global index of the tile's stage 0
+    if (!shared_ring) {
+        if (tid == 0) {
+            for (int s = 0; s < NS; ++s) {
+                mbar_init(&full[s], 1);
+                mbar_init(&empty[s], NCW);
+            }
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
     }
-    __syncthreads();
 
     if (warp == NCW) {  // ---------------- TMA producer warp
         if (lane == 0) {
-            const int nst = (nplanes + ZP - 1) / ZP;
             for (int k = 0; k < nst; ++k) {  // stage k holds planes ZP*k .. ZP*k+ZP-1
                 const int s = k % NS;
-                if (k >= NS) mbar_wait(&empty[s], (uint32_t)((k / NS - 1) & 1));
+                const int kg = k0 + k;
+                if (kg >= NS) mbar_wait(&empty[s], (uint32_t)((kg / NS - 1) & 1));
                 const int lz = REV ? lzq0 - ZP * k - (ZP - 1) : lzq0 + ZP * k;  // lowest plane of the box
                 // ZP == 1: the bare operand only for computed planes; ZP > 1: always
                 const bool epi = use_c && (ZP > 1 || (k >= 1 && k <= nplanes - 2));
@@ -695,9 +719,16 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
                 if (use_b) tma_load3(st + BOFF, C.map_b, lx0 - 2, ly0 - 1, lz, &full[s]);
                 if (epi) tma_load3(st + COFF, C.map_c, lx0, ly0, lz, &full[s]);
             }
+            if (shared_ring) {  // pad the last round: empty stages keep every barrier's phase in step
+                for (int k = nst; k < rounds * NS; ++k) {
+                    const int kg = k0 + k;
+                    if (kg >= NS) mbar_wait(&empty[k % NS], (uint32_t)((kg / NS - 1) & 1));
+                    mbar_arrive(&full[k % NS]);
+                }
+            }
         }
         __syncwarp();
-        return;
+        return shared_ring ? rounds : 0;
     }
 
     // ---------------- consumers: thread (tx, ty) owns column x = lx0 + tx of
@@ -742,12 +773,13 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
         row_in[r] = lx < pdx && ly_0 + r < pdy;
     }
 
+    const uint32_t par0 = shared_ring ? (uint32_t)(round0 & 1) : 0u;
     double u_prev[RY], u_cur[RY];
-    mbar_wait(&full[0], 0u);
+    mbar_wait(&full[0], par0);
     if (tid == 0) BS_STAMP(1);
 #pragma unroll
     for (int r = 0; r < RY; ++r) u_prev[r] = uval(smem + slot(0) * (SC * 8), own[r], 0, gjr[r], lzq0);
-    if (ZP == 1) mbar_wait(&full[1], 0u);
+    if (ZP == 1) mbar_wait(&full[1], par0);
     const unsigned char *st1 = smem + (ZP == 1 ? STB : 0) + slot(1) * (SC * 8);
 #pragma unroll
     for (int r = 0; r < RY; ++r) u_cur[r] = uval(st1, own[r], 0, gjr[r], lzq0 + DZ);
@@ -914,7 +946,7 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
         }
     };
     // q = 1 .. nplanes-2 in rounds of NS stages (NS*ZP planes) aligned to stage 0
-    uint32_t par = 0;  // completion parity of the stages of this round
+    uint32_t par = par0;  // completion parity of the stages of this round
     for (int q0 = 0; q0 <= nplanes - 2; q0 += NS * ZP, par ^= 1u) {
 #pragma unroll
         for (int u = 0; u < NS * ZP; ++u) {
@@ -926,6 +958,21 @@ __device__ void sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, dou
         }
     }
     if (tid == 0) BS_STAMP(2);
+    if (shared_ring) {
+        // release the stages the plane loop did not: the one holding only the
+        // last (never computed) plane, and the padding — after waiting for
+        // each, so no barrier can run a phase ahead of the producer's wait
+        const int released = (nplanes - 1 - ZP) / ZP + 1;
+        const uint32_t parl = (uint32_t)((round0 + rounds - 1) & 1);
+        __syncwarp();
+        for (int k = released; k < rounds * NS; ++k) {
+            mbar_wait(&full[k % NS], parl);  // all in the tile's last round
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[k % NS]);
+        }
+        return rounds;
+    }
+    return 0;
 }
 
 // ------------------------------------------------------------------ scalars
@@ -1298,17 +1345,12 @@ __device__ void finish_block(const KParams &P, int b, int ph, bool served, doubl
     }
 }
 
-template <int NTH, int OPK, bool POINT = false>
-__device__ void finish(const KParams &P, int b, int ph, bool served, double (&acc)[NQ], int nq,
-                       unsigned char *smem, int vcta) {
-    finish_block<NTH, POINT>(P, b, ph, served, acc, nq, smem, vcta);
-    // Pointwise (GMRES) passes are host-sequenced and never end a loop: the
-    // launch-level bookkeeping (one atomic per CTA on a single counter) is
-    // only needed by sweeps.
-    if (POINT) return;
-    const int nctas = POINT ? P.npctas : P.nctas;
+// Launch-level epilogue of a sweep: every CTA counts into the launch; the
+// launch's last CTA publishes the loop conditions and rewinds the tile
+// counter (flag: one int of shared memory).
+template <int OPK>
+__device__ void finish_launch(const KParams &P, int *flag) {
     const int tid = threadIdx.x;
-    int *flag = reinterpret_cast<int *>(reinterpret_cast<double *>(smem) + NQ * (NTH / 32) + 256);
     if (tid == 0) {
         __threadfence();
         const unsigned prev = atomicAdd(P.launch_counter, 1u);
@@ -1343,10 +1385,65 @@ __device__ void finish(const KParams &P, int b, int ph, bool served, double (&ac
     if (OPK == OP_RESID && P.use_graph) P.ctl->resid_runs += 1;
     *P.n_active = active;
     *P.launch_counter = 0u;
+    *P.tile_counter = 0u;
     if (P.use_graph) {
         cudaGraphSetConditional(P.h_loop, active ? 1u : 0u);
         if (OPK == OP_S2) cudaGraphSetConditional(P.h_verify, verify ? 1u : 0u);
     }
+}
+
+// Tile epilogue of a multi-tile sweep, on the consumer warps only (the
+// producer is streaming the next tile): the tile partial with cta_sum<NTHR>'s
+// exact order (warps 0..NCW-1, then the producer warp's +0.0), and the
+// block's last tile reduces the block in tile order and advances it — the
+// same numbers as finish_block.
+__device__ void tile_epilogue(const KParams &P, int b, int ph, double (&acc)[NQ], int nq, int cta, double *red,
+                              double *scratch, int *flag) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const double v = warp_sum(acc[q]);
+        if (lane == 0) red[q * NCW + warp] = v;
+    }
+    consumer_sync();
+    const DBlock &B = P.blocks[b];
+    if (tid == 0) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            double sum = red[q * NCW];
+            for (int w = 1; w < NCW; ++w) sum = add(sum, red[q * NCW + w]);
+            P.partials[(size_t)q * P.nctas + cta] = add(sum, 0.0);
+        }
+        __threadfence();
+        const unsigned prev = atomicAdd(&P.blk_counter[b], 1u);
+        *flag = (prev == (unsigned)(B.cta_end - B.cta_begin) - 1u);
+    }
+    consumer_sync();
+    if (*flag) {  // last tile of block b
+        __threadfence();
+        double q[NQ];
+        for (int i = 0; i < NQ; ++i)
+            q[i] = i < nq ? range_sum<NT, true>(P.partials + (size_t)i * P.nctas, B.cta_begin, B.cta_end, scratch) : 0.0;
+        if (tid == 0) {
+            DState Sn = ld_state(P.states + b);
+            transition(B, Sn, P.gstates ? P.gstates + b : nullptr, ph, q);
+            P.states[b] = Sn;
+            P.blk_counter[b] = 0u;
+            __threadfence();
+        }
+    }
+    consumer_sync();  // red / flag are reused by the next tile
+}
+
+template <int NTH, int OPK, bool POINT = false>
+__device__ void finish(const KParams &P, int b, int ph, bool served, double (&acc)[NQ], int nq,
+                       unsigned char *smem, int vcta) {
+    finish_block<NTH, POINT>(P, b, ph, served, acc, nq, smem, vcta);
+    // Pointwise (GMRES) passes are host-sequenced and never end a loop: the
+    // launch-level bookkeeping (one atomic per CTA on a single counter) is
+    // only needed by sweeps.
+    if (POINT) return;
+    finish_launch<OPK>(P, reinterpret_cast<int *>(reinterpret_cast<double *>(smem) + NQ * (NTH / 32) + 256));
 }
 
 // One sweep over every block whose phase this kernel serves.
@@ -1397,31 +1494,76 @@ __host__ __device__ constexpr int op_nq() { return OPK == OP_RESID ? NQ : (OPK =
 template <int OPK, bool BOX>
 __global__ void __launch_bounds__(NTHR, BS_MINBLOCKS) k_sweep(const KParams P) {
     extern __shared__ __align__(1024) unsigned char smem[];
-    // reversed sweeps also take the tiles in reverse order: with more tiles
-    // than resident CTAs, the last wave of the previous sweep is the first
-    // wave of this one (L2 reuse across the sweep boundary)
-    const int cta = P.cta_base + (op_rev(OPK) ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x);
-    const int b = P.cta_block[cta];
-    const DBlock &B = P.blocks[b];
-    const DState S = P.states[b];
-    const int ph = S.phase;
-    const bool served = serves<OPK, -1>(S, P);
-    double acc[NQ] = {0.0, 0.0, 0.0, 0.0};
-    if (threadIdx.x == 0) BS_STAMP(0);
+    __shared__ double s_red[NQ * NCW];
+    __shared__ double s_scratch[256];
+    __shared__ int s_flag, s_tile[2];
+    __shared__ __align__(8) uint64_t s_tfull[2], s_tempty[2];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) BS_STAMP(0);
 #ifdef BS_TRACE
-    if (threadIdx.x == 0 && blockIdx.x < TRACE_CTAS) {
+    if (tid == 0 && blockIdx.x < TRACE_CTAS) {
         unsigned sm;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
         g_trace[4][blockIdx.x] = sm;
     }
 #endif
-    if (served) {
-        const SweepCtx C = make_ctx<OPK>(P, b, B, S);
-        sweep_tile<OPK, BOX>(C, cta - B.cta_begin, smem, acc);
-        __syncthreads();  // all planes consumed: the stage ring is free for reuse
+    // Each CTA streams tiles back to back through ONE ring: the producer runs
+    // into the next tile while the consumers finish the last planes and the
+    // epilogue of this one (no per-tile ring fill or CTA launch).  Tiles are
+    // handed out dynamically (one counter per launch), so CTAs on busier SMs
+    // simply take fewer; the producer lane fetches the next index and passes
+    // it to the consumer warps through a two-slot mailbox.  Reversed sweeps
+    // take the tiles in reverse order (the previous sweep's last tiles are
+    // still in L2).  Results do not depend on the assignment: partials are
+    // per tile.
+    if (tid == 0) {
+        uint64_t *full = reinterpret_cast<uint64_t *>(smem + op_stages(OPK) * op_stage_bytes(OPK));
+        for (int s = 0; s < op_stages(OPK); ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&full[op_stages(OPK) + s], NCW);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&s_tfull[s], 1);
+            mbar_init(&s_tempty[s], NCW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
-    finish<NTHR, OPK>(P, b, ph, served, acc, op_nq<OPK>(), smem, cta);
-    if (threadIdx.x == 0) BS_STAMP(3);
+    __syncthreads();
+    const int T = P.ntiles;
+    int round = 0;
+    for (int n = 0;; ++n) {
+        const int slot = n & 1;
+        const uint32_t ph = (uint32_t)((n >> 1) & 1);
+        int i = 0;
+        if (warp == NCW) {
+            if (lane == 0) {
+                if (n >= 2) mbar_wait(&s_tempty[slot], ph ^ 1u);  // the slot's previous index was read
+                i = (int)atomicAdd(P.tile_counter, 1u);
+                s_tile[slot] = i;
+                mbar_arrive(&s_tfull[slot]);
+            }
+            i = __shfl_sync(0xffffffffu, i, 0);
+        } else {
+            mbar_wait(&s_tfull[slot], ph);
+            i = s_tile[slot];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_tempty[slot]);
+        }
+        if (i >= T) break;
+        const int cta = P.cta_base + (op_rev(OPK) ? T - 1 - i : i);
+        const int b = P.cta_block[cta];
+        const DBlock &B = P.blocks[b];
+        const DState S = P.states[b];  // constant until every tile of b is done
+        if (!serves<OPK, -1>(S, P)) continue;
+        double acc[NQ] = {0.0, 0.0, 0.0, 0.0};
+        const SweepCtx C = make_ctx<OPK>(P, b, B, S);
+        round += sweep_tile<OPK, BOX>(C, cta - B.cta_begin, smem, acc, round);
+        if (tid < NT) tile_epilogue(P, b, S.phase, acc, op_nq<OPK>(), cta, s_red, s_scratch, &s_flag);
+    }
+    __syncthreads();
+    finish_launch<OPK>(P, &s_flag);
+    if (tid == 0) BS_STAMP(3);
 }
 
 // ---- persistent CG: the whole solve in one cooperative launch.  Each CTA
@@ -2329,6 +2471,8 @@ struct bs_ctx {
     double *dpartials = nullptr;
     unsigned *dblk_counter = nullptr;
     unsigned *dlaunch_counter = nullptr;
+    unsigned *dtile_counter = nullptr;     // dynamic tile hand-out of sweep launches
+    std::map<const void *, int> sweep_cap;  // co-resident CTAs of each sweep kernel
     int *dnactive = nullptr;
     Control *dctl = nullptr;
     int *dactive = nullptr;
@@ -2400,6 +2544,7 @@ KParams make_params(bs_ctx *c, bool graph, cudaGraphConditionalHandle hl = 0,
     P.partials = c->dpartials;
     P.blk_counter = c->dblk_counter;
     P.launch_counter = c->dlaunch_counter;
+    P.tile_counter = c->dtile_counter;
     P.n_active = c->dnactive;
     P.ctl = c->dctl;
     P.h_loop = hl;
@@ -2411,16 +2556,46 @@ KParams make_params(bs_ctx *c, bool graph, cudaGraphConditionalHandle hl = 0,
     P.launch_i = 0;
     P.cta_base = 0;
     P.pcta_base = 0;
+    P.ntiles = c->nctas;
     return P;
+}
+
+// Grid of a sweep over `ntiles` tiles: one CTA per co-resident slot
+// (occupancy x SMs), each streaming tiles until the launch's counter runs
+// out.  BS_SWEEP_TILES=1 launches one CTA per tile instead (A/B switch).
+int sweep_ctas(bs_ctx *c, const void *fn, int smem, int ntiles) {
+    static const int one_per_cta = [] {
+        const char *e = std::getenv("BS_SWEEP_TILES");
+        return e && std::atoi(e) == 1;
+    }();
+    if (one_per_cta || ntiles <= 0) return std::max(ntiles, 1);
+    auto it = c->sweep_cap.find(fn);
+    if (it == c->sweep_cap.end()) {
+        int per_sm = 0, sms = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NTHR, smem) != cudaSuccess ||
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device) != cudaSuccess || per_sm < 1) {
+            cudaGetLastError();
+            per_sm = 0;
+        }
+        it = c->sweep_cap.emplace(fn, per_sm * sms).first;
+    }
+    return it->second > 0 ? std::min(ntiles, it->second) : ntiles;
 }
 
 // Grid of a sweep (pointwise) launch over every block (blk < 0) or only
 // block blk's CTA range, with the matching CTA-table base in P.
-int sweep_grid(bs_ctx *c, KParams &P, int blk) {
-    if (blk < 0) return c->nctas;
-    const DBlock &B = c->hblocks[blk];
-    P.cta_base = B.cta_begin;
-    return B.cta_end - B.cta_begin;
+template <int OPK>
+void *sweep_fn(bool box) {
+    return box ? (void *)k_sweep<OPK, true> : (void *)k_sweep<OPK, false>;
+}
+
+int sweep_grid(bs_ctx *c, KParams &P, int blk, const void *fn, int smem) {
+    if (blk >= 0) {
+        const DBlock &B = c->hblocks[blk];
+        P.cta_base = B.cta_begin;
+        P.ntiles = B.cta_end - B.cta_begin;
+    }
+    return sweep_ctas(c, fn, smem, P.ntiles);
 }
 
 int point_grid(bs_ctx *c, KParams &P, int blk) {
@@ -2447,7 +2622,7 @@ void launch_point(bs_ctx *c, cudaStream_t st, int j, int i, int blk = -1) {
 void launch_gspmv(bs_ctx *c, cudaStream_t st, int j, int blk = -1) {
     KParams P = make_params(c, false);
     P.launch_j = j;
-    const int grid = sweep_grid(c, P, blk);
+    const int grid = sweep_grid(c, P, blk, sweep_fn<OP_GSPMV>(c->box), op_smem(OP_GSPMV));
     if (c->box)
         k_sweep<OP_GSPMV, true><<<grid, NTHR, op_smem(OP_GSPMV), st>>>(P);
     else
@@ -2455,15 +2630,11 @@ void launch_gspmv(bs_ctx *c, cudaStream_t st, int j, int blk = -1) {
     ++g_launches;
 }
 
-template <int OPK>
-void *sweep_fn(bool box) {
-    return box ? (void *)k_sweep<OPK, true> : (void *)k_sweep<OPK, false>;
-}
 
 template <int OPK>
 void launch_sweep(bs_ctx *c, cudaStream_t st, int slot, int blk = -1) {
     KParams P = make_params(c, false);
-    const int grid = sweep_grid(c, P, blk);
+    const int grid = sweep_grid(c, P, blk, sweep_fn<OPK>(c->box), op_smem(OPK));
     if (c->timing && slot >= 0) cudaEventRecord(c->ev[2 * slot], st);
     if (c->box)
         k_sweep<OPK, true><<<grid, NTHR, op_smem(OPK), st>>>(P);
@@ -2498,7 +2669,7 @@ int add_sweep_node(bs_ctx *c, cudaGraph_t g, cudaGraphNode_t *node, const cudaGr
     void *args[] = {&P};
     cudaKernelNodeParams kp = {};
     kp.func = sweep_fn<OPK>(c->box);
-    kp.gridDim = dim3(c->nctas);
+    kp.gridDim = dim3(sweep_ctas(c, kp.func, op_smem(OPK), P.ntiles));
     kp.blockDim = dim3(NTHR);
     kp.sharedMemBytes = op_smem(OPK);
     kp.kernelParams = args;
@@ -2747,6 +2918,7 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
         e = cudaMemcpy(c->dpcta_block, pcta_block.data(), sizeof(int) * c->npctas, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&c->dblk_counter, sizeof(unsigned) * nblocks);
     if (e == cudaSuccess) e = cudaMalloc(&c->dlaunch_counter, sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMalloc(&c->dtile_counter, sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMalloc(&c->dnactive, sizeof(int));
     if (e == cudaSuccess) e = cudaMalloc(&c->dctl, sizeof(Control));
     if (e == cudaSuccess) e = cudaMalloc(&c->dactive, sizeof(int) * nblocks);
@@ -2765,6 +2937,7 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
     if (e == cudaSuccess) e = cudaMemset(c->dstates, 0, sizeof(DState) * nblocks);
     if (e == cudaSuccess) e = cudaMemset(c->dblk_counter, 0, sizeof(unsigned) * nblocks);
     if (e == cudaSuccess) e = cudaMemset(c->dlaunch_counter, 0, sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMemset(c->dtile_counter, 0, sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemset(c->dnactive, 0, sizeof(int));
     if (e == cudaSuccess) e = cudaMemset(c->dctl, 0, sizeof(Control));
     {
@@ -2805,6 +2978,7 @@ int bs_ctx_destroy(bs_ctx *c) {
     cudaFree(c->dpartials);
     cudaFree(c->dblk_counter);
     cudaFree(c->dlaunch_counter);
+    cudaFree(c->dtile_counter);
     cudaFree(c->dnactive);
     cudaFree(c->dctl);
     cudaFree(c->dactive);
