@@ -2577,6 +2577,8 @@ int sweep_ctas(bs_ctx *c, const void *fn, int smem, int ntiles) {
             cudaGetLastError();
             per_sm = 0;
         }
+        if (const char *e = std::getenv("BS_SWEEP_PER_SM"))  // A/B: fewer resident sweep CTAs per SM
+            per_sm = std::min(per_sm, std::max(1, std::atoi(e)));
         it = c->sweep_cap.emplace(fn, per_sm * sms).first;
     }
     return it->second > 0 ? std::min(ntiles, it->second) : ntiles;
