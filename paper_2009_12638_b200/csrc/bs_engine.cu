@@ -46,6 +46,7 @@
 #include <cstring>
 #include <map>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 namespace {
@@ -805,14 +806,19 @@ __device__ int sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, doub
     // plane q: stage s, slot sl; the next plane: stage sn, slot sln, waited
     // for only when it opens a new stage; the stage is released after its
     // last plane.
-    auto single_step = [&](int q, int s, int sl, int sn, int sln, bool wait_next, uint32_t par_n, bool release) {
+    // FC = std::true_type: a fast round — box region, full tile, and no plane
+    // of the round without its z-1 neighbour — so no presence, row or region
+    // test is evaluated per plane (only the uniform plane-range guard).
+    auto single_step = [&](auto FC, int q, int s, int sl, int sn, int sln, bool wait_next, uint32_t par_n,
+                           bool release) {
+        constexpr bool FR = decltype(FC)::value;
         const int lz = lzq0 + DZ * q;
         const unsigned char *st = smem + s * STB + sl * (SC * 8);
         const double *cst = reinterpret_cast<const double *>(smem + s * STB + COFF + sl * SEG_O);
         // Phase A, before plane q+1 is waited for: the in-plane neighbours and,
         // on the interior fast path, the reduceat chain up to its last term
         // (z+1 enters second to last), so the wait overlaps the DP latency.
-        if (!BOX && BS_EASY) {
+        if (!FR && !BOX && BS_EASY) {
             const int gk = B.plo[2] + lz;
             bool e = true;
 #pragma unroll
@@ -825,7 +831,7 @@ __device__ int sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, doub
         // inside the chain leaves every partial sum unchanged.  So only the
         // z-1 presence selects it — tiles on the low x / y faces stream as
         // fast as interior ones (they used to finish each sweep last).
-        const bool fast = easy && lz > 0;
+        const bool fast = FR || (easy && lz > 0);
         double xm_[RY], xp_[RY], ym_[RY], yp_[RY], pre_[RY];
 #pragma unroll
         for (int r = 0; r < RY; ++r) {
@@ -846,7 +852,8 @@ __device__ int sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, doub
         for (int r = 0; r < RY; ++r) {
             const int ly = ly_0 + r;
             const int gj = gjr[r];
-            const bool here = (BOX || easy) ? row_in[r] : (row_in[r] && in_region(B, gi, gj, B.plo[2] + lz));
+            const bool here =
+                FR || ((BOX || easy) ? row_in[r] : (row_in[r] && in_region(B, gi, gj, B.plo[2] + lz)));
             if (!here) continue;
             const double xm = xm_[r], xp = xp_[r], ym = ym_[r], yp = yp_[r];
             const double zm = REV ? u_next[r] : u_prev[r], zp = REV ? u_prev[r] : u_next[r];
@@ -947,14 +954,44 @@ __device__ int sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, doub
     };
     // q = 1 .. nplanes-2 in rounds of NS stages (NS*ZP planes) aligned to stage 0
     uint32_t par = par0;  // completion parity of the stages of this round
+    const bool tile_full = lx0 + TX <= pdx && ly0 + TY <= pdy;
+    // the computed plane with lz == 0 (no z-1 neighbour), if the tile has one
+    const int q_zero = lz0 == 0 ? (REV ? lz1 : 1) : -1;
     for (int q0 = 0; q0 <= nplanes - 2; q0 += NS * ZP, par ^= 1u) {
+        constexpr int QR = NS * ZP;  // planes per round
+        // measured per op: the CG sweeps take both fast variants; the residual,
+        // Jacobi and GMRES sweeps only the unguarded one (a third unrolled
+        // copy makes them spill); the standalone SpMV none (its general path
+        // is already short)
+        constexpr bool FAST_ROUNDS = BOX && OP != OP_APPLY;
+        constexpr bool GUARDED_FAST = OP == OP_S1 || OP == OP_S2;
+        bool fround = false;
+        if constexpr (FAST_ROUNDS) fround = tile_full && !(q_zero >= q0 && q_zero < q0 + QR);
+        if (fround && q0 >= 1 && q0 + QR - 1 <= nplanes - 2) {  // interior round: no guards at all
 #pragma unroll
-        for (int u = 0; u < NS * ZP; ++u) {
-            const int q = q0 + u;
-            const int un = u + 1;
-            if (q >= 1 && q <= nplanes - 2)
-                single_step(q, u / ZP, slot(u), (un / ZP) % NS, slot(un), un % ZP == 0,
-                            un == NS * ZP ? par ^ 1u : par, u % ZP == ZP - 1);
+            for (int u = 0; u < QR; ++u) {
+                const int un = u + 1;
+                single_step(std::true_type{}, q0 + u, u / ZP, slot(u), (un / ZP) % NS, slot(un), un % ZP == 0,
+                            un == QR ? par ^ 1u : par, u % ZP == ZP - 1);
+            }
+        } else if (GUARDED_FAST && fround) {  // first / last round: the uniform plane-range guard only
+#pragma unroll
+            for (int u = 0; u < QR; ++u) {
+                const int q = q0 + u;
+                const int un = u + 1;
+                if (q >= 1 && q <= nplanes - 2)
+                    single_step(std::true_type{}, q, u / ZP, slot(u), (un / ZP) % NS, slot(un), un % ZP == 0,
+                                un == QR ? par ^ 1u : par, u % ZP == ZP - 1);
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < QR; ++u) {
+                const int q = q0 + u;
+                const int un = u + 1;
+                if (q >= 1 && q <= nplanes - 2)
+                    single_step(std::false_type{}, q, u / ZP, slot(u), (un / ZP) % NS, slot(un), un % ZP == 0,
+                                un == QR ? par ^ 1u : par, u % ZP == ZP - 1);
+            }
         }
     }
     if (tid == 0) BS_STAMP(2);
