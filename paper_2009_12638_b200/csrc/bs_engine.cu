@@ -351,13 +351,6 @@ __device__ __forceinline__ double stencil7(double zm, double ym, double xm, doub
     return add(t3, add(add(-xp, -yp), -zp));
 }
 
-// Interior row (all seven terms present): the reduceat order without any
-// presence logic.  Callers take this path only when it is warp-uniform.
-__device__ __forceinline__ double stencil7_interior(double zm, double ym, double xm, double c, double xp, double yp,
-                                                    double zp) {
-    return add(-zm, add(add(add(add(add(-ym, -xm), mul(6.0, c)), -xp), -yp), -zp));
-}
-
 // One row of the operator without its diagonal (linalg.py:144-159) under the
 // same reduceat rule: present terms [-zm, -ym, -xm, -xp, -yp, -zp], the first
 // present one plus the left-to-right sum of those after it (absent ones are
@@ -860,7 +853,7 @@ __device__ int sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, doub
             const long long sxr = sx + (long long)r * pitch;
             double au, od = 0.0;
             if (fast) {
-                // = stencil7_interior(zm, ym, xm, u_cur, xp, yp, zp), same association
+                // = stencil7(zm, ym, xm, u_cur, xp, yp, zp, true, true, true), same association
                 au = REV ? add(-zm, pre_[r]) : add(-zm, add(pre_[r], -zp));
                 if (OP == OP_JAC) od = offdiag6(zm, ym, xm, xp, yp, zp, true, true, true, true, true, true);
             } else {
