@@ -146,6 +146,14 @@ __host__ __device__ constexpr bool op_has_b(int op) { return op == OP_RESID || o
 #ifndef BS_REV_PASSES
 #define BS_REV_PASSES 1
 #endif
+// Cache policy of the GMRES pointwise passes.  1: the streams the next pass
+// re-reads (w, v_i, the fresh v_{j+1}) are loaded/stored with the default L2
+// policy and the one it does not (v_{i-1}, v_j in FINAL, NORM's source) is
+// marked evict-first, so with BS_REV_PASSES the next pass starts on L2 hits.
+// 0: every w access streaming (evict-first), V through the read-only path.
+#ifndef BS_MGS_HINT
+#define BS_MGS_HINT 1
+#endif
 #ifndef BS_REV_S2
 #define BS_REV_S2 1
 #endif
@@ -1954,8 +1962,10 @@ __global__ void __launch_bounds__(NPT) k_point(const KParams P) {
 #pragma unroll
                 for (int u = 0; u < PB; ++u) {
                     const long long e2 = pair0 + (long long)(it0 + u) * NPT;
-                    if (full_chunk || e2 < npairs)
-                        __stcs(vj + e2, make_double2(__ddiv_rn(v[u].x, nrm), __ddiv_rn(v[u].y, nrm)));
+                    if (!(full_chunk || e2 < npairs)) continue;
+                    const double2 q = make_double2(__ddiv_rn(v[u].x, nrm), __ddiv_rn(v[u].y, nrm));
+                    if (BS_MGS_HINT) __stcg(vj + e2, q);
+                    else __stcs(vj + e2, q);
                 }
             }
         } else if (PKK == PK_MGS || PKK == PK_FINAL) {
@@ -1971,9 +1981,15 @@ __global__ void __launch_bounds__(NPT) k_point(const KParams P) {
                 for (int u = 0; u < PB; ++u) {
                     const long long e2 = pair0 + (long long)(it0 + u) * NPT;
                     if (full_chunk || e2 < npairs) {
-                        w[u] = __ldcs(w2 + e2);
-                        a[u] = __ldg(va + e2);
-                        if (PKK == PK_MGS) c[u] = __ldg(vb + e2);
+                        if (BS_MGS_HINT) {
+                            w[u] = __ldcg(w2 + e2);
+                            a[u] = __ldcs(va + e2);
+                            if (PKK == PK_MGS) c[u] = __ldcg(vb + e2);
+                        } else {
+                            w[u] = __ldcs(w2 + e2);
+                            a[u] = __ldg(va + e2);
+                            if (PKK == PK_MGS) c[u] = __ldg(vb + e2);
+                        }
                     }
                 }
 #pragma unroll
@@ -1981,7 +1997,8 @@ __global__ void __launch_bounds__(NPT) k_point(const KParams P) {
                     const long long e2 = pair0 + (long long)(it0 + u) * NPT;
                     if (!(full_chunk || e2 < npairs)) continue;
                     const double w0 = sub(w[u].x, mul(h, a[u].x)), w1 = sub(w[u].y, mul(h, a[u].y));
-                    __stcs(w2 + e2, make_double2(w0, w1));
+                    if (BS_MGS_HINT) __stcg(w2 + e2, make_double2(w0, w1));
+                    else __stcs(w2 + e2, make_double2(w0, w1));
                     if (PKK == PK_MGS) {
                         acc[0] = add(acc[0], mul(c[u].x, w0));
                         acc[0] = add(acc[0], mul(c[u].y, w1));
