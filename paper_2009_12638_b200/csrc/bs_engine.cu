@@ -150,9 +150,16 @@ __host__ __device__ constexpr bool op_has_b(int op) { return op == OP_RESID || o
 // re-reads (w, v_i, the fresh v_{j+1}) are loaded/stored with the default L2
 // policy and the one it does not (v_{i-1}, v_j in FINAL, NORM's source) is
 // marked evict-first, so with BS_REV_PASSES the next pass starts on L2 hits.
+// 2 (default): as 1, but in a launch over one block, MGS/FINAL CTAs among
+// the last BS_MGS_KEEP of the launch (the chunks the next, reversed pass reads first; 256 chunks = 64 MB
+// of w + v_i) access w and v_i with an L2 evict_last policy and every other
+// MGS/FINAL access is evict_first (profiles/r01_ab_mgs_cache_hint.log).
 // 0: every w access streaming (evict-first), V through the read-only path.
 #ifndef BS_MGS_HINT
-#define BS_MGS_HINT 1
+#define BS_MGS_HINT 2
+#endif
+#ifndef BS_MGS_KEEP
+#define BS_MGS_KEEP 256  // BS_MGS_HINT 2: trailing chunks per pass kept evict_last
 #endif
 #ifndef BS_REV_S2
 #define BS_REV_S2 1
@@ -341,6 +348,28 @@ __device__ __forceinline__ double ghost_at(const DBlock &B, int i, int j, int k,
 // ------------------------------------------------------------------ arithmetic
 
 __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+
+template <int V>
+struct IntC {
+    static constexpr int value = V;
+};
+
+// L2 cache-policy loads/stores (BS_MGS_HINT 2): evict_last for the data the
+// next GMRES pass re-reads first, evict_first for the rest.
+__device__ __forceinline__ uint64_t l2_policy(bool keep) {
+    uint64_t pol;
+    if (keep) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ double2 ld_pol(const double2 *p, uint64_t pol) {
+    double2 v;
+    asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st_pol(double2 *p, double2 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+}
 __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
 
@@ -1975,39 +2004,60 @@ __global__ void __launch_bounds__(NPT) k_point(const KParams P) {
             const double2 *va = reinterpret_cast<const double2 *>(V + (PKK == PK_MGS ? i - 1 : j) * vs);
             const double2 *vb = reinterpret_cast<const double2 *>(V + i * vs);
             double2 *w2 = reinterpret_cast<double2 *>(W);
-            for (int it0 = 0; it0 < PITER; it0 += PB) {
-                double2 w[PB], a[PB], c[PB];
+            // evict_last tail only when the launch covers one block: in an
+            // all-block launch the time-last CTAs may belong to finished blocks
+            const bool one_block = P.pcta_block[P.pcta_base] == P.pcta_block[P.pcta_base + (int)gridDim.x - 1];
+            const bool pol2 = BS_MGS_HINT == 2 && one_block;
+            uint64_t pol_keep = 0, pol_drop = 0;
+            if (pol2) {
+                pol_keep = l2_policy((int)blockIdx.x >= (int)gridDim.x - BS_MGS_KEEP);
+                pol_drop = l2_policy(false);
+            }
+            // one loop per cache mode (a run-time mode test inside the batch
+            // loop costs the batching its memory-level parallelism)
+            auto pass = [&](auto mode_c) {
+                constexpr int MODE = decltype(mode_c)::value;
+                for (int it0 = 0; it0 < PITER; it0 += PB) {
+                    double2 w[PB], a[PB], c[PB];
 #pragma unroll
-                for (int u = 0; u < PB; ++u) {
-                    const long long e2 = pair0 + (long long)(it0 + u) * NPT;
-                    if (full_chunk || e2 < npairs) {
-                        if (BS_MGS_HINT) {
-                            w[u] = __ldcg(w2 + e2);
-                            a[u] = __ldcs(va + e2);
-                            if (PKK == PK_MGS) c[u] = __ldcg(vb + e2);
+                    for (int u = 0; u < PB; ++u) {
+                        const long long e2 = pair0 + (long long)(it0 + u) * NPT;
+                        if (full_chunk || e2 < npairs) {
+                            if (MODE == 2) {
+                                w[u] = ld_pol(w2 + e2, pol_keep);
+                                a[u] = ld_pol(va + e2, pol_drop);
+                                if (PKK == PK_MGS) c[u] = ld_pol(vb + e2, pol_keep);
+                            } else if (MODE == 1) {
+                                w[u] = __ldcg(w2 + e2);
+                                a[u] = __ldcs(va + e2);
+                                if (PKK == PK_MGS) c[u] = __ldcg(vb + e2);
+                            } else {
+                                w[u] = __ldcs(w2 + e2);
+                                a[u] = __ldg(va + e2);
+                                if (PKK == PK_MGS) c[u] = __ldg(vb + e2);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < PB; ++u) {
+                        const long long e2 = pair0 + (long long)(it0 + u) * NPT;
+                        if (!(full_chunk || e2 < npairs)) continue;
+                        const double w0 = sub(w[u].x, mul(h, a[u].x)), w1 = sub(w[u].y, mul(h, a[u].y));
+                        if (MODE == 2) st_pol(w2 + e2, make_double2(w0, w1), pol_keep);
+                        else if (MODE == 1) __stcg(w2 + e2, make_double2(w0, w1));
+                        else __stcs(w2 + e2, make_double2(w0, w1));
+                        if (PKK == PK_MGS) {
+                            acc[0] = add(acc[0], mul(c[u].x, w0));
+                            acc[0] = add(acc[0], mul(c[u].y, w1));
                         } else {
-                            w[u] = __ldcs(w2 + e2);
-                            a[u] = __ldg(va + e2);
-                            if (PKK == PK_MGS) c[u] = __ldg(vb + e2);
+                            acc[0] = add(acc[0], mul(w0, w0));
+                            acc[0] = add(acc[0], mul(w1, w1));
                         }
                     }
                 }
-#pragma unroll
-                for (int u = 0; u < PB; ++u) {
-                    const long long e2 = pair0 + (long long)(it0 + u) * NPT;
-                    if (!(full_chunk || e2 < npairs)) continue;
-                    const double w0 = sub(w[u].x, mul(h, a[u].x)), w1 = sub(w[u].y, mul(h, a[u].y));
-                    if (BS_MGS_HINT) __stcg(w2 + e2, make_double2(w0, w1));
-                    else __stcs(w2 + e2, make_double2(w0, w1));
-                    if (PKK == PK_MGS) {
-                        acc[0] = add(acc[0], mul(c[u].x, w0));
-                        acc[0] = add(acc[0], mul(c[u].y, w1));
-                    } else {
-                        acc[0] = add(acc[0], mul(w0, w0));
-                        acc[0] = add(acc[0], mul(w1, w1));
-                    }
-                }
-            }
+            };
+            if (pol2) pass(IntC<2>{});
+            else pass(IntC<(BS_MGS_HINT ? 1 : 0)>{});
         } else {
             const int pitch = B.pitch, pdx = B.pdim[0], pdy = B.pdim[1];
             for (int it = 0; it < PCHUNK / NPT; ++it) {
