@@ -2069,8 +2069,19 @@ __global__ void __launch_bounds__(NPT) k_point(const KParams P) {
                 const int gi = B.plo[0] + lx, gj = B.plo[1] + (int)(t2 % pdy), gk = B.plo[2] + (int)(t2 / pdy);
                 if (PKK == PK_FORM) {  // x = x + V[:j+1]^T y (inner_solvers.py:173-175)
                     if (!BOX && !in_region(B, gi, gj, gk)) continue;
+                    // same left-to-right sum; the basis loads are issued 8 at a
+                    // time ahead of their adds (one load in flight per thread
+                    // held this pass at ~45% of HBM bandwidth)
                     double acc_t = mul(V[e], G.y[0]);
-                    for (int k = 1; k <= j; ++k) acc_t = add(acc_t, mul(V[k * vs + e], G.y[k]));
+                    int k = 1;
+                    for (; k + 8 <= j + 1; k += 8) {
+                        double v8[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) v8[u] = __ldcs(V + (k + u) * vs + e);
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) acc_t = add(acc_t, mul(v8[u], G.y[k + u]));
+                    }
+                    for (; k <= j; ++k) acc_t = add(acc_t, mul(V[k * vs + e], G.y[k]));
                     B.x[e] = add(B.x[e], acc_t);
                 } else {  // PK_OWNRES
                     // Local residual with owner-canonical values (multisplit.py:372-396):
