@@ -257,6 +257,110 @@ def stencil_apply(u3: np.ndarray, region: np.ndarray | None = None) -> np.ndarra
     return np.where(region, y, 0.0)
 
 
+def stencil_apply_box(u3: np.ndarray) -> np.ndarray:
+    """``stencil_apply(u3)`` on a whole box, bit for bit, in a few in-place
+    passes (the full-size fixtures at 512^3 need it to be fast).
+
+    Every row with its z-1 neighbour present evaluates ``t0 + chain(1)``
+    where ``chain(1) = ((((t1 + t2) + t3) + t4) + t5) + t6`` (absent terms are
+    exact signed zeros, which leave a partial sum unchanged, so they are
+    simply skipped); ``t0 + s`` is formed as ``s - u(z-1)`` (IEEE addition
+    commutes, and ``a - b`` is ``a + (-b)``).  Plane 0 (no z-1 neighbour)
+    takes the general ``stencil_apply`` on its two-plane slice.
+    """
+    u = np.asarray(u3, dtype=np.float64)
+    nz = u.shape[0]
+    s = np.empty_like(u)
+    s[:, 0, :] = -0.0
+    np.negative(u[:, :-1, :], out=s[:, 1:, :])  # t1 = -u(y-1)
+    s[:, :, 1:] -= u[:, :, :-1]  # + t2
+    s += 6.0 * u  # + t3
+    s[:, :, :-1] -= u[:, :, 1:]  # + t4
+    s[:, :-1, :] -= u[:, 1:, :]  # + t5
+    s[:-1] -= u[1:]  # + t6
+    s[1:] -= u[:-1]  # t0 + chain(1)
+    s[0] = stencil_apply(u[:min(2, nz)])[0]
+    return s
+
+
+def outer_solve_slabs(shape, b: np.ndarray, nslabs: int, max_iterations: int, tolerance: float,
+                      basis: str = "initial", sweeps: int = 1, pool=None, on_sweep=None):
+    """Synchronous block Jacobi on z-slabs with overlap 0 and inner CG, matrix
+    free — the same algorithm as ``outer_solve_sync`` (multisplit.py:544-707,
+    paper residual mode) for ``block_grid=(1, 1, nslabs)``, for grids whose
+    global CSR does not fit (configs 3/4 at 512^3).
+
+    * block system A_ii = the slab's principal submatrix = ``stencil_apply_box``
+      of the slab (problems.py:362-406); its coupling has one -1 per face row;
+    * rhs = b - C halo (multisplit.py:333-338): a face row's coupling sum is
+      ``-h`` (one term), so rhs = b - (-h);
+    * payload = the neighbour's boundary plane (merge with m = 1, 341-369);
+    * local residual r = (b - A_ii x) - C owner_halo on the slab rows, num =
+      ||r||, den = ||b_owned|| else ||b|| else 1 (372-396); estimate =
+      sqrt(sum(local^2)) in block order (comm.py:442-445).
+
+    Runs exactly ``sweeps`` sweeps (no termination test) and returns one
+    record per sweep: per-block iteration counts, local residuals, estimate
+    and the iterates.  ``pool`` (a ``multiprocessing`` pool) solves the
+    blocks of a sweep in parallel — they are independent in sync mode.
+    """
+    nx, ny, nz = shape
+    b3 = np.asarray(b, dtype=np.float64).reshape(nz, ny, nx)
+    ranges = split_ranges(nz, nslabs)
+    bnorm = float(np.linalg.norm(b3.ravel()))
+    dens = []
+    for z0, z1 in ranges:
+        d = float(np.linalg.norm(b3[z0:z1].ravel()))
+        dens.append(d if d != 0.0 else (bnorm if bnorm != 0.0 else 1.0))
+    xs = [np.zeros((z1 - z0, ny, nx)) for z0, z1 in ranges]
+    halo_lo = [None] + [np.zeros((ny, nx)) for _ in range(nslabs - 1)]
+    halo_hi = [np.zeros((ny, nx)) for _ in range(nslabs - 1)] + [None]
+    records = []
+    for k in range(sweeps):
+        jobs = []
+        for blk, (z0, z1) in enumerate(ranges):
+            rhs = b3[z0:z1].copy()
+            if halo_lo[blk] is not None:
+                rhs[0] -= -halo_lo[blk]
+            if halo_hi[blk] is not None:
+                rhs[-1] -= -halo_hi[blk]
+            jobs.append((rhs, xs[blk], max_iterations, tolerance, basis))
+        outs = pool.map(_slab_cg, jobs) if pool is not None else [_slab_cg(j) for j in jobs]
+        its = []
+        for blk, (x_new, it) in enumerate(outs):
+            xs[blk] = x_new
+            its.append(it)
+        for blk in range(nslabs):  # payloads of sweep k (multisplit.py:341-369, m = 1)
+            if blk > 0:
+                halo_lo[blk] = xs[blk - 1][-1].copy()
+            if blk < nslabs - 1:
+                halo_hi[blk] = xs[blk + 1][0].copy()
+        locals_ = []
+        for blk, (z0, z1) in enumerate(ranges):
+            r = b3[z0:z1] - stencil_apply_box(xs[blk])
+            if halo_lo[blk] is not None:
+                r[0] -= -halo_lo[blk]
+            if halo_hi[blk] is not None:
+                r[-1] -= -halo_hi[blk]
+            locals_.append(float(np.linalg.norm(r.ravel())) / dens[blk])
+        estimate = math.sqrt(float(sum(locals_[w] ** 2 for w in range(nslabs))))
+        rec = {"k": k, "its": its, "locals": locals_, "estimate": estimate, "x": xs}
+        records.append(rec)
+        if on_sweep is not None:
+            on_sweep(rec)
+    return records
+
+
+def _slab_cg(job):
+    rhs, x0, max_iterations, tolerance, basis = job
+    shape = rhs.shape
+    x, rep = cg(lambda v: stencil_apply_box(v.reshape(shape)).ravel(), rhs.ravel(), x0.ravel(),
+                max_iterations, tolerance, basis)
+    if rep.stop_reason == "breakdown":
+        raise RuntimeError("breakdown in a slab solve")
+    return x.reshape(shape), rep.iterations_used
+
+
 def offdiag_apply(u3: np.ndarray, region: np.ndarray | None = None) -> np.ndarray:
     """(A - D) u matrix-free on ``region``: ``csr_spmv`` of
     ``csr_without_diagonal`` bit for bit.  Present terms

@@ -1930,6 +1930,251 @@ __global__ void __launch_bounds__(NTHR, 2) k_cg_persistent(const KParams P) {
     }
 }
 
+// ---- streaming persistent CG: many tiles (and up to MAXB_STREAM blocks) per
+// co-resident grid.  When the tiles outnumber the co-resident CTAs (config 3:
+// eight 512^2 x 64 slabs = 8192 tiles, or one slab = 1024 tiles per GPU at
+// 8 GPUs), the whole inner solve is still ONE cooperative launch: every sweep
+// each CTA streams tiles back to back through one ring (the multi-tile
+// machinery of k_sweep: tiles handed out by a per-sweep counter, the producer
+// warp running into the next tile while the consumers finish the last), a
+// software grid barrier separates sweeps, and every CTA reduces all blocks'
+// tile partials itself (local decision, as cg_persistent_local).  Tile
+// partials and their reduction order are those of the launch path, so the
+// numbers are bit for bit the graph path's.
+constexpr int MAXB_STREAM = 16;
+
+// The partials of one tile (consumer warps only; the producer may already be
+// streaming the next tile): cta_sum<NTHR>'s order — warps 0..NCW-1, then the
+// producer warp's +0.0 — exactly as tile_epilogue.
+__device__ __forceinline__ void tile_partial(const KParams &P, double (&acc)[NQ], int cta, double *red, double *part) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const double v = warp_sum(acc[q]);
+        if (lane == 0) red[q * NCW + warp] = v;
+    }
+    consumer_sync();
+    if (tid == 0) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            double sum = red[q * NCW];
+            for (int w = 1; w < NCW; ++w) sum = add(sum, red[q * NCW + w]);
+            part[(size_t)q * P.nctas + cta] = add(sum, 0.0);
+        }
+    }
+    consumer_sync();  // red is reused by the next tile
+}
+
+template <int OPK, bool BOX>
+__device__ void stream_sweep(const KParams &P, unsigned char *smem, const DState *s_states, double *part,
+                             unsigned *counter, uint64_t *s_tfull, uint64_t *s_tempty, int *s_tile, double *s_red) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr int NS = op_stages(OPK);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + NS * op_stage_bytes(OPK));
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&full[NS + s], NCW);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&s_tfull[s], 1);
+            mbar_init(&s_tempty[s], NCW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    const int T = P.nctas;
+    int round = 0;
+    for (int n = 0;; ++n) {
+        const int slot = n & 1;
+        const uint32_t ph = (uint32_t)((n >> 1) & 1);
+        int i = 0;
+        if (warp == NCW) {
+            if (lane == 0) {
+                if (n >= 2) mbar_wait(&s_tempty[slot], ph ^ 1u);
+                i = (int)atomicAdd(counter, 1u);
+                s_tile[slot] = i;
+                mbar_arrive(&s_tfull[slot]);
+            }
+            i = __shfl_sync(0xffffffffu, i, 0);
+        } else {
+            mbar_wait(&s_tfull[slot], ph);
+            i = s_tile[slot];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_tempty[slot]);
+        }
+        if (i >= T) break;
+        const int cta = op_rev(OPK) ? T - 1 - i : i;
+        const int b = P.cta_block[cta];
+        const DBlock &B = P.blocks[b];
+        const DState &S = s_states[b];
+        if (!serves<OPK, -1>(S, P)) continue;
+        double acc[NQ] = {0.0, 0.0, 0.0, 0.0};
+        const SweepCtx C = make_ctx<OPK>(P, b, B, S);
+        round += sweep_tile<OPK, BOX>(C, cta - B.cta_begin, smem, acc, round);
+        if (tid < NT) tile_partial(P, acc, cta, s_red, part);
+    }
+    __syncthreads();
+    if (tid == 0) {  // the next sweep re-initialises this memory for its own ring
+        for (int s = 0; s < 2 * NS; ++s)
+            asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(full + s)) : "memory");
+        for (int s = 0; s < 2; ++s) {
+            asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(s_tfull + s)) : "memory");
+            asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(s_tempty + s)) : "memory");
+        }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Local-decision barrier of the streaming kernel: arrive, wait for all, then
+// reduce every served block's tile partials at once — virtual lane l of
+// (block, quantity) pair p sums part[cta_begin + l + 256 k] from 0.0 in k
+// order, warp w folds pairs w, w + 9, ... with range_sum's tree: the same
+// bits as range_sum per block — and advance the shared-memory block states.
+template <int OPK>
+__device__ void grid_sync_stream(const KParams &P, unsigned char *smem, DState *s_states, const double *part,
+                                 unsigned &target, LocalCtl &L, int *s_list, double *s_q) {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __syncthreads();
+    target += gridDim.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        unsigned prev;
+        asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&P.ctl->bar_count) : "memory");
+        unsigned cur = prev + 1u;
+        while ((int)(cur - target) < 0)
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(&P.ctl->bar_count) : "memory");
+        int n = 0;
+        for (int b = 0; b < P.nblocks; ++b)
+            if (serves<OPK, -1>(s_states[b], P)) s_list[n++] = b;
+        s_list[MAXB_STREAM] = n;
+    }
+    __syncthreads();
+    constexpr int NQK = op_nq<OPK>();
+    double *scratch = reinterpret_cast<double *>(smem);  // the ring is idle: SMEM_MAX bytes
+    constexpr int CHUNK = SMEM_MAX / (256 * 8);          // (block, quantity) pairs per pass
+    const int npairs = s_list[MAXB_STREAM] * NQK;
+    for (int p0 = 0; p0 < npairs; p0 += CHUNK) {
+        const int cnt = min(CHUNK, npairs - p0);
+        for (int idx = tid; idx < cnt * 256; idx += NTHR) {
+            const int p = p0 + idx / 256, l = idx % 256;
+            const DBlock &B = P.blocks[s_list[p / NQK]];
+            const double *src = part + (size_t)(p % NQK) * P.nctas;
+            double s = 0.0;
+            for (int c = B.cta_begin + l; c < B.cta_end; c += 256) s = add(s, __ldcg(src + c));
+            scratch[idx] = s;
+        }
+        __syncthreads();
+        for (int pp = warp; pp < cnt; pp += NTHR / 32) {
+            double v[8];
+#pragma unroll
+            for (int m = 0; m < 8; ++m) v[m] = scratch[pp * 256 + lane + 32 * m];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) v[m] = add(v[m], v[m + 4]);
+            v[0] = add(v[0], v[2]);
+            v[1] = add(v[1], v[3]);
+            double t = add(v[0], v[1]);
+#pragma unroll
+            for (int w = 16; w > 0; w >>= 1) t = add(t, __shfl_down_sync(0xffffffffu, t, w));
+            if (lane == 0) s_q[p0 + pp] = t;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        for (int n = 0; n < s_list[MAXB_STREAM]; ++n) {
+            const int b = s_list[n];
+            double q[NQ] = {0.0, 0.0, 0.0, 0.0};
+            for (int i = 0; i < NQK; ++i) q[i] = s_q[n * NQK + i];
+            transition(P.blocks[b], s_states[b], nullptr, s_states[b].phase, q, blockIdx.x == 0);
+        }
+        int active = 0, verify = 0;
+        for (int bb = 0; bb < P.nblocks; ++bb) {
+            const int p2 = s_states[bb].phase;
+            if (p2 != PH_DONE && p2 != PH_IDLE) ++active;
+            if (p2 == PH_VERIFY || p2 == PH_INIT || p2 == PH_RESID) ++verify;
+        }
+        if (OPK == OP_S2) {
+            L.cycles += 1;
+            if (L.max_cycles > 0 && L.cycles > L.max_cycles && active) {
+                for (int bb = 0; bb < P.nblocks; ++bb) {
+                    DState &Sb = s_states[bb];
+                    if (Sb.phase != PH_DONE && Sb.phase != PH_IDLE) {
+                        Sb.phase = PH_DONE;
+                        Sb.stop = STOP_STALLED;
+                    }
+                }
+                L.stalled = 1;
+                active = 0;
+                verify = 0;
+            }
+        }
+        if (OPK == OP_RESID) L.resid_runs += 1;
+        L.active = active;
+        L.verify = verify;
+    }
+    __syncthreads();
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+#ifndef BS_STREAM_MINBLOCKS
+#define BS_STREAM_MINBLOCKS 3
+#endif
+
+template <bool BOX>
+__global__ void __launch_bounds__(NTHR, BS_STREAM_MINBLOCKS) k_cg_stream(const KParams P) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    __shared__ DState s_states[MAXB_STREAM];
+    __shared__ LocalCtl L;
+    __shared__ double s_red[NQ * NCW];
+    __shared__ double s_q[MAXB_STREAM * NQ];
+    __shared__ int s_tile[2], s_list[MAXB_STREAM + 1];
+    __shared__ __align__(8) uint64_t s_tfull[2], s_tempty[2];
+    if (threadIdx.x < P.nblocks) s_states[threadIdx.x] = ld_state(P.states + threadIdx.x);
+    if (threadIdx.x == 0) L = LocalCtl{0, 0, 0, 0, 0, *(volatile int *)&P.ctl->max_cycles};
+    __syncthreads();
+    double *part[2] = {P.partials, P.partials + (size_t)NQ * P.nctas};
+    unsigned *ctr = P.tile_counter + 2;  // [0], [1] by sweep parity; zeroed by the host before the launch
+    unsigned target = 0;                 // bar_count is zeroed by k_reset_control before the launch
+    int sw = 0;
+    auto next = [&] {
+        ++sw;
+        // the counter of sweep sw+1 was last used by sweep sw-1: every CTA
+        // fetched from it before that barrier; the reset is released by this
+        // CTA's arrival at the barrier of sweep sw
+        if (blockIdx.x == 0 && threadIdx.x == 0) ctr[(sw + 1) & 1] = 0u;
+    };
+    stream_sweep<OP_RESID, BOX>(P, smem, s_states, part[sw & 1], ctr + (sw & 1), s_tfull, s_tempty, s_tile, s_red);
+    grid_sync_stream<OP_RESID>(P, smem, s_states, part[sw & 1], target, L, s_list, s_q);
+    next();
+    while (L.active) {
+        stream_sweep<OP_S1, BOX>(P, smem, s_states, part[sw & 1], ctr + (sw & 1), s_tfull, s_tempty, s_tile, s_red);
+        grid_sync_stream<OP_S1>(P, smem, s_states, part[sw & 1], target, L, s_list, s_q);
+        next();
+        stream_sweep<OP_S2, BOX>(P, smem, s_states, part[sw & 1], ctr + (sw & 1), s_tfull, s_tempty, s_tile, s_red);
+        grid_sync_stream<OP_S2>(P, smem, s_states, part[sw & 1], target, L, s_list, s_q);
+        next();
+        if (L.verify) {
+            stream_sweep<OP_RESID, BOX>(P, smem, s_states, part[sw & 1], ctr + (sw & 1), s_tfull, s_tempty, s_tile,
+                                        s_red);
+            grid_sync_stream<OP_RESID>(P, smem, s_states, part[sw & 1], target, L, s_list, s_q);
+            next();
+        }
+    }
+    if (blockIdx.x == 0) {
+        if (threadIdx.x < P.nblocks) P.states[threadIdx.x] = s_states[threadIdx.x];
+        if (threadIdx.x == 0) {
+            Control *ctl = P.ctl;
+            ctl->cycles = L.cycles;
+            ctl->stalled = L.stalled;
+            ctl->resid_runs = L.resid_runs;
+            ctl->active = L.active;
+            ctl->verify = L.verify;
+            *P.n_active = L.active;
+        }
+    }
+}
+
 // Pointwise GMRES passes over a block's region, tile by tile (same CTA table
 // and deterministic reduction order as the sweeps).
 template <int PKK, bool BOX>
@@ -2609,6 +2854,7 @@ struct bs_ctx {
     cudaStream_t cap_stream = nullptr;
     int run_kind = KIND_CG;    // solve armed last: bs_run drives its loop
     int pgrid = -1;            // persistent CG grid (co-resident CTAs), -1 = not computed
+    int sgrid = -1;            // streaming persistent CG grid (k_cg_stream), -1 = not computed
     bool jac_dirty = false;    // a Jacobi iterate may sit in p[0] (flush before other solves)
     // optional CUDA-event timing of the sweep kernels (launch mode only)
     bool timing = false;
@@ -3028,7 +3274,7 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
         e = cudaMemcpy(c->dpcta_block, pcta_block.data(), sizeof(int) * c->npctas, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&c->dblk_counter, sizeof(unsigned) * nblocks);
     if (e == cudaSuccess) e = cudaMalloc(&c->dlaunch_counter, sizeof(unsigned));
-    if (e == cudaSuccess) e = cudaMalloc(&c->dtile_counter, sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMalloc(&c->dtile_counter, 4 * sizeof(unsigned));  // [0] sweep launches, [2..3] k_cg_stream
     if (e == cudaSuccess) e = cudaMalloc(&c->dnactive, sizeof(int));
     if (e == cudaSuccess) e = cudaMalloc(&c->dctl, sizeof(Control));
     if (e == cudaSuccess) e = cudaMalloc(&c->dactive, sizeof(int) * nblocks);
@@ -3047,7 +3293,7 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
     if (e == cudaSuccess) e = cudaMemset(c->dstates, 0, sizeof(DState) * nblocks);
     if (e == cudaSuccess) e = cudaMemset(c->dblk_counter, 0, sizeof(unsigned) * nblocks);
     if (e == cudaSuccess) e = cudaMemset(c->dlaunch_counter, 0, sizeof(unsigned));
-    if (e == cudaSuccess) e = cudaMemset(c->dtile_counter, 0, sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMemset(c->dtile_counter, 0, 4 * sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemset(c->dnactive, 0, sizeof(int));
     if (e == cudaSuccess) e = cudaMemset(c->dctl, 0, sizeof(Control));
     {
@@ -3056,7 +3302,8 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
                              sweep_fn<OP_GSPMV>(true),    sweep_fn<OP_GSPMV>(false), sweep_fn<OP_JAC>(true),
                              sweep_fn<OP_JAC>(false),     (const void *)k_apply<true>,
                              (const void *)k_cg_persistent<true>, (const void *)k_cg_persistent<false>,
-                             (const void *)k_apply<false>};
+                             (const void *)k_apply<false>, (const void *)k_cg_stream<true>,
+                             (const void *)k_cg_stream<false>};
         for (const void *f : fns)
             if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
     }
@@ -3219,12 +3466,19 @@ int bs_residual(bs_ctx *c, const int32_t *active, void *stream) {
 }
 
 namespace {
-// Persistent CG applies when every tile has its own co-resident CTA (one
-// wave); BS_PERSIST=0 disables it, BS_PERSIST=2 also allows tile loops.
-bool use_persistent(bs_ctx *c) {
+// Run path of CG solves (BS_PERSIST, default 1): 1 = one persistent launch —
+// k_cg_persistent when every tile has its own co-resident CTA, else the
+// streaming k_cg_stream (<= MAXB_STREAM blocks); 0 = the CUDA-graph path;
+// 2 = k_cg_persistent with tile loops; 3 = k_cg_stream always.  All paths
+// give bitwise-identical results.
+int persist_mode() {
     const char *env = std::getenv("BS_PERSIST");
-    const int mode = env ? std::atoi(env) : 1;
-    if (mode == 0) return false;
+    return env ? std::atoi(env) : 1;
+}
+
+bool use_persistent(bs_ctx *c) {
+    const int mode = persist_mode();
+    if (mode == 0 || mode == 3) return false;
     if (c->pgrid < 0) {
         int per_sm = 0, sms = 0, coop = 0;
         const void *fn = c->box ? (const void *)k_cg_persistent<true> : (const void *)k_cg_persistent<false>;
@@ -3241,6 +3495,29 @@ bool use_persistent(bs_ctx *c) {
     return mode == 2 || c->pgrid == c->nctas;
 }
 
+bool use_stream(bs_ctx *c) {
+    const int mode = persist_mode();
+    if ((mode != 1 && mode != 3) || c->nblocks > MAXB_STREAM) return false;
+    if (c->sgrid < 0) {
+        int per_sm = 0, sms = 0, coop = 0;
+        const void *fn = c->box ? (const void *)k_cg_stream<true> : (const void *)k_cg_stream<false>;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NTHR, SMEM_MAX) != cudaSuccess ||
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device) != cudaSuccess ||
+            cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c->device) != cudaSuccess || !coop) {
+            cudaGetLastError();
+            c->sgrid = 0;
+        } else {
+            if (const char *e = std::getenv("BS_SWEEP_PER_SM"))  // A/B: fewer resident CTAs per SM
+                per_sm = std::min(per_sm, std::max(1, std::atoi(e)));
+            c->sgrid = std::min(c->nctas, per_sm * sms);
+        }
+    }
+    return c->sgrid > 0;
+}
+
+}  // namespace
+
+namespace {
 // Jacobi solves: graph mode (one launch) or launch mode (timing), sweep count out
 int run_jacobi(bs_ctx *c, int batch, int max_launches, cudaStream_t st, int64_t *sweeps_out) {
     if (!c->timing) {
@@ -3293,6 +3570,27 @@ int bs_run(bs_ctx *c, int batch, int max_launches, void *stream, int64_t *sweeps
             // computes the same thing (same tile partials, same order)
             cudaGetLastError();
             c->pgrid = 0;
+        } else {
+            ++g_launches;
+            BS_CU(cudaMemcpyAsync(c->hctl, c->dctl, sizeof(Control), cudaMemcpyDeviceToHost, st));
+            BS_CU(cudaStreamSynchronize(st));
+            const Control ctl = *c->hctl;
+            if (sweeps_out) *sweeps_out = (long long)ctl.resid_runs + 2LL * ctl.cycles;
+            if (ctl.stalled) return fail(BS_ESTATE, "bs_run: solves still active after max_launches sweeps");
+            return BS_OK;
+        }
+    }
+    if (!c->timing && use_stream(c)) {
+        // the whole solve in one cooperative launch, tiles streamed per CTA
+        ++g_launches;
+        k_reset_control<<<1, 1, 0, st>>>(c->dctl, max_launches > 0 ? (max_launches + 2) / 3 : 0);
+        BS_CU(cudaMemsetAsync(c->dtile_counter + 2, 0, 2 * sizeof(unsigned), st));
+        KParams P = make_params(c, false);
+        void *args[] = {&P};
+        const void *fn = c->box ? (const void *)k_cg_stream<true> : (const void *)k_cg_stream<false>;
+        if (cudaLaunchCooperativeKernel(fn, dim3(c->sgrid), dim3(NTHR), args, SMEM_MAX, st) != cudaSuccess) {
+            cudaGetLastError();  // SMs held by another context: the graph path computes the same numbers
+            c->sgrid = 0;
         } else {
             ++g_launches;
             BS_CU(cudaMemcpyAsync(c->hctl, c->dctl, sizeof(Control), cudaMemcpyDeviceToHost, st));

@@ -54,7 +54,7 @@ def make_inner(eng, spec, config):
 
 
 def run_sync(eng, config, dens, bnorm, nblocks, local_ids, exchange, allreduce_rows, t_start,
-             on_sweep=None, merge=None, eng_index=None):
+             on_sweep=None, merge=None, eng_index=None, probe=None):
     """Run sweeps until the reference's termination rule fires.
 
     ``exchange()`` performs the overlap-0 halo exchange; ``allreduce_rows(a)``
@@ -63,6 +63,12 @@ def run_sync(eng, config, dens, bnorm, nblocks, local_ids, exchange, allreduce_r
     merge (default: ``eng.overlap_merge``); ``eng_index[li]`` is the engine
     slot of ``local_ids[li]`` (default: li).  Returns (rows, per_block, converged,
     final_true) with rows = (k, time, estimate, true_or_None, inner_total).
+
+    ``probe`` (measurement only, e.g. ``bench.py``): an object whose
+    ``begin(phase, k)`` / ``end(phase, k)`` bracket the inner solve
+    (phase "solve", sweep k) and the halo exchange ("exchange") on the host
+    thread that launches them, and whose ``sweep(k, its)`` is called once per
+    completed sweep with the global per-block inner iteration counts.
     """
     spec = config.inner
     overlap = eng.overlap
@@ -70,8 +76,12 @@ def run_sync(eng, config, dens, bnorm, nblocks, local_ids, exchange, allreduce_r
         merge = eng.overlap_merge
     eng_index = list(eng_index) if eng_index is not None else list(range(len(local_ids)))
     arm, solve = make_inner(eng, spec, config)
+    if probe is None:
+        probe = _NoProbe()
     arm()
+    probe.begin("solve", 0)
     solve()  # sweep 0: rhs = b (zero halos), x0 = 0
+    probe.end("solve", 0)
     rows, per_block = [], []
     converged = False
     final_true = math.nan
@@ -79,7 +89,9 @@ def run_sync(eng, config, dens, bnorm, nblocks, local_ids, exchange, allreduce_r
     while True:
         its_reps = eng.reports()
         if overlap == 0:
+            probe.begin("exchange", k)
             exchange()
+            probe.end("exchange", k)
             arm()
             eng.sweep_resid()
         else:
@@ -106,6 +118,7 @@ def run_sync(eng, config, dens, bnorm, nblocks, local_ids, exchange, allreduce_r
         rows.append((k, now, estimate, true_res if want_true else None, int(sum(its))))
         if on_sweep is not None:
             on_sweep(k)
+        probe.sweep(k, its)
         final_true = true_res
         if estimate < config.tol or k + 1 >= config.max_outer:  # check_termination (409-426)
             converged = estimate < config.tol
@@ -117,6 +130,19 @@ def run_sync(eng, config, dens, bnorm, nblocks, local_ids, exchange, allreduce_r
             break
         if overlap:
             arm()
+        probe.begin("solve", k + 1)
         solve()
+        probe.end("solve", k + 1)
         k += 1
     return rows, per_block, converged, final_true
+
+
+class _NoProbe:
+    def begin(self, phase, k):
+        pass
+
+    def end(self, phase, k):
+        pass
+
+    def sweep(self, k, its):
+        pass

@@ -326,3 +326,72 @@ def test_iteration_operator_radius_matches_reference(key):
     if ref["converged"]:
         assert abs(e.iterations_used - ref["iterations_used"]) <= 1
     assert e.radius == pytest.approx(ref["radius"], rel=1e-9)
+
+
+# ---------------------------------------------------------------- full-size slab oracle (config 3 fixture)
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (5, 1, 7), (7, 5, 1), (9, 11, 13), (16, 16, 16), (3, 2, 2)])
+def test_box_stencil_bit_equal(shape):
+    """stencil_apply_box (the fast whole-box path of the 512^3 fixture) ==
+    stencil_apply bit for bit, signed zeros included."""
+    nx, ny, nz = shape
+    rng = np.random.default_rng(7)
+    u = rng.standard_normal((nz, ny, nx)) * np.exp(rng.uniform(-20, 20, (nz, ny, nx)))
+    a, b = O.stencil_apply(u), O.stencil_apply_box(u)
+    assert np.array_equal(a, b) and np.array_equal(np.signbit(a), np.signbit(b))
+
+
+def test_box_stencil_matches_reference_spmv():
+    A = arrays()
+    for shape in [(6, 5, 4), (16, 16, 16), (7, 1, 3)]:
+        key = "spmv/%dx%dx%d" % shape
+        nx, ny, nz = shape
+        assert np.array_equal(O.stencil_apply_box(A[key + "/x"].reshape(nz, ny, nx)).ravel(), A[key + "/y"])
+
+
+def test_slab_oracle_matches_reference_trace():
+    """The matrix-free z-slab outer sweep against the reference's own trace
+    (outer/cfg3_16_paper: 16^3, 4 slabs, fixed 10 CG its, paper mode)."""
+    A, M = arrays(), meta()["outer/cfg3_16_paper"]
+    n = M["case"]["n"]
+    recs = O.outer_solve_slabs((n, n, n), A["outer/cfg3_16_paper/rhs"], 4, 10, 0.0, "rhs",
+                               sweeps=M["outer_iterations"])
+    for rec, ref in zip(recs, M["trace"]):
+        assert sum(rec["its"]) == ref[4]
+        assert rec["estimate"] == pytest.approx(ref[2], rel=1e-10)
+    x = np.concatenate([xx.ravel() for xx in recs[-1]["x"]])
+    sol = A["outer/cfg3_16_paper/solution"]
+    assert np.linalg.norm(x - sol) <= 1e-12 * np.linalg.norm(sol)
+
+
+def test_slab_oracle_equals_csr_oracle():
+    """outer_solve_slabs == outer_solve_sync bit for bit (counts, estimates,
+    iterates) on the config-3 analogue with the r0-relative basis."""
+    n = 16
+    b = O.seeded_rhs(n ** 3, 0)
+    res = O.outer_solve_sync((n, n, n), b, (1, 1, 4), 0,
+                             dict(kind="cg", max_iterations=30, tolerance=1e-3, basis="initial"),
+                             tol=1e-30, max_outer=6)
+    recs = O.outer_solve_slabs((n, n, n), b, 4, 30, 1e-3, "initial", sweeps=6)
+    for rec, row, its in zip(recs, res.rows, res.per_block_inner):
+        assert rec["its"] == its
+        assert rec["estimate"] == row.estimated_residual
+    assert np.array_equal(np.concatenate([xx.ravel() for xx in recs[-1]["x"]]), res.solution)
+
+
+def test_cfg3_fixture_is_consistent():
+    """The committed 512^3 fixture: 8 slabs x 3 sweeps, estimates = the
+    block-order combiner of its local residuals (comm.py:442-445)."""
+    import json
+    import math
+    import os
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "cfg3_512.json")) as fh:
+        m = json.load(fh)
+    assert m["n"] == 512 and m["nslabs"] == 8 and len(m["sweeps"]) == 3
+    for s in m["sweeps"]:
+        assert len(s["its"]) == 8 and all(1 <= i <= 100 for i in s["its"])
+        assert s["estimate"] == math.sqrt(float(sum(v ** 2 for v in s["locals"])))
+    est = [s["estimate"] for s in m["sweeps"]]
+    assert est == sorted(est, reverse=True)
