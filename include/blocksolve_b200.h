@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define BS_ABI_VERSION 1
+#define BS_ABI_VERSION 2
 
 #define BS_OK 0
 #define BS_EINVAL -1   /* bad argument  -> ValueError / ConfigurationError */
@@ -86,6 +86,8 @@ typedef struct bs_block_report {
     double r_owned_sq;   /* same restricted to owned rows (local residual)  */
     double rglob_owned_sq; /* ||b - A_global x||^2 over owned rows (true mode) */
     double scale;
+    int32_t last_iterations;   /* the solve before the last bs_*_begin (its count / */
+    int32_t last_stop_reason;  /* stop), so the outer sweep reads them with the residual */
 } bs_block_report;
 
 typedef struct bs_ctx bs_ctx;
@@ -106,6 +108,11 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
                   bs_ctx **out);
 int bs_ctx_destroy(bs_ctx *ctx);
 int bs_ctx_num_ctas(const bs_ctx *ctx);
+/* How the last bs_run drove its solves: 0 CUDA graph of sweep launches,
+ * 1 persistent cooperative kernel (one tile per CTA), 2 streaming persistent
+ * kernel (k_cg_stream), 3 launch mode (per-kernel timing), 4 point-Jacobi
+ * graph, -1 none yet. */
+int bs_ctx_run_path(const bs_ctx *ctx);
 
 /* Row pitch (in doubles) of block `block`'s padded-box vectors: the x extent
  * rounded up to 4 (TMA needs 16-byte row strides).  Index of padded-box cell

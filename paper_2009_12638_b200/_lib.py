@@ -55,6 +55,8 @@ class BlockReport(ctypes.Structure):
         ("r_owned_sq", ctypes.c_double),
         ("rglob_owned_sq", ctypes.c_double),
         ("scale", ctypes.c_double),
+        ("last_iterations", ctypes.c_int32),
+        ("last_stop_reason", ctypes.c_int32),
     ]
 
 
@@ -66,6 +68,7 @@ _SIGS = {
     "bs_ctx_create": ([_I, _I, ctypes.POINTER(BlockDesc), _I, ctypes.POINTER(_P)], _I),
     "bs_ctx_destroy": ([_P], _I),
     "bs_ctx_num_ctas": ([_P], _I),
+    "bs_ctx_run_path": ([_P], _I),
     "bs_block_pitch": ([_P, _I], _I),
     "bs_stencil_apply": ([_P, _I, _P, _P, _P], _I),
     "bs_cg_begin": ([_P, _I, ctypes.c_double, _I, _P, _P], _I),
@@ -118,7 +121,7 @@ def load() -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    if lib.bs_abi_version() != 1:
+    if lib.bs_abi_version() != 2:
         raise DeviceError("libbsgpu.so ABI version mismatch")
     _lib = lib
     return lib

@@ -247,6 +247,7 @@ struct alignas(16) DState {
     double alpha, beta, alpha_pend, rr;
     // rest: recurrence bookkeeping, touched only by transitions and reports
     int stop, it, max_its, basis, gflag, gm;
+    int last_it, last_stop;  // the previous solve's count / stop, kept by k_arm(PH_INIT)
     double tol, tol_eff, scale, rel;
     double q[NQ];
     double cycle_start, gnrm;
@@ -295,6 +296,7 @@ struct KParams {
     int cta_base, pcta_base;   // first CTA-table entry of this launch (one-block launches)
     int ntiles;                // tiles of this sweep launch (CTA-table entries from cta_base)
     unsigned *tile_counter;    // next tile of a sweep launch (rewound by its last CTA)
+    int part_stride;           // doubles per quantity of one parity buffer of `partials`
 };
 
 // ------------------------------------------------------------------ geometry
@@ -614,7 +616,7 @@ __device__ unsigned long long g_trace[5][TRACE_CTAS];  // [4] = SM id
 // persistent kernel: [sweep][stamp][cta] for the first PT_SWEEPS sweeps:
 // 0 sweep start, 1 tiles done, 2 partials written, 3 barrier released,
 // 4 = SM clock at stamp 0 (low 48 bits) | SM id << 48
-constexpr int PT_SWEEPS = 2048, PT_CTAS = 296;
+constexpr int PT_SWEEPS = 2048, PT_CTAS = 448;
 __device__ __forceinline__ unsigned smid() {
     unsigned r;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
@@ -628,6 +630,15 @@ __device__ unsigned long long g_ptrace[PT_SWEEPS][5][PT_CTAS];  // [4]: SM clock
             if ((i) == 0) g_ptrace[(sw) % PT_SWEEPS][4][blockIdx.x] = (clock64() & 0xFFFFFFFFFFFFull) | ((unsigned long long)smid() << 48); \
         }                                                                            \
     } while (0)
+// streaming kernel: [sweep][stamp][cta], stamps 0..6 (see k_cg_stream), [7] SM clock at stamp 0
+__device__ unsigned long long g_strace[PT_SWEEPS][8][PT_CTAS];
+#define BS_SSTAMP(sw, i)                                                             \
+    do {                                                                             \
+        if (threadIdx.x == 0 && blockIdx.x < PT_CTAS) {                              \
+            g_strace[(sw) % PT_SWEEPS][(i)][blockIdx.x] = global_ns();               \
+            if ((i) == 0) g_strace[(sw) % PT_SWEEPS][7][blockIdx.x] = (clock64() & 0xFFFFFFFFFFFFull) | ((unsigned long long)smid() << 48); \
+        }                                                                            \
+    } while (0)
 #define BS_STAMP(i)                                                                  \
     do {                                                                             \
         if ((threadIdx.x == 0 || threadIdx.x == NT) && blockIdx.x < TRACE_CTAS)       \
@@ -638,6 +649,9 @@ __device__ unsigned long long g_ptrace[PT_SWEEPS][5][PT_CTAS];  // [4]: SM clock
     do {            \
     } while (0)
 #define BS_PSTAMP(sw, i) \
+    do {                 \
+    } while (0)
+#define BS_SSTAMP(sw, i) \
     do {                 \
     } while (0)
 #endif
@@ -679,14 +693,17 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 // next one reads.  Per point the arithmetic is the same in both directions
 // (the stencil chain is fixed by column order, not by traversal); only the
 // order of a thread's partial sums moves, deterministically per op.
-// round0 < 0: the tile owns the ring (initialised here, one tile per ring).
-// round0 >= 0: the ring is shared by a sequence of tiles (multi-tile CTAs):
-// initialised once, and this tile's stages are rounds round0, round0+1, ...
-// of NS stages each — the producer pads the last round with empty stages, so
-// every tile starts on stage 0 and the compile-time stage schedule below
-// holds.  Returns the rounds the tile used (0 for round0 < 0).
+// g0 < 0: the tile owns the ring (initialised here, one tile per ring).
+// g0 >= 0: the ring is shared by a sequence of tiles (multi-tile CTAs):
+// initialised once, and this tile's stages are ring-global stages g0, g0+1,
+// ... — tiles follow each other with no gap in the ring, so the producer
+// streams the next tile's first planes while the consumers finish this one.
+// The consumers' plane loop stays aligned to ring rounds of NS stages (the
+// compile-time stage schedule below): a tile starting at stage g0 % NS = o
+// enters its first round at plane -o*ZP, whose planes < 1 belong to the
+// previous tile and are skipped.  Returns the stages the tile used (0 for g0 < 0).
 template <int OP, bool BOX>
-__device__ int sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, double (&acc)[NQ], int round0 = -1) {
+__device__ int sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, double (&acc)[NQ], int g0 = -1) {
     const DBlock &B = *C.B;
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
@@ -717,10 +734,10 @@ __device__ int sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, doub
     // slot of plane q inside its stage's box (boxes run upwards in z)
     auto slot = [](int qq) { return REV ? ZP - 1 - qq % ZP : qq % ZP; };
 
-    const bool shared_ring = round0 >= 0;
+    const bool shared_ring = g0 >= 0;
     const int nst = (nplanes + ZP - 1) / ZP;   // stages with data
-    const int rounds = (nst + NS - 1) / NS;    // rounds this tile occupies (shared ring)
-    const int k0 = shared_ring ? round0 * NS : 0;  // ring-global index of the tile's stage 0
+    const int k0 = shared_ring ? g0 : 0;       // ring-global index of the tile's stage 0
+    const int o = k0 % NS;                     // ring stage of the tile's stage 0
     if (!shared_ring) {
         if (tid == 0) {
             for (int s = 0; s < NS; ++s) {
@@ -736,8 +753,8 @@ __device__ int sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, doub
     if (warp == NCW) {  // ---------------- TMA producer warp
         if (lane == 0) {
             for (int k = 0; k < nst; ++k) {  // stage k holds planes ZP*k .. ZP*k+ZP-1
-                const int s = k % NS;
                 const int kg = k0 + k;
+                const int s = kg % NS;
                 if (kg >= NS) mbar_wait(&empty[s], (uint32_t)((kg / NS - 1) & 1));
                 const int lz = REV ? lzq0 - ZP * k - (ZP - 1) : lzq0 + ZP * k;  // lowest plane of the box
                 // ZP == 1: the bare operand only for computed planes; ZP > 1: always
@@ -750,16 +767,9 @@ __device__ int sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, doub
                 if (use_b) tma_load3(st + BOFF, C.map_b, lx0 - 2, ly0 - 1, lz, &full[s]);
                 if (epi) tma_load3(st + COFF, C.map_c, lx0, ly0, lz, &full[s]);
             }
-            if (shared_ring) {  // pad the last round: empty stages keep every barrier's phase in step
-                for (int k = nst; k < rounds * NS; ++k) {
-                    const int kg = k0 + k;
-                    if (kg >= NS) mbar_wait(&empty[k % NS], (uint32_t)((kg / NS - 1) & 1));
-                    mbar_arrive(&full[k % NS]);
-                }
-            }
         }
         __syncwarp();
-        return shared_ring ? rounds : 0;
+        return shared_ring ? nst : 0;
     }
 
     // ---------------- consumers: thread (tx, ty) owns column x = lx0 + tx of
@@ -804,19 +814,20 @@ __device__ int sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, doub
         row_in[r] = lx < pdx && ly_0 + r < pdy;
     }
 
-    const uint32_t par0 = shared_ring ? (uint32_t)(round0 & 1) : 0u;
+    const uint32_t par0 = (uint32_t)((k0 / NS) & 1);  // completion parity of the tile's first round
     double u_prev[RY], u_cur[RY];
-    mbar_wait(&full[0], par0);
+    mbar_wait(&full[o], par0);
     if (tid == 0) BS_STAMP(1);
 #pragma unroll
-    for (int r = 0; r < RY; ++r) u_prev[r] = uval(smem + slot(0) * (SC * 8), own[r], 0, gjr[r], lzq0);
-    if (ZP == 1) mbar_wait(&full[1], par0);
-    const unsigned char *st1 = smem + (ZP == 1 ? STB : 0) + slot(1) * (SC * 8);
+    for (int r = 0; r < RY; ++r) u_prev[r] = uval(smem + o * STB + slot(0) * (SC * 8), own[r], 0, gjr[r], lzq0);
+    const int s1 = ZP == 1 ? (k0 + 1) % NS : o;
+    if (ZP == 1) mbar_wait(&full[s1], (uint32_t)(((k0 + 1) / NS) & 1));
+    const unsigned char *st1 = smem + s1 * STB + slot(1) * (SC * 8);
 #pragma unroll
     for (int r = 0; r < RY; ++r) u_cur[r] = uval(st1, own[r], 0, gjr[r], lzq0 + DZ);
     if (ZP == 1) {  // plane 0 is never computed: its stage is free (ZP > 1: plane 1 shares it)
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[0]);
+        if (lane == 0) mbar_arrive(&empty[o]);
     }
 
     const bool px_box = lx > 0;
@@ -987,7 +998,7 @@ __device__ int sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, doub
     const bool tile_full = lx0 + TX <= pdx && ly0 + TY <= pdy;
     // the computed plane with lz == 0 (no z-1 neighbour), if the tile has one
     const int q_zero = lz0 == 0 ? (REV ? lz1 : 1) : -1;
-    for (int q0 = 0; q0 <= nplanes - 2; q0 += NS * ZP, par ^= 1u) {
+    for (int q0 = -o * ZP; q0 <= nplanes - 2; q0 += NS * ZP, par ^= 1u) {
         constexpr int QR = NS * ZP;  // planes per round
         // measured per op: the CG sweeps take both fast variants; the residual,
         // Jacobi and GMRES sweeps only the unguarded one (a third unrolled
@@ -1026,18 +1037,18 @@ __device__ int sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, doub
     }
     if (tid == 0) BS_STAMP(2);
     if (shared_ring) {
-        // release the stages the plane loop did not: the one holding only the
-        // last (never computed) plane, and the padding — after waiting for
-        // each, so no barrier can run a phase ahead of the producer's wait
+        // release the stages the plane loop did not (the one holding only the
+        // last, never computed, plane) — after waiting for each, so no
+        // barrier can run a phase ahead of the producer's wait
         const int released = (nplanes - 1 - ZP) / ZP + 1;
-        const uint32_t parl = (uint32_t)((round0 + rounds - 1) & 1);
         __syncwarp();
-        for (int k = released; k < rounds * NS; ++k) {
-            mbar_wait(&full[k % NS], parl);  // all in the tile's last round
+        for (int k = released; k < nst; ++k) {
+            const int kg = k0 + k;
+            mbar_wait(&full[kg % NS], (uint32_t)((kg / NS) & 1));
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[k % NS]);
+            if (lane == 0) mbar_arrive(&empty[kg % NS]);
         }
-        return rounds;
+        return nst;
     }
     return 0;
 }
@@ -1598,7 +1609,7 @@ __global__ void __launch_bounds__(NTHR, BS_MINBLOCKS) k_sweep(const KParams P) {
     }
     __syncthreads();
     const int T = P.ntiles;
-    int round = 0;
+    int gstage = 0;  // ring-global stage of the next tile
     for (int n = 0;; ++n) {
         const int slot = n & 1;
         const uint32_t ph = (uint32_t)((n >> 1) & 1);
@@ -1625,7 +1636,7 @@ __global__ void __launch_bounds__(NTHR, BS_MINBLOCKS) k_sweep(const KParams P) {
         if (!serves<OPK, -1>(S, P)) continue;
         double acc[NQ] = {0.0, 0.0, 0.0, 0.0};
         const SweepCtx C = make_ctx<OPK>(P, b, B, S);
-        round += sweep_tile<OPK, BOX>(C, cta - B.cta_begin, smem, acc, round);
+        gstage += sweep_tile<OPK, BOX>(C, cta - B.cta_begin, smem, acc, gstage);
         if (tid < NT) tile_epilogue(P, b, S.phase, acc, op_nq<OPK>(), cta, s_red, s_scratch, &s_flag);
     }
     __syncthreads();
@@ -1931,22 +1942,27 @@ __global__ void __launch_bounds__(NTHR, 2) k_cg_persistent(const KParams P) {
 }
 
 // ---- streaming persistent CG: many tiles (and up to MAXB_STREAM blocks) per
-// co-resident grid.  When the tiles outnumber the co-resident CTAs (config 3:
-// eight 512^2 x 64 slabs = 8192 tiles, or one slab = 1024 tiles per GPU at
-// 8 GPUs), the whole inner solve is still ONE cooperative launch: every sweep
-// each CTA streams tiles back to back through one ring (the multi-tile
-// machinery of k_sweep: tiles handed out by a per-sweep counter, the producer
-// warp running into the next tile while the consumers finish the last), a
-// software grid barrier separates sweeps, and every CTA reduces all blocks'
-// tile partials itself (local decision, as cg_persistent_local).  Tile
-// partials and their reduction order are those of the launch path, so the
-// numbers are bit for bit the graph path's.
+// launch.  When the tiles outnumber the co-resident CTAs (config 3: eight
+// 512^2 x 64 slabs = 8192 tiles, or one slab = 1024 tiles per GPU at 8 GPUs),
+// the whole inner solve is still ONE cooperative launch of exactly LANES = 256
+// CTAs.  CTA c owns reduction lane c of every block: the tiles
+// cta_begin + c + 256 k (k = 0, 1, ...), streamed back to back through one
+// ring (sweep_tile's shared-ring mode: no gap between tiles), and it sums
+// their tile partials in k order itself — exactly range_sum's lane c.  So a
+// sweep publishes one value per (block, quantity, lane), every CTA reduces a
+// block from 256 lane sums with range_sum's tree after a software grid
+// barrier (local decision, as cg_persistent_local), and the numbers are bit
+// for bit the graph path's.  The static assignment gives every CTA the same
+// work (1024 tiles -> 4 per CTA) and keeps the 256 CTAs marching through the
+// same band of each plane together.
 constexpr int MAXB_STREAM = 16;
+constexpr int LANES = 256;          // = range_sum's virtual lanes = the grid
+constexpr int MAXK_STREAM = 64;     // tiles per lane and block (s_tp capacity)
 
 // The partials of one tile (consumer warps only; the producer may already be
 // streaming the next tile): cta_sum<NTHR>'s order — warps 0..NCW-1, then the
-// producer warp's +0.0 — exactly as tile_epilogue.
-__device__ __forceinline__ void tile_partial(const KParams &P, double (&acc)[NQ], int cta, double *red, double *part) {
+// producer warp's +0.0 — exactly as tile_epilogue; thread 0 stores them at out.
+__device__ __forceinline__ void tile_partial(double (&acc)[NQ], double *red, double *out) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
@@ -1959,16 +1975,17 @@ __device__ __forceinline__ void tile_partial(const KParams &P, double (&acc)[NQ]
         for (int q = 0; q < NQ; ++q) {
             double sum = red[q * NCW];
             for (int w = 1; w < NCW; ++w) sum = add(sum, red[q * NCW + w]);
-            part[(size_t)q * P.nctas + cta] = add(sum, 0.0);
+            out[q] = add(sum, 0.0);
         }
     }
     consumer_sync();  // red is reused by the next tile
 }
 
+// Lane sums of one sweep: lanes[(q * nblocks + b) * LANES + c].
 template <int OPK, bool BOX>
-__device__ void stream_sweep(const KParams &P, unsigned char *smem, const DState *s_states, double *part,
-                             unsigned *counter, uint64_t *s_tfull, uint64_t *s_tempty, int *s_tile, double *s_red) {
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+__device__ __noinline__ void stream_sweep(const KParams &P, unsigned char *smem, const DState *s_states, double *lanes,
+                                          double *s_red, double *s_tp, int sw) {
+    const int tid = threadIdx.x;
     constexpr int NS = op_stages(OPK);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + NS * op_stage_bytes(OPK));
     if (tid == 0) {
@@ -1976,118 +1993,100 @@ __device__ void stream_sweep(const KParams &P, unsigned char *smem, const DState
             mbar_init(&full[s], 1);
             mbar_init(&full[NS + s], NCW);
         }
-        for (int s = 0; s < 2; ++s) {
-            mbar_init(&s_tfull[s], 1);
-            mbar_init(&s_tempty[s], NCW);
-        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncthreads();
-    const int T = P.nctas;
-    int round = 0;
-    for (int n = 0;; ++n) {
-        const int slot = n & 1;
-        const uint32_t ph = (uint32_t)((n >> 1) & 1);
-        int i = 0;
-        if (warp == NCW) {
-            if (lane == 0) {
-                if (n >= 2) mbar_wait(&s_tempty[slot], ph ^ 1u);
-                i = (int)atomicAdd(counter, 1u);
-                s_tile[slot] = i;
-                mbar_arrive(&s_tfull[slot]);
-            }
-            i = __shfl_sync(0xffffffffu, i, 0);
-        } else {
-            mbar_wait(&s_tfull[slot], ph);
-            i = s_tile[slot];
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&s_tempty[slot]);
-        }
-        if (i >= T) break;
-        const int cta = op_rev(OPK) ? T - 1 - i : i;
-        const int b = P.cta_block[cta];
-        const DBlock &B = P.blocks[b];
+    BS_SSTAMP(sw, 0);
+    const int c = blockIdx.x;
+    int gstage = 0;  // ring-global stage of the next tile
+    // reversed ops (S2) walk the blocks and their tiles backwards: the
+    // previous sweep's last planes are still in L2 (as k_sweep)
+    for (int bi = 0; bi < P.nblocks; ++bi) {
+        const int b = op_rev(OPK) ? P.nblocks - 1 - bi : bi;
         const DState &S = s_states[b];
         if (!serves<OPK, -1>(S, P)) continue;
-        double acc[NQ] = {0.0, 0.0, 0.0, 0.0};
-        const SweepCtx C = make_ctx<OPK>(P, b, B, S);
-        round += sweep_tile<OPK, BOX>(C, cta - B.cta_begin, smem, acc, round);
-        if (tid < NT) tile_partial(P, acc, cta, s_red, part);
-    }
-    __syncthreads();
-    if (tid == 0) {  // the next sweep re-initialises this memory for its own ring
-        for (int s = 0; s < 2 * NS; ++s)
-            asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(full + s)) : "memory");
-        for (int s = 0; s < 2; ++s) {
-            asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(s_tfull + s)) : "memory");
-            asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(s_tempty + s)) : "memory");
+        const DBlock &B = P.blocks[b];
+        const int span = B.cta_end - B.cta_begin;
+        const int nk = span > c ? (span - c + LANES - 1) / LANES : 0;
+        if (nk > 0) {
+            const SweepCtx C = make_ctx<OPK>(P, b, B, S);
+            for (int kk = 0; kk < nk; ++kk) {
+                const int k = op_rev(OPK) ? nk - 1 - kk : kk;
+                double acc[NQ] = {0.0, 0.0, 0.0, 0.0};
+                gstage += sweep_tile<OPK, BOX>(C, c + LANES * k, smem, acc, gstage);
+                if (tid < NT) tile_partial(acc, s_red, s_tp + k * NQ);
+            }
+        }
+        if (tid == 0) {  // lane c of block b: its tile partials in k order (range_sum)
+#pragma unroll
+            for (int q = 0; q < op_nq<OPK>(); ++q) {
+                double sum = 0.0;
+                for (int k = 0; k < nk; ++k) sum = add(sum, s_tp[k * NQ + q]);
+                lanes[((size_t)q * P.nblocks + b) * LANES + c] = sum;
+            }
         }
     }
+    BS_SSTAMP(sw, 1);
+    __syncthreads();
+    if (tid == 0)  // the next sweep re-initialises this memory for its own ring
+        for (int s = 0; s < 2 * NS; ++s)
+            asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(full + s)) : "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 // Local-decision barrier of the streaming kernel: arrive, wait for all, then
-// reduce every served block's tile partials at once — virtual lane l of
-// (block, quantity) pair p sums part[cta_begin + l + 256 k] from 0.0 in k
-// order, warp w folds pairs w, w + 9, ... with range_sum's tree: the same
-// bits as range_sum per block — and advance the shared-memory block states.
+// warp w folds (block, quantity) pairs w, w + 9, ...: the 256 lane sums of a
+// pair with range_sum's tree (8 loads in flight per lane), and one thread per
+// served block advances its shared-memory state.
 template <int OPK>
-__device__ void grid_sync_stream(const KParams &P, unsigned char *smem, DState *s_states, const double *part,
-                                 unsigned &target, LocalCtl &L, int *s_list, double *s_q) {
+__device__ void grid_sync_stream(const KParams &P, DState *s_states, const double *lanes, unsigned &target, LocalCtl &L,
+                                 int *s_list, double *s_q, int sw) {
     asm volatile("fence.proxy.async.global;" ::: "memory");
     __syncthreads();
     target += gridDim.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
         unsigned prev;
+        BS_SSTAMP(sw, 2);
         asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&P.ctl->bar_count) : "memory");
         unsigned cur = prev + 1u;
         while ((int)(cur - target) < 0)
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(&P.ctl->bar_count) : "memory");
+        BS_SSTAMP(sw, 3);
         int n = 0;
         for (int b = 0; b < P.nblocks; ++b)
             if (serves<OPK, -1>(s_states[b], P)) s_list[n++] = b;
         s_list[MAXB_STREAM] = n;
     }
     __syncthreads();
+    BS_SSTAMP(sw, 4);
     constexpr int NQK = op_nq<OPK>();
-    double *scratch = reinterpret_cast<double *>(smem);  // the ring is idle: SMEM_MAX bytes
-    constexpr int CHUNK = SMEM_MAX / (256 * 8);          // (block, quantity) pairs per pass
-    const int npairs = s_list[MAXB_STREAM] * NQK;
-    for (int p0 = 0; p0 < npairs; p0 += CHUNK) {
-        const int cnt = min(CHUNK, npairs - p0);
-        for (int idx = tid; idx < cnt * 256; idx += NTHR) {
-            const int p = p0 + idx / 256, l = idx % 256;
-            const DBlock &B = P.blocks[s_list[p / NQK]];
-            const double *src = part + (size_t)(p % NQK) * P.nctas;
-            double s = 0.0;
-            for (int c = B.cta_begin + l; c < B.cta_end; c += 256) s = add(s, __ldcg(src + c));
-            scratch[idx] = s;
-        }
-        __syncthreads();
-        for (int pp = warp; pp < cnt; pp += NTHR / 32) {
-            double v[8];
+    const int nserved = s_list[MAXB_STREAM];
+    for (int pp = warp; pp < nserved * NQK; pp += NTHR / 32) {
+        const double *src = lanes + ((size_t)(pp % NQK) * P.nblocks + s_list[pp / NQK]) * LANES;
+        double v[8];
 #pragma unroll
-            for (int m = 0; m < 8; ++m) v[m] = scratch[pp * 256 + lane + 32 * m];
+        for (int m = 0; m < 8; ++m) v[m] = __ldcg(src + lane + 32 * m);
 #pragma unroll
-            for (int m = 0; m < 4; ++m) v[m] = add(v[m], v[m + 4]);
-            v[0] = add(v[0], v[2]);
-            v[1] = add(v[1], v[3]);
-            double t = add(v[0], v[1]);
+        for (int m = 0; m < 4; ++m) v[m] = add(v[m], v[m + 4]);  // range_sum's tree
+        v[0] = add(v[0], v[2]);
+        v[1] = add(v[1], v[3]);
+        double t = add(v[0], v[1]);
 #pragma unroll
-            for (int w = 16; w > 0; w >>= 1) t = add(t, __shfl_down_sync(0xffffffffu, t, w));
-            if (lane == 0) s_q[p0 + pp] = t;
-        }
-        __syncthreads();
+        for (int w = 16; w > 0; w >>= 1) t = add(t, __shfl_down_sync(0xffffffffu, t, w));
+        if (lane == 0) s_q[pp] = t;
     }
+    __syncthreads();
+    BS_SSTAMP(sw, 5);
+    if (tid < nserved) {  // one thread per served block (CTA 0 records the histories)
+        const int b = s_list[tid];
+        double q[NQ] = {0.0, 0.0, 0.0, 0.0};
+        for (int i = 0; i < NQK; ++i) q[i] = s_q[tid * NQK + i];
+        transition(P.blocks[b], s_states[b], nullptr, s_states[b].phase, q, blockIdx.x == 0);
+    }
+    __syncthreads();
     if (tid == 0) {
-        for (int n = 0; n < s_list[MAXB_STREAM]; ++n) {
-            const int b = s_list[n];
-            double q[NQ] = {0.0, 0.0, 0.0, 0.0};
-            for (int i = 0; i < NQK; ++i) q[i] = s_q[n * NQK + i];
-            transition(P.blocks[b], s_states[b], nullptr, s_states[b].phase, q, blockIdx.x == 0);
-        }
         int active = 0, verify = 0;
         for (int bb = 0; bb < P.nblocks; ++bb) {
             const int p2 = s_states[bb].phase;
@@ -2112,13 +2111,14 @@ __device__ void grid_sync_stream(const KParams &P, unsigned char *smem, DState *
         if (OPK == OP_RESID) L.resid_runs += 1;
         L.active = active;
         L.verify = verify;
+        BS_SSTAMP(sw, 6);
     }
     __syncthreads();
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 #ifndef BS_STREAM_MINBLOCKS
-#define BS_STREAM_MINBLOCKS 3
+#define BS_STREAM_MINBLOCKS 2
 #endif
 
 template <bool BOX>
@@ -2128,37 +2128,31 @@ __global__ void __launch_bounds__(NTHR, BS_STREAM_MINBLOCKS) k_cg_stream(const K
     __shared__ LocalCtl L;
     __shared__ double s_red[NQ * NCW];
     __shared__ double s_q[MAXB_STREAM * NQ];
-    __shared__ int s_tile[2], s_list[MAXB_STREAM + 1];
-    __shared__ __align__(8) uint64_t s_tfull[2], s_tempty[2];
+    __shared__ double s_tp[MAXK_STREAM * NQ];
+    __shared__ int s_list[MAXB_STREAM + 1];
     if (threadIdx.x < P.nblocks) s_states[threadIdx.x] = ld_state(P.states + threadIdx.x);
     if (threadIdx.x == 0) L = LocalCtl{0, 0, 0, 0, 0, *(volatile int *)&P.ctl->max_cycles};
     __syncthreads();
-    double *part[2] = {P.partials, P.partials + (size_t)NQ * P.nctas};
-    unsigned *ctr = P.tile_counter + 2;  // [0], [1] by sweep parity; zeroed by the host before the launch
-    unsigned target = 0;                 // bar_count is zeroed by k_reset_control before the launch
+    // lane sums alternate between two buffers by sweep parity (a buffer is
+    // overwritten only after the next barrier, which every CTA reaches after
+    // reading it)
+    double *lanes[2] = {P.partials, P.partials + (size_t)NQ * P.part_stride};
+    unsigned target = 0;  // bar_count is zeroed by k_reset_control before the launch
     int sw = 0;
-    auto next = [&] {
-        ++sw;
-        // the counter of sweep sw+1 was last used by sweep sw-1: every CTA
-        // fetched from it before that barrier; the reset is released by this
-        // CTA's arrival at the barrier of sweep sw
-        if (blockIdx.x == 0 && threadIdx.x == 0) ctr[(sw + 1) & 1] = 0u;
-    };
-    stream_sweep<OP_RESID, BOX>(P, smem, s_states, part[sw & 1], ctr + (sw & 1), s_tfull, s_tempty, s_tile, s_red);
-    grid_sync_stream<OP_RESID>(P, smem, s_states, part[sw & 1], target, L, s_list, s_q);
-    next();
+    stream_sweep<OP_RESID, BOX>(P, smem, s_states, lanes[sw & 1], s_red, s_tp, sw);
+    grid_sync_stream<OP_RESID>(P, s_states, lanes[sw & 1], target, L, s_list, s_q, sw);
+    ++sw;
     while (L.active) {
-        stream_sweep<OP_S1, BOX>(P, smem, s_states, part[sw & 1], ctr + (sw & 1), s_tfull, s_tempty, s_tile, s_red);
-        grid_sync_stream<OP_S1>(P, smem, s_states, part[sw & 1], target, L, s_list, s_q);
-        next();
-        stream_sweep<OP_S2, BOX>(P, smem, s_states, part[sw & 1], ctr + (sw & 1), s_tfull, s_tempty, s_tile, s_red);
-        grid_sync_stream<OP_S2>(P, smem, s_states, part[sw & 1], target, L, s_list, s_q);
-        next();
+        stream_sweep<OP_S1, BOX>(P, smem, s_states, lanes[sw & 1], s_red, s_tp, sw);
+        grid_sync_stream<OP_S1>(P, s_states, lanes[sw & 1], target, L, s_list, s_q, sw);
+        ++sw;
+        stream_sweep<OP_S2, BOX>(P, smem, s_states, lanes[sw & 1], s_red, s_tp, sw);
+        grid_sync_stream<OP_S2>(P, s_states, lanes[sw & 1], target, L, s_list, s_q, sw);
+        ++sw;
         if (L.verify) {
-            stream_sweep<OP_RESID, BOX>(P, smem, s_states, part[sw & 1], ctr + (sw & 1), s_tfull, s_tempty, s_tile,
-                                        s_red);
-            grid_sync_stream<OP_RESID>(P, smem, s_states, part[sw & 1], target, L, s_list, s_q);
-            next();
+            stream_sweep<OP_RESID, BOX>(P, smem, s_states, lanes[sw & 1], s_red, s_tp, sw);
+            grid_sync_stream<OP_RESID>(P, s_states, lanes[sw & 1], target, L, s_list, s_q, sw);
+            ++sw;
         }
     }
     if (blockIdx.x == 0) {
@@ -2483,6 +2477,8 @@ __global__ void k_arm(const DBlock *blocks, DState *states, const int *active, i
     DState &S = states[b];
     S.phase = phase;
     if (phase == PH_INIT) {
+        S.last_it = S.it;
+        S.last_stop = S.stop;
         S.stop = BS_STOP_NONE;
         S.it = 0;
         S.first = 1;
@@ -2855,6 +2851,9 @@ struct bs_ctx {
     int run_kind = KIND_CG;    // solve armed last: bs_run drives its loop
     int pgrid = -1;            // persistent CG grid (co-resident CTAs), -1 = not computed
     int sgrid = -1;            // streaming persistent CG grid (k_cg_stream), -1 = not computed
+    int part_stride = 0;       // per-quantity size of a parity buffer of dpartials
+    int stream_sumk = 0;       // tiles per lane of a whole sweep (k_cg_stream)
+    int run_path = -1;         // bs_ctx_run_path
     bool jac_dirty = false;    // a Jacobi iterate may sit in p[0] (flush before other solves)
     // optional CUDA-event timing of the sweep kernels (launch mode only)
     bool timing = false;
@@ -2911,6 +2910,7 @@ KParams make_params(bs_ctx *c, bool graph, cudaGraphConditionalHandle hl = 0,
     P.cta_base = 0;
     P.pcta_base = 0;
     P.ntiles = c->nctas;
+    P.part_stride = c->part_stride;
     return P;
 }
 
@@ -3268,13 +3268,16 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
     if (e == cudaSuccess) e = cudaMalloc(&c->dstates, sizeof(DState) * nblocks);
     if (e == cudaSuccess) e = cudaMalloc(&c->dtmaps, sizeof(CUtensorMap) * maps.size());
     if (e == cudaSuccess) e = cudaMalloc(&c->dcta_block, sizeof(int) * c->nctas);
-    if (e == cudaSuccess) e = cudaMalloc(&c->dpartials, 2 * sizeof(double) * NQ * std::max(c->nctas, c->npctas));  // x2: persistent parity buffers
+    // per quantity: one partial per sweep tile / pointwise chunk, or one lane
+    // sum per (block, lane) for k_cg_stream; x2: persistent parity buffers
+    c->part_stride = std::max(std::max(c->nctas, c->npctas), nblocks * LANES);
+    if (e == cudaSuccess) e = cudaMalloc(&c->dpartials, 2 * sizeof(double) * NQ * c->part_stride);
     if (e == cudaSuccess) e = cudaMalloc(&c->dpcta_block, sizeof(int) * c->npctas);
     if (e == cudaSuccess)
         e = cudaMemcpy(c->dpcta_block, pcta_block.data(), sizeof(int) * c->npctas, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&c->dblk_counter, sizeof(unsigned) * nblocks);
     if (e == cudaSuccess) e = cudaMalloc(&c->dlaunch_counter, sizeof(unsigned));
-    if (e == cudaSuccess) e = cudaMalloc(&c->dtile_counter, 4 * sizeof(unsigned));  // [0] sweep launches, [2..3] k_cg_stream
+    if (e == cudaSuccess) e = cudaMalloc(&c->dtile_counter, sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMalloc(&c->dnactive, sizeof(int));
     if (e == cudaSuccess) e = cudaMalloc(&c->dctl, sizeof(Control));
     if (e == cudaSuccess) e = cudaMalloc(&c->dactive, sizeof(int) * nblocks);
@@ -3293,7 +3296,7 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
     if (e == cudaSuccess) e = cudaMemset(c->dstates, 0, sizeof(DState) * nblocks);
     if (e == cudaSuccess) e = cudaMemset(c->dblk_counter, 0, sizeof(unsigned) * nblocks);
     if (e == cudaSuccess) e = cudaMemset(c->dlaunch_counter, 0, sizeof(unsigned));
-    if (e == cudaSuccess) e = cudaMemset(c->dtile_counter, 0, 4 * sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMemset(c->dtile_counter, 0, sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemset(c->dnactive, 0, sizeof(int));
     if (e == cudaSuccess) e = cudaMemset(c->dctl, 0, sizeof(Control));
     {
@@ -3353,6 +3356,8 @@ int bs_ctx_destroy(bs_ctx *c) {
 }
 
 int bs_ctx_num_ctas(const bs_ctx *c) { return c ? c->nctas : 0; }
+
+int bs_ctx_run_path(const bs_ctx *c) { return c ? c->run_path : -1; }
 
 int bs_block_pitch(const bs_ctx *c, int block) {
     if (!c || block < 0 || block >= c->nblocks) return fail(BS_EINVAL, "bs_block_pitch: bad arguments");
@@ -3501,18 +3506,32 @@ bool use_stream(bs_ctx *c) {
     if (c->sgrid < 0) {
         int per_sm = 0, sms = 0, coop = 0;
         const void *fn = c->box ? (const void *)k_cg_stream<true> : (const void *)k_cg_stream<false>;
+        int maxk = 0, sumk = 0;  // tiles per lane: of the largest block, of a whole sweep
+        for (const DBlock &B : c->hblocks) {
+            const int k = (B.cta_end - B.cta_begin + LANES - 1) / LANES;
+            maxk = std::max(maxk, k);
+            sumk += k;
+        }
+        // Static lanes put 2 CTAs on 108 SMs and 1 on 40: over long sweeps the
+        // SMs with two fall behind, while the graph path's dynamic hand-out
+        // over 3 CTAs on every SM stays balanced.  Measured per GPU on the
+        // config-3 slabs (scripts/proxy_ab.sh, profiles/r02_stream_proxy.log):
+        // stream 88.3 / 89.9 / 87.9 / 87.1 Gpts/s at 1 / 2 / 4 / 8 slabs
+        // (4 / 8 / 16 / 32 tiles per lane), graph 80.0 / 89.5 / 92.4 / 93.2.
+        c->stream_sumk = sumk;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NTHR, SMEM_MAX) != cudaSuccess ||
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device) != cudaSuccess ||
             cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c->device) != cudaSuccess || !coop) {
             cudaGetLastError();
             c->sgrid = 0;
         } else {
-            if (const char *e = std::getenv("BS_SWEEP_PER_SM"))  // A/B: fewer resident CTAs per SM
-                per_sm = std::min(per_sm, std::max(1, std::atoi(e)));
-            c->sgrid = std::min(c->nctas, per_sm * sms);
+            // exactly LANES co-resident CTAs (one per reduction lane)
+            c->sgrid = (per_sm * sms >= LANES && maxk <= MAXK_STREAM) ? LANES : 0;
         }
     }
-    return c->sgrid > 0;
+    int limit = 8;
+    if (const char *e = std::getenv("BS_STREAM_MAXK")) limit = std::atoi(e);
+    return c->sgrid > 0 && (mode == 3 || c->stream_sumk <= limit);
 }
 
 }  // namespace
@@ -3557,7 +3576,10 @@ int bs_run(bs_ctx *c, int batch, int max_launches, void *stream, int64_t *sweeps
     if (batch < 1) batch = 1;
     if (int e = set_dev(c)) return e;
     cudaStream_t st = (cudaStream_t)stream;
-    if (c->run_kind == KIND_JACOBI) return run_jacobi(c, batch, max_launches, st, sweeps_out);
+    if (c->run_kind == KIND_JACOBI) {
+        c->run_path = c->timing ? 3 : 4;
+        return run_jacobi(c, batch, max_launches, st, sweeps_out);
+    }
     if (!c->timing && use_persistent(c)) {
         // the whole solve in one cooperative launch (software grid barriers)
         ++g_launches;
@@ -3571,6 +3593,7 @@ int bs_run(bs_ctx *c, int batch, int max_launches, void *stream, int64_t *sweeps
             cudaGetLastError();
             c->pgrid = 0;
         } else {
+            c->run_path = 1;
             ++g_launches;
             BS_CU(cudaMemcpyAsync(c->hctl, c->dctl, sizeof(Control), cudaMemcpyDeviceToHost, st));
             BS_CU(cudaStreamSynchronize(st));
@@ -3584,7 +3607,6 @@ int bs_run(bs_ctx *c, int batch, int max_launches, void *stream, int64_t *sweeps
         // the whole solve in one cooperative launch, tiles streamed per CTA
         ++g_launches;
         k_reset_control<<<1, 1, 0, st>>>(c->dctl, max_launches > 0 ? (max_launches + 2) / 3 : 0);
-        BS_CU(cudaMemsetAsync(c->dtile_counter + 2, 0, 2 * sizeof(unsigned), st));
         KParams P = make_params(c, false);
         void *args[] = {&P};
         const void *fn = c->box ? (const void *)k_cg_stream<true> : (const void *)k_cg_stream<false>;
@@ -3592,6 +3614,7 @@ int bs_run(bs_ctx *c, int batch, int max_launches, void *stream, int64_t *sweeps
             cudaGetLastError();  // SMs held by another context: the graph path computes the same numbers
             c->sgrid = 0;
         } else {
+            c->run_path = 2;
             ++g_launches;
             BS_CU(cudaMemcpyAsync(c->hctl, c->dctl, sizeof(Control), cudaMemcpyDeviceToHost, st));
             BS_CU(cudaStreamSynchronize(st));
@@ -3604,6 +3627,7 @@ int bs_run(bs_ctx *c, int batch, int max_launches, void *stream, int64_t *sweeps
     if (!c->timing) {
         // device-side loop: one graph launch runs the solves to completion
         if (int e = build_graph(c)) return e;
+        c->run_path = 0;
         ++g_launches;
         k_reset_control<<<1, 1, 0, st>>>(c->dctl, max_launches > 0 ? (max_launches + 2) / 3 : 0);
         BS_CU(cudaGraphLaunch(c->graph_exec, st));
@@ -3617,6 +3641,7 @@ int bs_run(bs_ctx *c, int batch, int max_launches, void *stream, int64_t *sweeps
         return BS_OK;
     }
     // launch mode with per-kernel CUDA events (profiling)
+    c->run_path = 3;
     int64_t launched = 0;
     if ((int)c->ev.size() < 6 * batch) {
         for (int i = (int)c->ev.size(); i < 6 * batch; ++i) {
@@ -3876,6 +3901,12 @@ int bs_uniform_pcg64(double *out, int64_t n, uint64_t state_hi, uint64_t state_l
 }
 
 #ifdef BS_TRACE
+int bs_strace_read(unsigned long long *out) {  // PT_SWEEPS x 8 x PT_CTAS (BS_TRACE builds)
+    if (!out) return fail(BS_EINVAL, "bs_strace_read: bad arguments");
+    BS_CU(cudaMemcpyFromSymbol(out, g_strace, sizeof(g_strace)));
+    return BS_OK;
+}
+
 int bs_ptrace_read(unsigned long long *out) {  // PT_SWEEPS x 5 x PT_CTAS
     if (!out) return fail(BS_EINVAL, "bs_ptrace_read: bad arguments");
     BS_CU(cudaMemcpyFromSymbol(out, g_ptrace, sizeof(g_ptrace)));
@@ -4000,6 +4031,8 @@ int bs_read_reports(bs_ctx *c, bs_block_report *out, void *stream) {
         R.r_owned_sq = S.q[2];
         R.rglob_owned_sq = S.q[3];
         R.scale = S.scale;
+        R.last_iterations = S.last_it;
+        R.last_stop_reason = S.last_stop;
     }
     return BS_OK;
 }

@@ -164,15 +164,33 @@ class HaloExchange:
         self.eng.synchronize()
 
 
+def _auto_transport(group=None) -> str:
+    """"p2p" when every rank's GPU can map every other rank's memory (NVLink /
+    NVSwitch peers), else "nccl".  Decided from the gathered device list, so
+    every rank picks the same transport."""
+    dist = torch.distributed
+    if dist.get_backend(group) == "gloo" or not torch.cuda.is_available():
+        return "nccl"
+    dev = torch.cuda.current_device()
+    devs = [None] * dist.get_world_size(group)
+    dist.all_gather_object(devs, dev, group=group)
+    ok = all(a == b or torch.cuda.can_device_access_peer(a, b) for a in devs for b in devs)
+    flags = [None] * len(devs)
+    dist.all_gather_object(flags, bool(ok), group=group)
+    return "p2p" if all(flags) else "nccl"
+
+
 def _default_factory(grid_shape, owned, overlap, local_ids):
     dev = require_cuda(f"cuda:{int(os.environ.get('LOCAL_RANK', torch.cuda.current_device()))}")
     return BlockEngine(grid_shape, owned, overlap, dev, history_cap=1, block_ids=local_ids)
 
 
 def outer_solve_distributed(problem: LinearProblem, config: OuterConfig, group=None,
-                            engine_factory=None, transport: str = "nccl") -> SolveResult:
+                            engine_factory=None, transport: str = "nccl", probe=None) -> SolveResult:
     """Sharded synchronous two-stage solve; every rank returns the same result
-    (solution gathered on every rank)."""
+    (solution gathered on every rank).  ``transport``: "nccl", "p2p" or
+    "auto" (p2p when every pair of the ranks' GPUs has peer access, else
+    nccl).  ``probe``: measurement hooks (``sync_driver.run_sync``)."""
     dist = torch.distributed
     if not dist.is_initialized():
         raise ConfigurationError("distributed: torch.distributed is not initialised")
@@ -203,6 +221,8 @@ def outer_solve_distributed(problem: LinearProblem, config: OuterConfig, group=N
         if engine_factory is not None:
             raise ConfigurationError("distributed: overlap > 0 runs on the device engine")
         return _solve_overlap(config, group, grid, decomp, local_ids, owner, rank, world, b3, bnorm, dens)
+    if transport == "auto":
+        transport = _auto_transport(group)
     factory = engine_factory or _default_factory
     eng = factory(grid.shape, [decomp.owned[g] for g in local_ids], config.overlap, local_ids)
     eng.load_host("b", b3)
@@ -219,7 +239,7 @@ def outer_solve_distributed(problem: LinearProblem, config: OuterConfig, group=N
     t_start = time.perf_counter()
     try:
         trace, per_block, converged, final_true = run_sync(eng, config, dens, bnorm, nb, local_ids, exchange,
-                                                          allreduce_rows, t_start)
+                                                          allreduce_rows, t_start, probe=probe)
         eng.flush()
         sol = torch.zeros(nz, ny, nx, dtype=torch.float64, device=eng.comm_device)
         eng.gather_owned(sol)

@@ -191,6 +191,13 @@ class BlockEngine:
     def num_ctas(self) -> int:
         return self.lib.bs_ctx_num_ctas(self.ctx)
 
+    RUN_PATHS = {-1: "none", 0: "graph", 1: "persistent", 2: "stream", 3: "launch", 4: "jacobi-graph"}
+
+    @property
+    def run_path(self) -> str:
+        """How the last ``run`` drove its solves (bs_ctx_run_path)."""
+        return self.RUN_PATHS.get(self.lib.bs_ctx_run_path(self.ctx), "?")
+
     # -- data movement ----------------------------------------------------
     def load_global(self, name: str, g3: "torch.Tensor") -> None:
         """Scatter a global (nz, ny, nx) device tensor into every block's padded box."""

@@ -226,8 +226,11 @@ def _validate_device_path(config: OuterConfig) -> None:
             f"inner: {config.inner.kind!r} is outside the accelerated path (device kinds: jacobi, cg, gmres)")
 
 
-def outer_solve(problem: LinearProblem, config: OuterConfig) -> SolveResult:
-    """Run the two-stage solve on the GPU and gather the owned values."""
+def outer_solve(problem: LinearProblem, config: OuterConfig, probe=None) -> SolveResult:
+    """Run the two-stage solve on the GPU and gather the owned values.
+
+    ``probe``: optional measurement hooks of the sync sweep loop (see
+    ``sync_driver.run_sync``); results do not depend on it."""
     _validate_device_path(config)
     grid = problem.grid
     nx, ny, nz = grid.shape
@@ -280,7 +283,7 @@ def outer_solve(problem: LinearProblem, config: OuterConfig) -> SolveResult:
         try:
             trace, per_block, converged, final_true = run_sync(
                 eng, config, dens, bnorm, decomp.num_blocks, list(range(decomp.num_blocks)),
-                lambda: eng.halo_pack(plan), lambda table: table, t_start, on_sweep=capture)
+                lambda: eng.halo_pack(plan), lambda table: table, t_start, on_sweep=capture, probe=probe)
             eng.flush()
             sol = torch.empty(nz, ny, nx, dtype=torch.float64, device=dev)
             eng.gather_owned(sol)

@@ -78,6 +78,8 @@ def run_sync(eng, config, dens, bnorm, nblocks, local_ids, exchange, allreduce_r
     arm, solve = make_inner(eng, spec, config)
     if probe is None:
         probe = _NoProbe()
+    if hasattr(probe, "attach"):
+        probe.attach(eng)
     arm()
     probe.begin("solve", 0)
     solve()  # sweep 0: rhs = b (zero halos), x0 = 0
@@ -87,22 +89,26 @@ def run_sync(eng, config, dens, bnorm, nblocks, local_ids, exchange, allreduce_r
     final_true = math.nan
     k = 0
     while True:
-        its_reps = eng.reports()
         if overlap == 0:
+            # one device -> host read per sweep: arm() (k_arm) keeps the solve's
+            # count and stop reason as last_* while it re-arms the blocks
             probe.begin("exchange", k)
             exchange()
             probe.end("exchange", k)
             arm()
             eng.sweep_resid()
+            reps = eng.reports()
+            its_stop = [(r.last_iterations, r.last_stop_reason) for r in reps]
         else:
             eng.flush()
             merge()
             eng.owner_residual()
-        reps = eng.reports()
+            reps = eng.reports()
+            its_stop = [(r.iterations_used, r.stop_reason) for r in reps]
         table = np.zeros((nblocks, 4))
         for li, gid in enumerate(local_ids):
             e = eng_index[li]
-            table[gid] = (its_reps[e].iterations_used, 1.0 if int(its_reps[e].stop_reason) == 3 else 0.0,
+            table[gid] = (its_stop[e][0], 1.0 if int(its_stop[e][1]) == 3 else 0.0,
                           reps[e].r_owned_sq, reps[e].rglob_owned_sq)
         table = allreduce_rows(table)
         broken = np.nonzero(table[:, 1])[0]

@@ -88,6 +88,7 @@ class FakeEngine:
     # solves
     def cg_begin(self, max_iterations, tolerance, basis="rhs", active=None):
         self._params = (max_iterations, tolerance, basis)
+        self._last = (list(self._its), list(self._stop))  # k_arm(PH_INIT) keeps the previous solve's
 
     def run(self, batch=4, max_launches=0):
         its, tol, basis = self._params
@@ -105,8 +106,10 @@ class FakeEngine:
             self._rsq[i] = float(r @ r)
 
     def reports(self):
+        last_its, last_stop = getattr(self, "_last", (self._its, self._stop))
         return [SimpleNamespace(iterations_used=self._its[i], stop_reason=self._stop[i], r_owned_sq=self._rsq[i],
-                                rglob_owned_sq=self._rsq[i]) for i in range(len(self.blocks))]
+                                rglob_owned_sq=self._rsq[i], last_iterations=last_its[i],
+                                last_stop_reason=last_stop[i]) for i in range(len(self.blocks))]
 
     def cancel(self, active=None):
         pass

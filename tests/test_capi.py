@@ -40,7 +40,7 @@ def test_ctypes_signatures_cover_header():
 
 def test_abi_version_and_error_path_without_gpu():
     lib = _lib.load()
-    assert lib.bs_abi_version() == 1
+    assert lib.bs_abi_version() == 2
     # argument validation happens before any CUDA call
     assert lib.bs_ctx_create(0, 0, None, 0, None) == -1
     assert b"bad arguments" in lib.bs_last_error()
@@ -51,4 +51,4 @@ def test_abi_version_and_error_path_without_gpu():
 def test_struct_layout_matches_header():
     # bs_block_desc: 10 int32 (+4 pad) + 5 ptr + 6 ptr + ptr + int32 (+4 pad)
     assert ctypes.sizeof(_lib.BlockDesc) == 40 + 8 * 12 + 8
-    assert ctypes.sizeof(_lib.BlockReport) == 16 + 6 * 8
+    assert ctypes.sizeof(_lib.BlockReport) == 16 + 6 * 8 + 8
