@@ -578,24 +578,11 @@ def run_config2_line(args):
 
 
 def region_sizes(n, block_grid, overlap):
-    """Points of each block's extended region: the owned box dilated `overlap`
-    times by the 7-point stencil (an L1 ball, problems.py:178-190) clipped to
-    the n^3 grid, counted analytically (SURVEY §8 notation N_b)."""
-    from paper_2009_12638_b200.problems import _split_ranges
+    """N_b of every block: its extended region (SURVEY §8 notation)."""
+    from paper_2009_12638_b200.problems import Grid3D, decompose, region_size
 
-    sizes = []
-    gx, gy, gz = block_grid
-    for bz in range(gz):
-        for by in range(gy):
-            for bx in range(gx):
-                counts = []
-                for g, bi in ((gx, bx), (gy, by), (gz, bz)):
-                    lo, hi = _split_ranges(n, g)[bi]
-                    counts.append([hi - lo] + [int(lo - k >= 0) + int(hi - 1 + k < n) for k in range(1, overlap + 1)])
-                cx, cy, cz = counts
-                sizes.append(sum(cx[a] * cy[b] * cz[c] for a in range(overlap + 1) for b in range(overlap + 1)
-                                 for c in range(overlap + 1) if a + b + c <= overlap))
-    return sizes
+    decomp = decompose(Grid3D(n, n, n), block_grid, overlap)
+    return [region_size((n, n, n), box, overlap) for box in decomp.owned]
 
 
 def run_outer_workload(args):

@@ -48,6 +48,9 @@ from .errors import ConfigurationError, SolverBreakdownError
 
 RING_SLOTS_MAX = 8  # without injected delays deeper rings only hold stale planes
 NO_FILTER = (1 << 63) - 1  # receiver_k that accepts every published slot
+# Test hook: called as SWEEP_HOOK(block, k) by a block's thread before it
+# begins sweep k (e.g. to suspend one block for a while; tests only).
+SWEEP_HOOK = None
 
 
 class SendPool:
@@ -290,6 +293,8 @@ def outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, spec, lo
                 estimate = math.inf
                 k = 0
                 while True:
+                    if SWEEP_HOOK is not None:
+                        SWEEP_HOOK(b, k)
                     with board.lock:
                         board.progress[b] = k
                     # freshest delivered payloads (comm.py:401-416); under injected

@@ -285,6 +285,20 @@ def _box_l1_gap(a: Box, b: Box) -> int:
     return gap
 
 
+def region_size(grid_shape, owned: Box, overlap: int) -> int:
+    """Points of a block's extended region — the owned box dilated ``overlap``
+    times by the 7-point stencil (an L1 ball, problems.py:178-190) clipped to
+    the grid — counted analytically: the rows of its block system A_ii."""
+    counts = []
+    for d in range(3):
+        lo, hi, n = owned.lo[d], owned.hi[d], grid_shape[d]
+        # coordinates at L1 distance exactly t outside [lo, hi) on this axis
+        counts.append([hi - lo] + [int(lo - t >= 0) + int(hi - 1 + t < n) for t in range(1, overlap + 1)])
+    cx, cy, cz = counts
+    return sum(cx[a] * cy[b] * cz[c] for a in range(overlap + 1) for b in range(overlap + 1 - a)
+               for c in range(overlap + 1 - a - b))
+
+
 def decompose(grid: Grid3D, block_grid: tuple, overlap: int = 0) -> BlockDecomposition:
     """Analytic ``decompose`` (problems.py:287-359).
 

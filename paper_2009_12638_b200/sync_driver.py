@@ -25,7 +25,8 @@ import time
 import numpy as np
 
 from .engine import launch_bound
-from .errors import SolverBreakdownError
+from .errors import ConfigurationError, SolverBreakdownError
+from .problems import region_size
 
 
 def make_inner(eng, spec, config):
@@ -34,8 +35,14 @@ def make_inner(eng, spec, config):
         # _make_inner_solver (multisplit.py:532-536): one cycle of the configured
         # length unless a restart is given; gmres_solve caps it at n (162)
         restart = spec.restart if spec.restart is not None else spec.max_iterations
-        restart = min(restart, min(bb.padded.size for bb in eng.blocks if bb is not None))
-        eng.gmres_setup(restart)
+        # gmres_solve caps the restart at the block's row count (inner_solvers.py:162)
+        caps = sorted({min(restart, region_size(eng.grid_shape, bb.owned, eng.overlap))
+                       for bb in eng.blocks if bb is not None})
+        if len(caps) > 1:
+            raise ConfigurationError(
+                f"restart: blocks with fewer than {restart} unknowns would restart after {caps[0]} steps while "
+                f"others use {caps[-1]}; the device GMRES runs one restart length per engine")
+        eng.gmres_setup(caps[0])
 
         def arm():
             eng.gmres_begin(spec.max_iterations, spec.tolerance, config.tolerance_basis)

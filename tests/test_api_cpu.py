@@ -207,3 +207,16 @@ def test_block_system_matches_reference(key):
         assert op.nnz == wss[b].a_ii.values.shape[0]
     with pytest.raises(ValueError, match="out of range"):
         bs.block_system(prob, dec, dec.num_blocks)
+
+
+def test_region_size_counts_the_dilated_region():
+    """problems.region_size (rows of a block system, the GMRES restart cap of
+    inner_solvers.py:162) == the oracle's L1-ball mask (= the reference's
+    repeated dilation, pinned in test_oracle_golden)."""
+    from oracle import blocksolve_oracle as O
+    from paper_2009_12638_b200.problems import Grid3D, decompose, region_size
+
+    for n, bg, o in [(12, (2, 2, 2), 2), (16, (2, 2, 2), 2), (10, (2, 1, 1), 1), (13, (3, 1, 2), 3), (6, (1, 1, 1), 0)]:
+        d = decompose(Grid3D(n, n, n), bg, o)
+        for box in d.owned:
+            assert region_size((n, n, n), box, o) == int(O.region_mask((n, n, n), (box.lo, box.hi), o).sum())

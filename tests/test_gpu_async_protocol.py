@@ -1,0 +1,218 @@
+"""Asynchronous halo protocol on the device (comm.py:94-132, 367-418 of the
+reference; its own tests test_acceptance.py:253-306, test_comm.py:159-206).
+
+* a suspended neighbour: posts into its mailbox never block, receives find
+  nothing fresh, the R-slot pool fills and further posts are skipped — and in
+  a full asynchronous solve, one block stalled for hundreds of the others'
+  sweeps does not stop them, and the confirmation round still stops
+  truthfully;
+* the ring invariants over >= 1000 posts per channel under injected delays:
+  applied sequence numbers strictly increase, staleness <= d + 1, pool
+  conservation (in flight + free = R) at every step;
+* torn reads: a sender overwriting a one-slot ring as fast as it can while
+  the receiver copies — the seqlock rejects every overwritten-while-read
+  payload, so an applied halo plane is always one complete post."""
+
+import math
+import threading
+import time
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import blocksolve_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+import paper_2009_12638_b200 as bs  # noqa: E402
+from paper_2009_12638_b200 import _lib, async_driver  # noqa: E402
+from paper_2009_12638_b200.async_driver import NO_FILTER, SendPool, _Mailbox  # noqa: E402
+from paper_2009_12638_b200.engine import BlockEngine  # noqa: E402
+from paper_2009_12638_b200.problems import Box  # noqa: E402
+
+
+def _pair(n=16, nz=8):
+    """Two z-slab engines (one per block, as the async driver keeps them) and
+    the mailbox 0 -> 1 (receiver 1's ghost z-1 plane) and 1 -> 0."""
+    dev = torch.device("cuda", 0)
+    owned = [Box((0, 0, 0), (n, n, nz)), Box((0, 0, nz), (n, n, 2 * nz))]
+    e0 = BlockEngine((n, n, 2 * nz), [owned[0]], 0, dev, history_cap=1)
+    e1 = BlockEngine((n, n, 2 * nz), [owned[1]], 0, dev, history_cap=1)
+    return dev, e0, e1
+
+
+def _post(eng, mb, k, deliver_at, slot, stream):
+    _lib.check(eng.lib.bs_async_post_slot(eng.ctx, 0, mb.post_dir, mb.ring_ptr, mb.seqs_ptr, mb.deliver_ptr,
+                                          slot, 2 * k, deliver_at, stream))
+
+
+def _receive(eng, mb, limit, stream):
+    _lib.check(eng.lib.bs_async_receive_at(eng.ctx, 0, mb.ghost_dir, mb.ring.data_ptr(), mb.seqs.data_ptr(),
+                                           mb.deliver.data_ptr(), mb.R + 1, limit, mb.applied.data_ptr(),
+                                           mb.stage.data_ptr(), mb.torn.data_ptr(), stream))
+
+
+def test_suspended_neighbour_never_blocks():
+    """Block 1 never begins an iteration: block 0 posts 2000 times (fixed
+    delay 1, R = 5) and receives every step — nothing fresh arrives, its halo
+    stays untouched, the pool ends full with every further post skipped, and
+    no call waits (comm.py:376-400; test_comm.py:159-169)."""
+    dev, e0, e1 = _pair()
+    st = e0.stream
+    to1 = _Mailbox(1, 0, 0, e1.blocks[0].ghost[0].numel(), 5, dev)  # 0 -> 1, in 1's memory
+    to0 = _Mailbox(0, 5, 1, e0.blocks[0].ghost[5].numel(), 5, dev)  # 1 -> 0 (1 never posts)
+    pool = SendPool(5, bs.DelayModel("fixed", fixed=1))
+    e0.blocks[0].ghost[5].fill_(7.0)
+    t0 = time.perf_counter()
+    for k in range(2000):
+        pool.reclaim(-1)  # the receiver never began an iteration
+        got = pool.post(k, 1)
+        if got is not None:
+            _post(e0, to1, k, got[1], got[0], st)
+        _receive(e0, to0, k - 1, st)
+        assert pool.free_slots + len(pool.in_flight) == pool.capacity
+    torch.cuda.synchronize()
+    elapsed = time.perf_counter() - t0
+    assert elapsed < 30.0
+    assert len(pool.in_flight) == 5 and pool.free_slots == 0 and pool.skipped == 2000 - 5
+    assert int(to0.applied.item()) == 0 and int(to0.torn.item()) == 0
+    assert torch.all(e0.blocks[0].ghost[5] == 7.0)
+    # the five posts that got a slot are all published in 1's ring
+    assert sorted(int(s) for s in to1.seqs[:5].tolist()) == [1, 3, 5, 7, 9]
+    e0.close()
+    e1.close()
+
+
+@pytest.mark.parametrize("bound", [0, 1, 3])
+def test_ring_invariants_under_injected_delay(bound):
+    """Two blocks exchanging every step for 1200 steps with delays drawn
+    uniformly from 0..bound and R = 4: every applied payload is newer than the
+    last (strictly increasing sequence), never older than bound + 1 sweeps at
+    the receiver, and in flight + free = R after every post
+    (test_acceptance.py:272-306, test_comm.py:171-197)."""
+    dev, e0, e1 = _pair()
+    st = e0.stream
+    engines = (e0, e1)
+    box = {0: _Mailbox(0, 5, 1, e0.blocks[0].ghost[5].numel(), 4, dev),   # 1 -> 0
+           1: _Mailbox(1, 0, 0, e1.blocks[0].ghost[0].numel(), 4, dev)}   # 0 -> 1
+    delay = bs.DelayModel("uniform", low=0, high=bound, seed=8)
+    rng = np.random.default_rng(8)
+    for mb in box.values():
+        mb.pool = SendPool(4, delay)
+    applied = {0: [], 1: []}
+    for k in range(1200):
+        for w in (0, 1):  # receive (deliveries due by k - 1), then post
+            mb = box[w]
+            _receive(engines[w], mb, k - 1, st)
+        seqs = [int(box[w].applied.item()) for w in (0, 1)]
+        for w in (0, 1):
+            if seqs[w]:
+                s = (seqs[w] - 1) // 2
+                if not applied[w] or applied[w][-1][1] != s:
+                    applied[w].append((k, s))
+        for w, other in ((0, 1), (1, 0)):
+            mb = box[other]  # w posts into other's mailbox
+            mb.pool.reclaim(k)
+            got = mb.pool.post(k, delay.draw(rng) if mb.pool.free_slots else 0)
+            if got is not None:
+                _post(engines[w], mb, k, got[1], got[0], st)
+            assert mb.pool.free_slots + len(mb.pool.in_flight) == mb.pool.capacity == 4
+    for w in (0, 1):
+        seq = [s for _, s in applied[w]]
+        assert len(seq) > 200
+        assert all(b > a for a, b in zip(seq, seq[1:]))
+        assert all(k - s <= bound + 1 for k, s in applied[w])
+        assert int(box[w].torn.item()) == 0
+    e0.close()
+    e1.close()
+
+
+def test_torn_reads_are_rejected():
+    """A one-slot ring overwritten continuously by the sender (its own stream
+    and host thread) while the receiver copies: every applied halo plane is
+    one complete post (all cells equal the post's value), sequence numbers
+    never go backwards, and overwritten-while-read copies are counted as
+    torn, not applied."""
+    dev, e0, e1 = _pair(n=256, nz=4)
+    mb = _Mailbox(1, 0, 0, e1.blocks[0].ghost[0].numel(), 1, dev)  # 0 -> 1, R = 1
+    s_send, s_recv = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    stop = threading.Event()
+    errors = []
+
+    def sender():
+        with torch.cuda.stream(s_send):
+            st = e0.stream
+            k = 1
+            while not stop.is_set() and k < 200000:
+                e0.blocks[0].x.fill_(float(k))  # the boundary plane = k (no pending alpha p)
+                _lib.check(e0.lib.bs_async_post_slot(e0.ctx, 0, 5, mb.ring_ptr, mb.seqs_ptr, mb.deliver_ptr, 0,
+                                                     2 * k, 0, st))
+                k += 1
+                if k % 64 == 0:
+                    s_send.synchronize()
+
+    th = threading.Thread(target=sender)
+    th.start()
+    last, applied_count = 0, 0
+    try:
+        with torch.cuda.stream(s_recv):
+            st = e1.stream
+            for _ in range(3000):
+                _receive(e1, mb, NO_FILTER, st)
+                g = e1.blocks[0].ghost[0].cpu()
+                seq = int(mb.applied.item())
+                if seq:
+                    k = (seq - 1) // 2
+                    assert seq >= last
+                    if seq != last:
+                        applied_count += 1
+                    last = seq
+                    vals = torch.unique(g)
+                    if vals.numel() != 1 or float(vals[0]) != float(k):
+                        errors.append((k, vals[:4].tolist()))
+    finally:
+        stop.set()
+        th.join()
+    torch.cuda.synchronize()
+    assert not errors, errors[:3]
+    assert applied_count > 100
+    print(f"applied {applied_count} payloads, rejected {int(mb.torn.item())} torn copies")
+    e0.close()
+    e1.close()
+
+
+def test_suspended_block_in_async_solve(monkeypatch):
+    """Block 3 of eight z-slabs stalls for ~2 s at sweep 5 while the others keep
+    sweeping on its stale halo (hundreds of sweeps: the estimate stays above
+    tol because block 3's published residual is stale, so no confirmation
+    round is requested while it sleeps).  Nobody blocks on it; once it
+    resumes the solve converges, and the confirmed stop is truthful."""
+    n = 32
+    b = O.seeded_rhs(n ** 3, 0)
+    prob = bs.LinearProblem(bs.StencilOperator(n, n, n), b, bs.Grid3D(n, n, n))
+    progress = {}
+    lock = threading.Lock()
+
+    def hook(blk, k):
+        with lock:
+            progress[blk] = k
+        if blk == 3 and k == 5:
+            time.sleep(2.0)
+            with lock:
+                progress["others_during_stall"] = max(v for key, v in progress.items()
+                                                      if isinstance(key, int) and key != 3)
+
+    monkeypatch.setattr(async_driver, "SWEEP_HOOK", hook)
+    tol = 1e-8
+    cfg = bs.OuterConfig(block_grid=(1, 1, 8), inner=bs.InnerSolverSpec("cg", 20), mode="async", tol=tol,
+                         max_outer=200000, residual_check_every=1)
+    res = bs.outer_solve(prob, cfg)
+    assert progress["others_during_stall"] >= 200  # the neighbours swept on meanwhile
+    assert res.converged and res.final_true_residual < tol
+    assert max(r.max_halo_staleness for r in res.trace.rows) >= 100
+    a = O.laplace_csr(n, n, n)
+    tight, _ = O.cg(lambda v: O.csr_spmv(a, v), b, np.zeros(n ** 3), 5000, 1e-13)
+    ro = O.outer_solve_sync((n, n, n), b, (1, 1, 8), 0, dict(kind="cg", max_iterations=20), tol=tol)
+    sync_err = np.linalg.norm(ro.solution - tight) / np.linalg.norm(tight)
+    assert np.linalg.norm(res.solution - tight) / np.linalg.norm(tight) <= 10 * sync_err
