@@ -351,6 +351,192 @@ def outer_solve_slabs(shape, b: np.ndarray, nslabs: int, max_iterations: int, to
     return records
 
 
+class _Frame:
+    """A block's working box for the matrix-free overlap sweep: its owned box
+    grown by overlap + 1 on every side (region, halo and beyond), with the
+    grid, region, owned, halo and shared masks over it, in (z, y, x) order."""
+
+    def __init__(self, shape, box, overlap: int):
+        nx, ny, nz = shape
+        (x0, y0, z0), (x1, y1, z1) = box
+        g = overlap + 1
+        self.lo = (x0 - g, y0 - g, z0 - g)
+        self.hi = (x1 + g, y1 + g, z1 + g)
+        k, j, i = np.meshgrid(np.arange(self.lo[2], self.hi[2]), np.arange(self.lo[1], self.hi[1]),
+                              np.arange(self.lo[0], self.hi[0]), indexing="ij")
+        self.grid = (i >= 0) & (i < nx) & (j >= 0) & (j < ny) & (k >= 0) & (k < nz)
+        d = (np.maximum(0, np.maximum(x0 - i, i - (x1 - 1))) + np.maximum(0, np.maximum(y0 - j, j - (y1 - 1)))
+             + np.maximum(0, np.maximum(z0 - k, k - (z1 - 1))))
+        self.region = self.grid & (d <= overlap)
+        self.owned = self.grid & (d == 0)
+        self.shared = self.region & ~self.owned
+        # halo: in-grid cells outside the region next to it (the coupling columns)
+        near = np.zeros_like(self.region)
+        for axis in range(3):
+            near |= _shift(self.region, axis, -1, False) | _shift(self.region, axis, 1, False)
+        self.halo = self.grid & ~self.region & near
+        self.shape = self.region.shape
+
+    def overlap_slices(self, other: "_Frame"):
+        """(slices into self, slices into other) of the two frames' intersection."""
+        lo = [max(self.lo[d], other.lo[d]) for d in range(3)]
+        hi = [min(self.hi[d], other.hi[d]) for d in range(3)]
+        if any(lo[d] >= hi[d] for d in range(3)):
+            return None
+        mine = tuple(slice(lo[d] - self.lo[d], hi[d] - self.lo[d]) for d in (2, 1, 0))
+        theirs = tuple(slice(lo[d] - other.lo[d], hi[d] - other.lo[d]) for d in (2, 1, 0))
+        return mine, theirs
+
+    def take(self, glob3: np.ndarray) -> np.ndarray:
+        """A global (nz, ny, nx) array over the frame, 0 outside the grid."""
+        nz, ny, nx = glob3.shape
+        out = np.zeros(self.shape)
+        lo = [max(0, self.lo[d]) for d in range(3)]
+        hi = [min((nx, ny, nz)[d], self.hi[d]) for d in range(3)]
+        out[tuple(slice(lo[d] - self.lo[d], hi[d] - self.lo[d]) for d in (2, 1, 0))] = \
+            glob3[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]]
+        return out
+
+
+def coupling_apply(h3: np.ndarray, region: np.ndarray, grid: np.ndarray) -> np.ndarray:
+    """C h matrix-free: for each region row, the couplings to in-grid
+    neighbours outside the region, -h(c), in ascending column order
+    (z-1, y-1, x-1, x+1, y+1, z+1) combined as ``t_first + seq(t_rest)``
+    (the reduceat rule of linalg.py:188-193 on the coupling CSR,
+    multisplit.py:219-228); rows without couplings are 0."""
+    outside = grid & ~region
+    steps = ((0, -1), (1, -1), (2, -1), (2, 1), (1, 1), (0, 1))
+    t = [-_shift(np.where(outside, h3, 0.0), ax, st, 0.0) for ax, st in steps]
+    pres = [_shift(outside, ax, st, False) for ax, st in steps]
+    y = np.zeros_like(h3)
+    for lead in range(5, -1, -1):  # the first present term leads, absent later terms are exact zeros
+        s = t[lead]
+        if lead < 5:
+            rest = t[lead + 1]
+            for q in range(lead + 2, 6):
+                rest = rest + t[q]
+            s = s + rest
+        y = np.where(pres[lead], s, y)
+    return np.where(region, y, 0.0)
+
+
+def outer_solve_boxes(shape, b: np.ndarray, block_grid, overlap: int, inner: dict, sweeps: int,
+                      pool=None, on_sweep=None):
+    """Synchronous two-stage sweep with overlapping box blocks, matrix free —
+    ``outer_solve_sync`` (multisplit.py:544-707, paper mode) for grids whose
+    global CSR does not fit (config 5 at 512^3 / 1024^3).
+
+    Per block, over its frame (``_Frame``): A_ii = ``stencil_apply`` on the
+    region; rhs = b - C halo (``coupling_apply``, multisplit.py:333-338);
+    merge (341-369): halo(c) = (0 + sum of the neighbours' sweep-k values at c,
+    ascending block order) / cover(c), shared(s) = (own + neighbours') /
+    cover(s), owner copies for the residual; local residual (372-396) on the
+    owned rows with shared values replaced by their owners'.  Inner solves
+    see the region's points in ascending global order (the reference's
+    extended ordering).  Runs ``sweeps`` sweeps; one record per sweep."""
+    nx, ny, nz = shape
+    b3 = np.asarray(b, dtype=np.float64).reshape(nz, ny, nx)
+    bnorm = float(np.linalg.norm(b3.ravel()))
+    boxes = owned_boxes(shape, block_grid)
+    frames = [_Frame(shape, box, overlap) for box in boxes]
+    nb = len(boxes)
+    # cover counts over every frame; neighbours = blocks whose region meets
+    # this block's region or halo (dilate(ext, 1) & ext_q, problems.py:343-349)
+    cover = [np.zeros(f.shape) for f in frames]
+    nbrs = [[] for _ in range(nb)]
+    for p_, fp in enumerate(frames):
+        for q, fq in enumerate(frames):
+            sl = fp.overlap_slices(fq)
+            if sl is None:
+                continue
+            mine, theirs = sl
+            cover[p_][mine] += fq.region[theirs]
+            if q != p_ and np.any(fq.region[theirs] & (fp.region[mine] | fp.halo[mine])):
+                nbrs[p_].append(q)
+    owner_of = []  # per frame: index of the block owning each in-grid cell
+    for p_, fp in enumerate(frames):
+        own = np.full(fp.shape, -1)
+        for q, fq in enumerate(frames):
+            sl = fp.overlap_slices(fq)
+            if sl is not None:
+                mine, theirs = sl
+                own[mine] = np.where(fq.owned[theirs], q, own[mine])
+        owner_of.append(own)
+    bb = [f.take(b3) for f in frames]
+    dens = []
+    for p_, f in enumerate(frames):
+        d = float(np.linalg.norm(bb[p_][f.owned]))
+        dens.append(d if d != 0.0 else (bnorm if bnorm != 0.0 else 1.0))
+    xs = [np.zeros(f.shape) for f in frames]
+    halo = [np.zeros(f.shape) for f in frames]
+    kind = inner["kind"]
+    records = []
+    for k in range(sweeps):
+        jobs = []
+        for p_, f in enumerate(frames):
+            rhs = np.where(f.region, bb[p_] - coupling_apply(halo[p_], f.region, f.grid), 0.0)
+            jobs.append((kind, rhs[f.region], xs[p_][f.region], f.region, inner))
+        outs = pool.map(_region_solve, jobs) if pool is not None else [_region_solve(j) for j in jobs]
+        its = []
+        for p_, (xr, it) in enumerate(outs):
+            xs[p_] = np.zeros(frames[p_].shape)
+            xs[p_][frames[p_].region] = xr
+            its.append(it)
+        new_x, owner_halo, owner_shared = [], [], []
+        for p_, f in enumerate(frames):
+            acc_h = np.zeros(f.shape)
+            acc_s = np.where(f.shared, xs[p_], 0.0)
+            own_vals = np.zeros(f.shape)
+            for q in nbrs[p_]:
+                mine, theirs = f.overlap_slices(frames[q])
+                inq = frames[q].region[theirs]
+                xq = xs[q][theirs]
+                sub = acc_h[mine]
+                acc_h[mine] = np.where(inq & f.halo[mine], sub + xq, sub)
+                sub = acc_s[mine]
+                acc_s[mine] = np.where(inq & f.shared[mine], sub + xq, sub)
+                ov = own_vals[mine]
+                own_vals[mine] = np.where(frames[q].owned[theirs] & (f.halo[mine] | f.shared[mine]), xq, ov)
+            halo_new = np.where(f.halo, acc_h / np.where(f.halo, cover[p_], 1.0), 0.0)
+            xn = np.where(f.shared, acc_s / np.where(f.shared, cover[p_], 1.0), xs[p_])
+            new_x.append((halo_new, xn))
+            owner_halo.append(np.where(f.halo, own_vals, 0.0))
+            owner_shared.append(np.where(f.shared, own_vals, 0.0))
+        locals_ = []
+        for p_, f in enumerate(frames):
+            halo[p_], xs[p_] = new_x[p_]
+            xv = np.where(f.shared, owner_shared[p_], xs[p_])
+            r = np.where(f.region, bb[p_] - stencil_apply(xv, f.region), 0.0)
+            r = r - coupling_apply(owner_halo[p_], f.region, f.grid)
+            locals_.append(float(np.linalg.norm(r[f.owned])) / dens[p_])
+        estimate = math.sqrt(float(sum(locals_[w] ** 2 for w in range(nb))))
+        rec = {"k": k, "its": its, "locals": locals_, "estimate": estimate,
+               "owned": [xs[p_][f.owned] for p_, f in enumerate(frames)], "boxes": boxes}
+        records.append(rec)
+        if on_sweep is not None:
+            on_sweep(rec)
+    return records
+
+
+def _region_solve(job):
+    kind, rhs, x0, region, inner = job
+
+    def apply(v):
+        u = np.zeros(region.shape)
+        u[region] = v
+        return stencil_apply(u, region)[region]
+
+    its, tol, basis = inner["max_iterations"], inner.get("tolerance", 0.0), inner.get("basis", "rhs")
+    if kind == "gmres":
+        restart = inner.get("restart") or its
+        x, rep = gmres(apply, rhs, x0, its, tol, restart, basis)
+    else:
+        x, rep = cg(apply, rhs, x0, its, tol, basis)
+    if rep.stop_reason == "breakdown":
+        raise RuntimeError("breakdown in a block solve")
+    return x, rep.iterations_used
+
+
 def _slab_cg(job):
     rhs, x0, max_iterations, tolerance, basis = job
     shape = rhs.shape

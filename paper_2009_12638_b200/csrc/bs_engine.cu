@@ -2297,6 +2297,61 @@ __global__ void __launch_bounds__(NPT) k_point(const KParams P) {
             };
             if (pol2) pass(IntC<2>{});
             else pass(IntC<(BS_MGS_HINT ? 1 : 0)>{});
+        } else if (PKK == PK_FORM) {
+            // x = x + V[:j+1]^T y (inner_solvers.py:173-175), element pairs:
+            // 16-byte loads of x and of 8 basis vectors at a time, all issued
+            // before their adds (the same left-to-right sum per element).  The
+            // coordinates of a thread's pair advance incrementally (no 64-bit
+            // division per element); pairs never straddle a row (pitch % 4 == 0).
+            const int pitch = B.pitch, pdx = B.pdim[0], pdy = B.pdim[1];
+            const double2 *V2 = reinterpret_cast<const double2 *>(V);
+            double2 *x2 = reinterpret_cast<double2 *>(B.x);
+            const long long vs2 = vs / 2;
+            long long e = base + 2 * tid;
+            int lx = (int)(e % pitch);
+            int row = (int)(e / pitch);
+            const double y0 = G.y[0];
+            for (int it = 0; it < PCHUNK / (2 * NPT); ++it, e += 2 * NPT) {
+                if (it) {
+                    lx += 2 * NPT;
+                    while (lx >= pitch) {
+                        lx -= pitch;
+                        ++row;
+                    }
+                }
+                if (e >= n) break;
+                bool in0 = lx < pdx, in1 = lx + 1 < pdx;
+                if (!BOX && (in0 || in1)) {
+                    const int gi = B.plo[0] + lx, gj = B.plo[1] + row % pdy, gk = B.plo[2] + row / pdy;
+                    in0 = in0 && in_region(B, gi, gj, gk);
+                    in1 = in1 && in_region(B, gi + 1, gj, gk);
+                }
+                if (!in0 && !in1) continue;
+                const long long p2 = e / 2;
+                const double2 v0 = __ldcs(V2 + p2);
+                double a0 = mul(v0.x, y0), a1 = mul(v0.y, y0);
+                int k = 1;
+                for (; k + 8 <= j + 1; k += 8) {
+                    double2 v8[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) v8[u] = __ldcs(V2 + (k + u) * vs2 + p2);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const double yk = G.y[k + u];
+                        a0 = add(a0, mul(v8[u].x, yk));
+                        a1 = add(a1, mul(v8[u].y, yk));
+                    }
+                }
+                for (; k <= j; ++k) {
+                    const double2 v = __ldcs(V2 + k * vs2 + p2);
+                    a0 = add(a0, mul(v.x, G.y[k]));
+                    a1 = add(a1, mul(v.y, G.y[k]));
+                }
+                double2 xv = x2[p2];
+                if (in0) xv.x = add(xv.x, a0);
+                if (in1) xv.y = add(xv.y, a1);
+                x2[p2] = xv;
+            }
         } else {
             const int pitch = B.pitch, pdx = B.pdim[0], pdy = B.pdim[1];
             for (int it = 0; it < PCHUNK / NPT; ++it) {
@@ -2306,23 +2361,7 @@ __global__ void __launch_bounds__(NPT) k_point(const KParams P) {
                 if (lx >= pdx) continue;
                 const long long t2 = e / pitch;
                 const int gi = B.plo[0] + lx, gj = B.plo[1] + (int)(t2 % pdy), gk = B.plo[2] + (int)(t2 / pdy);
-                if (PKK == PK_FORM) {  // x = x + V[:j+1]^T y (inner_solvers.py:173-175)
-                    if (!BOX && !in_region(B, gi, gj, gk)) continue;
-                    // same left-to-right sum; the basis loads are issued 8 at a
-                    // time ahead of their adds (one load in flight per thread
-                    // held this pass at ~45% of HBM bandwidth)
-                    double acc_t = mul(V[e], G.y[0]);
-                    int k = 1;
-                    for (; k + 8 <= j + 1; k += 8) {
-                        double v8[8];
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) v8[u] = __ldcs(V + (k + u) * vs + e);
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) acc_t = add(acc_t, mul(v8[u], G.y[k + u]));
-                    }
-                    for (; k <= j; ++k) acc_t = add(acc_t, mul(V[k * vs + e], G.y[k]));
-                    B.x[e] = add(B.x[e], acc_t);
-                } else {  // PK_OWNRES
+                {  // PK_OWNRES
                     // Local residual with owner-canonical values (multisplit.py:372-396):
                     // on owned rows every stencil neighbour is a region point (o >= 1),
                     // so this is b - A x_gathered with x_gathered = each owner's
@@ -3123,6 +3162,10 @@ int bs_ctx_create(int device, int nblocks, const bs_block_desc *blocks, int z_ch
     if (!out || !blocks || nblocks < 1) return fail(BS_EINVAL, "bs_ctx_create: bad arguments");
     bs_ctx *c = new bs_ctx();
     c->device = device;
+    // profiling: BS_LAUNCH_MODE=1 runs every solve in launch mode (one kernel
+    // launch per sweep, CUDA events around each) so that ncu sees the sweep
+    // kernels, which it cannot profile inside conditional CUDA graphs
+    if (const char *e = std::getenv("BS_LAUNCH_MODE")) c->timing = std::atoi(e) != 0;
     c->nblocks = nblocks;
     if (int e = set_dev(c)) {
         delete c;

@@ -93,10 +93,12 @@ def _assert_trace_matches(path, golden_path):
     for g, r in zip(got, ref):
         assert (g.outer_iteration, g.time, g.inner_iterations, g.max_halo_staleness) == \
                (r.outer_iteration, r.time, r.inner_iterations, r.max_halo_staleness)
-        assert g.estimated_residual == pytest.approx(r.estimated_residual, rel=1e-9, abs=1e-15)
+        # reassociated dots move a per-sweep residual by up to ~1e-12 absolute
+        # (tests/test_oracle_envelope.py, the reference against itself)
+        assert g.estimated_residual == pytest.approx(r.estimated_residual, rel=1e-9, abs=5e-12)
         assert (g.true_residual is None) == (r.true_residual is None)
         if r.true_residual is not None:
-            assert g.true_residual == pytest.approx(r.true_residual, rel=1e-9, abs=1e-15)
+            assert g.true_residual == pytest.approx(r.true_residual, rel=1e-9, abs=5e-12)
 
 
 @pytest.mark.gpu
@@ -132,4 +134,4 @@ def test_cli_sweep_matches_reference(tmp_path, capsys):
     for g, r in zip(got[1:], ref[1:]):
         g, r = g.split(","), r.split(",")
         assert g[:3] == r[:3] and g[4] == r[4]
-        assert float(g[3]) == pytest.approx(float(r[3]), rel=1e-9)
+        assert float(g[3]) == pytest.approx(float(r[3]), rel=1e-9, abs=5e-12)

@@ -36,3 +36,30 @@ def test_dot_reassociation_moves_late_inner_counts_only(monkeypatch):
     k_first = next((k for k, (x, y) in enumerate(zip(ra.per_block_inner, rb.per_block_inner)) if x != y), None)
     # identical early on; any divergence only once residuals are tiny
     assert k_first is None or ra.rows[k_first].true_residual is None or k_first > ra.outer_iterations // 2
+
+
+def test_fixed_short_inner_solves_amplify_roundoff(monkeypatch):
+    """Why tests/golden/make_cli_golden.py avoids CG(10) on 12 x 12 x 6 blocks:
+    there a pure dot reassociation moves the reference algorithm's own
+    per-sweep estimates by > 1e-5 relative within 20 sweeps (the outer count
+    stays), while with CG(40) they stay within 1e-9."""
+    n = 12
+    faces = {"z_lo": 1.0, "x_hi": 0.5}
+    b = O.dirichlet_rhs(n, n, n, faces)
+    orig = O.cg
+
+    def cg_pairwise(apply, rhs, x0, its, tol=0.0, basis="rhs"):
+        ap = lambda v: apply(np.asarray(v)).view(_Pairwise)
+        return orig(ap, np.asarray(rhs).view(_Pairwise), np.asarray(x0).view(_Pairwise), its, tol, basis)
+
+    def dev(its):
+        monkeypatch.setattr(O, "cg", orig)
+        ra = O.outer_solve_sync((n, n, n), b, (1, 1, 2), 0, dict(kind="cg", max_iterations=its), tol=1e-6)
+        monkeypatch.setattr(O, "cg", cg_pairwise)
+        rb = O.outer_solve_sync((n, n, n), b, (1, 1, 2), 0, dict(kind="cg", max_iterations=its), tol=1e-6)
+        assert ra.outer_iterations == rb.outer_iterations
+        return max(abs(x.estimated_residual - y.estimated_residual) / x.estimated_residual
+                   for x, y in zip(ra.rows, rb.rows))
+
+    assert dev(10) > 1e-5
+    assert dev(40) < 1e-9

@@ -395,3 +395,59 @@ def test_cfg3_fixture_is_consistent():
         assert s["estimate"] == math.sqrt(float(sum(v ** 2 for v in s["locals"])))
     est = [s["estimate"] for s in m["sweeps"]]
     assert est == sorted(est, reverse=True)
+
+
+# ---------------------------------------------------------------- full-size overlap oracle (config 5 fixture)
+
+
+@pytest.mark.parametrize("case", [
+    (12, (2, 2, 2), 2, dict(kind="gmres", max_iterations=10), {"z_lo": 1.0}),
+    (10, (2, 1, 1), 1, dict(kind="cg", max_iterations=6), None),
+    (12, (2, 2, 2), 0, dict(kind="cg", max_iterations=8), None),
+    (16, (2, 2, 2), 2, dict(kind="gmres", max_iterations=30, tolerance=1e-3, basis="initial"), {"z_lo": 1.0}),
+])
+def test_box_oracle_equals_csr_oracle(case):
+    """outer_solve_boxes (matrix-free frames, coupling_apply) == the CSR
+    outer_solve_sync bit for bit: counts, estimates and iterates."""
+    n, bg, ov, inner, faces = case
+    b = O.dirichlet_rhs(n, n, n, faces) if faces else O.seeded_rhs(n ** 3, 3)
+    res = O.outer_solve_sync((n, n, n), b, bg, ov, inner, tol=1e-30, max_outer=4)
+    recs = O.outer_solve_boxes((n, n, n), b, bg, ov, inner, sweeps=4)
+    for rec, row, its in zip(recs, res.rows, res.per_block_inner):
+        assert rec["its"] == its
+        assert rec["estimate"] == row.estimated_residual
+    sol = np.zeros((n, n, n))
+    for box, xo in zip(recs[-1]["boxes"], recs[-1]["owned"]):
+        (x0, y0, z0), (x1, y1, z1) = box
+        sol[z0:z1, y0:y1, x0:x1] = xo.reshape(z1 - z0, y1 - y0, x1 - x0)
+    assert np.array_equal(sol.ravel(), res.solution)
+
+
+def test_box_oracle_matches_reference_trace():
+    """The matrix-free overlap sweep against the reference's own trace
+    (outer/cfg5_12_o2: 12^3, 2x2x2, overlap 2, fixed GMRES 10 its)."""
+    A, M = arrays(), meta()["outer/cfg5_12_o2"]
+    c = M["case"]
+    n = c["n"]
+    b = O.dirichlet_rhs(n, n, n, c["faces"])
+    recs = O.outer_solve_boxes((n, n, n), b, tuple(c["bg"]), c["ov"],
+                               dict(kind="gmres", max_iterations=c["inner"][1]), sweeps=min(6, M["outer_iterations"]))
+    for rec, ref in zip(recs, M["trace"]):
+        assert sum(rec["its"]) == ref[4]
+        assert rec["estimate"] == pytest.approx(ref[2], rel=1e-10)
+
+
+def test_coupling_apply_is_the_coupling_csr():
+    """coupling_apply == the reference's coupling CSR (oracle build_workspaces,
+    pinned) applied to a wide-range halo vector, bit for bit."""
+    n, bg, ov = 12, (2, 2, 2), 2
+    rng = np.random.default_rng(4)
+    boxes, wss, _, _ = O.build_workspaces((n, n, n), np.zeros(n ** 3), bg, ov)
+    for ws, box in zip(wss, boxes):
+        f = O._Frame((n, n, n), box, ov)
+        h = rng.standard_normal(ws.halo_cols.shape[0]) * np.exp(rng.uniform(-15, 15, ws.halo_cols.shape[0]))
+        ref = O.csr_spmv(ws.coupling, h)
+        glob = np.zeros(n ** 3)
+        glob[ws.halo_cols] = h
+        got = O.coupling_apply(f.take(glob.reshape(n, n, n)), f.region, f.grid)[f.region]
+        assert np.array_equal(got, ref)
