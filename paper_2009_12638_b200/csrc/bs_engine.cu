@@ -97,6 +97,14 @@ constexpr int PITCH_ALIGN = 4;         // doubles
 #ifndef BS_MINBLOCKS
 #define BS_MINBLOCKS (BS_RY == 1 ? 3 : 2)  // resident CTAs per SM the sweep kernels are compiled for
 #endif
+// The residual and point-Jacobi sweeps (four sums, face couplings, two
+// reduceat chains) spill at the 72 registers of 3 CTAs per SM: ncu showed
+// long-scoreboard stalls on the spill reloads as the top stall of a serving
+// residual sweep (profiles/r02_ncu_resid_summary.md).  They are compiled for
+// 2 CTAs per SM (112 registers) instead.
+#ifndef BS_MINBLOCKS_HEAVY
+#define BS_MINBLOCKS_HEAVY 2
+#endif
 
 constexpr int SEG_H = ((SC * 8 + 127) / 128) * 128;  // staged haloed box, 128B aligned
 constexpr int SEG_O = TX * TY * 8;                    // bare tile
@@ -1569,8 +1577,12 @@ __device__ __forceinline__ SweepCtx make_ctx(const KParams &P, int b, const DBlo
 template <int OPK>
 __host__ __device__ constexpr int op_nq() { return OPK == OP_RESID ? NQ : (OPK == OP_JAC ? 2 : 1); }
 
+__host__ __device__ constexpr int op_minblocks(int op) {
+    return (op == OP_RESID || op == OP_JAC) ? BS_MINBLOCKS_HEAVY : BS_MINBLOCKS;
+}
+
 template <int OPK, bool BOX>
-__global__ void __launch_bounds__(NTHR, BS_MINBLOCKS) k_sweep(const KParams P) {
+__global__ void __launch_bounds__(NTHR, op_minblocks(OPK)) k_sweep(const KParams P) {
     extern __shared__ __align__(1024) unsigned char smem[];
     __shared__ double s_red[NQ * NCW];
     __shared__ double s_scratch[256];

@@ -75,7 +75,8 @@ def run_sync(eng, config, dens, bnorm, nblocks, local_ids, exchange, allreduce_r
     ``begin(phase, k)`` / ``end(phase, k)`` bracket the inner solve
     (phase "solve", sweep k) and the halo exchange ("exchange") on the host
     thread that launches them, and whose ``sweep(k, its)`` is called once per
-    completed sweep with the global per-block inner iteration counts.
+    completed sweep with the global per-block inner iteration counts (and
+    ``trace(k, estimate, true_residual, inner_total)``, if it has one).
     """
     spec = config.inner
     overlap = eng.overlap
@@ -129,6 +130,8 @@ def run_sync(eng, config, dens, bnorm, nblocks, local_ids, exchange, allreduce_r
         want_true = config.residual_check_mode == "true" or k % config.true_residual_interval == 0
         now = float(k) if config.execution == "replay" else time.perf_counter() - t_start
         rows.append((k, now, estimate, true_res if want_true else None, int(sum(its))))
+        if hasattr(probe, "trace"):
+            probe.trace(k, estimate, true_res, int(sum(its)))
         if on_sweep is not None:
             on_sweep(k)
         probe.sweep(k, its)

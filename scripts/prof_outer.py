@@ -11,7 +11,7 @@ import torch
 
 sys.path.insert(0, ".")
 import paper_2009_12638_b200 as bs  # noqa: E402
-from bench import OUTER_WORKLOADS  # noqa: E402
+from bench import WORKLOADS as OUTER_WORKLOADS  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "config5"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 256
