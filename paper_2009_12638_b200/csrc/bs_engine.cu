@@ -41,6 +41,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -2261,7 +2262,12 @@ __global__ void __launch_bounds__(NPT) k_point(const KParams P) {
             const bool pol2 = BS_MGS_HINT == 2 && one_block;
             uint64_t pol_keep = 0, pol_drop = 0;
             if (pol2) {
-                pol_keep = l2_policy((int)blockIdx.x >= (int)gridDim.x - BS_MGS_KEEP);
+                // the FINAL pass of a cycle's last step is w's last use in the
+                // cycle (FORM reads V and x, and streams V evict-first): demote
+                // its lines instead of pinning them in L2 for the FORM, the
+                // residual sweep and other blocks' passes
+                const bool last_use = PKK == PK_FINAL && j == S.gm - 1;
+                pol_keep = l2_policy(!last_use && (int)blockIdx.x >= (int)gridDim.x - BS_MGS_KEEP);
                 pol_drop = l2_policy(false);
             }
             // one loop per cache mode (a run-time mode test inside the batch
@@ -2854,7 +2860,9 @@ int encode_map(CUtensorMap *m, const void *ptr, const DBlock &B, bool halo, int 
 
 // ====================================================================== context
 
-static unsigned long long g_launches = 0;  // kernels launched by this library
+// Kernels launched by this library.  Atomic: the asynchronous driver's block
+// threads call into the library concurrently (one context each).
+static std::atomic<unsigned long long> g_launches{0};
 
 struct bs_ctx {
     int device = 0;
@@ -3419,7 +3427,7 @@ int bs_block_pitch(const bs_ctx *c, int block) {
     return c->hblocks[block].pitch;
 }
 
-unsigned long long bs_launch_count(void) { return g_launches; }
+unsigned long long bs_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int bs_timing(bs_ctx *c, int enable, double *ms_out, long long *n_out) {
     if (!c) return fail(BS_EINVAL, "bs_timing: null context");
