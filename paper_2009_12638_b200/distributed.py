@@ -186,7 +186,7 @@ def _default_factory(grid_shape, owned, overlap, local_ids):
 
 
 def outer_solve_distributed(problem: LinearProblem, config: OuterConfig, group=None,
-                            engine_factory=None, transport: str = "nccl", probe=None) -> SolveResult:
+                            engine_factory=None, transport: str = "auto", probe=None) -> SolveResult:
     """Sharded synchronous two-stage solve; every rank returns the same result
     (solution gathered on every rank).  ``transport``: "nccl", "p2p" or
     "auto" (p2p when every pair of the ranks' GPUs has peer access, else
