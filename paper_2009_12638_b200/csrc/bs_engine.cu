@@ -199,10 +199,22 @@ __host__ __device__ constexpr int op_zp(int op) {
 #ifndef BS_NSTAGE_APPLY
 #define BS_NSTAGE_APPLY 20  // ring depth (planes) of the standalone SpMV: nothing but the stencil per plane
 #endif
-__host__ __device__ constexpr int op_stages(int op) {
-    return ((op_has_b(op) ? BS_NSTAGE_AB : op == OP_APPLY ? BS_NSTAGE_APPLY : BS_NSTAGE_A) + op_zp(op) - 1) /
-           op_zp(op);
+// The residual and point-Jacobi sweeps run 2 CTAs per SM (BS_MINBLOCKS_HEAVY),
+// so each can afford a deeper ring than the 3-per-SM CG sweeps.
+#ifndef BS_NSTAGE_RESID
+#define BS_NSTAGE_RESID BS_NSTAGE_AB
+#endif
+#ifndef BS_NSTAGE_JAC
+#define BS_NSTAGE_JAC BS_NSTAGE_A
+#endif
+__host__ __device__ constexpr int op_planes(int op) {
+    return op == OP_RESID   ? BS_NSTAGE_RESID
+           : op == OP_JAC   ? BS_NSTAGE_JAC
+           : op_has_b(op)   ? BS_NSTAGE_AB
+           : op == OP_APPLY ? BS_NSTAGE_APPLY
+                            : BS_NSTAGE_A;
 }
+__host__ __device__ constexpr int op_stages(int op) { return (op_planes(op) + op_zp(op) - 1) / op_zp(op); }
 // stage layout: [A: zp haloed planes][B: zp haloed planes, if any][C: zp bare planes]
 __host__ __device__ constexpr int op_sega(int op) { return ((op_zp(op) * SC * 8 + 127) / 128) * 128; }
 __host__ __device__ constexpr int op_coff(int op) { return op_has_b(op) ? 2 * op_sega(op) : op_sega(op); }
@@ -383,6 +395,23 @@ __device__ __forceinline__ void st_pol(double2 *p, double2 v, uint64_t pol) {
 }
 __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+
+// x / 6 correctly rounded (= __ddiv_rn(x, 6.0), the reference's division by
+// the diagonal, inner_solvers.py:88) without the reciprocal refinement the
+// compiler repeats per division: with z = RN(1/6) (relative error 2^-54),
+// q = RN(x z) is within one ulp of x / 6, the residual e = x - 6 q is exact in
+// one FMA, and RN(q + e z) is the correctly rounded quotient (Markstein's
+// correction step; 6's significand is not all ones).  Zeros, subnormal-range
+// and huge operands take the generic division.
+__device__ __noinline__ double div6_generic(double x) { return __ddiv_rn(x, 6.0); }
+__device__ __forceinline__ double div6(double x) {
+    const unsigned ex = ((unsigned)__double2hiint(x) >> 20) & 0x7ffu;
+    if (ex - 200u > 1600u) return div6_generic(x);
+    const double z = 0x1.5555555555555p-3;
+    const double q = __dmul_rn(x, z);
+    const double e = __fma_rn(-6.0, q, x);
+    return __fma_rn(e, z, q);
+}
 
 // One CSR row of the 7-point operator as numpy's reduceat evaluates it
 // (linalg.py:188-193): present terms in ascending column order
@@ -794,9 +823,11 @@ __device__ int sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, doub
     const bool pend = C.pend, first = C.first;
     const long long pitch = B.pitch;
 
-    auto val = [&](const unsigned char *st, int cell) -> double {
+    // pd: the residual sweep's `pend` flag — the run-time one, or a constant in
+    // the lean rounds below (compiled once per value)
+    auto val_p = [&](const unsigned char *st, int cell, bool pd) -> double {
         const double a = reinterpret_cast<const double *>(st)[cell];
-        if (OP == OP_RESID) return pend ? add(a, mul(alpha_pend, reinterpret_cast<const double *>(st + BOFF)[cell])) : a;
+        if (OP == OP_RESID) return pd ? add(a, mul(alpha_pend, reinterpret_cast<const double *>(st + BOFF)[cell])) : a;
         if (OP == OP_S1) return first ? a : add(a, mul(beta, reinterpret_cast<const double *>(st + BOFF)[cell]));
         return a;
     };
@@ -809,10 +840,13 @@ __device__ int sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, doub
     // region (about 1% of a 514^3 block) takes the analytic path.
     bool easy = BOX;
     // u at (row gj_, x + dx) of plane lz (local z), masked to the region for !BOX
-    auto uval = [&](const unsigned char *st, int cell, int dx, int gj_, int lz) -> double {
-        const double v = val(st, cell);
+    auto uval_p = [&](const unsigned char *st, int cell, int dx, int gj_, int lz, bool pd) -> double {
+        const double v = val_p(st, cell, pd);
         if (BOX || easy) return v;
         return in_region(B, gi + dx, gj_, B.plo[2] + lz) ? v : 0.0;
+    };
+    auto uval = [&](const unsigned char *st, int cell, int dx, int gj_, int lz) -> double {
+        return uval_p(st, cell, dx, gj_, lz, pend);
     };
     int own[RY], gjr[RY];
     bool row_in[RY];
@@ -859,9 +893,16 @@ __device__ int sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, doub
     // FC = std::true_type: a fast round — box region, full tile, and no plane
     // of the round without its z-1 neighbour — so no presence, row or region
     // test is evaluated per plane (only the uniform plane-range guard).
-    auto single_step = [&](auto FC, int q, int s, int sl, int sn, int sln, bool wait_next, uint32_t par_n,
+    // PC: the residual sweep's pend flag as a constant (0 / 1) or -1 = run time.
+    // A fast round of the residual / Jacobi sweeps is *lean*: the round
+    // selection below guarantees that none of its rows has a coupling, so
+    // rhs = b and the global-row residual equals the local one — no face code
+    // at all in the unrolled copy.
+    auto single_step = [&](auto FC, auto PC, int q, int s, int sl, int sn, int sln, bool wait_next, uint32_t par_n,
                            bool release) {
         constexpr bool FR = decltype(FC)::value;
+        constexpr int PK = decltype(PC)::value;
+        const bool pd = PK < 0 ? pend : PK != 0;
         const int lz = lzq0 + DZ * q;
         const unsigned char *st = smem + s * STB + sl * (SC * 8);
         const double *cst = reinterpret_cast<const double *>(smem + s * STB + COFF + sl * SEG_O);
@@ -886,10 +927,10 @@ __device__ int sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, doub
 #pragma unroll
         for (int r = 0; r < RY; ++r) {
             const int gj = gjr[r];
-            xm_[r] = uval(st, own[r] - 1, -1, gj, lz);
-            xp_[r] = uval(st, own[r] + 1, 1, gj, lz);
-            ym_[r] = r > 0 ? u_cur[r > 0 ? r - 1 : 0] : uval(st, own[r] - SX, 0, gj - 1, lz);
-            yp_[r] = r < RY - 1 ? u_cur[r < RY - 1 ? r + 1 : 0] : uval(st, own[r] + SX, 0, gj + 1, lz);
+            xm_[r] = uval_p(st, own[r] - 1, -1, gj, lz, pd);
+            xp_[r] = uval_p(st, own[r] + 1, 1, gj, lz, pd);
+            ym_[r] = r > 0 ? u_cur[r > 0 ? r - 1 : 0] : uval_p(st, own[r] - SX, 0, gj - 1, lz, pd);
+            yp_[r] = r < RY - 1 ? u_cur[r < RY - 1 ? r + 1 : 0] : uval_p(st, own[r] + SX, 0, gj + 1, lz, pd);
             pre_[r] = fast ? add(add(add(add(-ym_[r], -xm_[r]), mul(6.0, u_cur[r])), -xp_[r]), -yp_[r]) : 0.0;
             // reversed: z+1 is the plane behind, so it enters the chain now
             if (REV && fast) pre_[r] = add(pre_[r], -u_prev[r]);
@@ -897,7 +938,8 @@ __device__ int sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, doub
         if (wait_next) mbar_wait(&full[sn], par_n & 1u);
         double u_next[RY];
 #pragma unroll
-        for (int r = 0; r < RY; ++r) u_next[r] = uval(smem + sn * STB + sln * (SC * 8), own[r], 0, gjr[r], lz + DZ);
+        for (int r = 0; r < RY; ++r)
+            u_next[r] = uval_p(smem + sn * STB + sln * (SC * 8), own[r], 0, gjr[r], lz + DZ, pd);
 #pragma unroll
         for (int r = 0; r < RY; ++r) {
             const int ly = ly_0 + r;
@@ -957,6 +999,18 @@ __device__ int sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, doub
                 if (pend)
                     out_x[sxr] = add(cst[ci], mul(alpha_pend, reinterpret_cast<const double *>(st + BOFF)[own[r]]));
                 acc[0] = add(acc[0], mul(u_cur[r], au));
+            } else if (FR) {  // lean round of OP_RESID / OP_JAC: no coupled row, rhs = b
+                const double bv = cst[ci];
+                const double rv = sub(bv, au);
+                acc[0] = add(acc[0], mul(bv, bv));
+                const double r2 = mul(rv, rv);
+                acc[1] = add(acc[1], r2);
+                if (OP == OP_JAC) {
+                    out_p[sxr] = div6(sub(bv, od));
+                } else {
+                    out_r[sxr] = rv;
+                    acc[3] = add(acc[3], r2);  // b - (global row) = rv bit for bit; acc[2]: see the tile's end
+                }
             } else {  // OP_RESID: r = (b - C*halo) - A_ii u ; OP_JAC: also the Jacobi update
                 const double bv = cst[ci];
                 const int gk = B.plo[2] + lz;
@@ -975,7 +1029,7 @@ __device__ int sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, doub
                 const double rv = sub(rhs, au);
                 if (OP == OP_JAC) {
                     // x_{k+1} = (rhs - offd x_k) / d (inner_solvers.py:88) ; ||rhs - A x_k||
-                    out_p[sxr] = __ddiv_rn(sub(rhs, od), 6.0);
+                    out_p[sxr] = div6(sub(rhs, od));
                     acc[0] = add(acc[0], mul(rhs, rhs));
                     acc[1] = add(acc[1], mul(rv, rv));
                 } else {
@@ -984,7 +1038,9 @@ __device__ int sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, doub
                     const double r2 = mul(rv, rv);
                     acc[1] = add(acc[1], r2);
                     if (BOX || in_owned(B, gi, gj, gk)) {
-                        acc[2] = add(acc[2], r2);
+                        // box blocks own every row: acc[2] would repeat acc[1]
+                        // add for add, so it is copied at the tile's end
+                        if (!BOX) acc[2] = add(acc[2], r2);
                         const double rg = sub(bv, rg_au);
                         acc[3] = add(acc[3], mul(rg, rg));
                     }
@@ -1007,6 +1063,18 @@ __device__ int sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, doub
     const bool tile_full = lx0 + TX <= pdx && ly0 + TY <= pdy;
     // the computed plane with lz == 0 (no z-1 neighbour), if the tile has one
     const int q_zero = lz0 == 0 ? (REV ? lz1 : 1) : -1;
+    // Residual / Jacobi sweeps: a fast round must not hold a coupled row
+    // (rhs = b - C*halo, global row != block row).  Couplings sit on block
+    // faces that are not grid faces: the tile's x / y face columns (tile_cpl)
+    // and the planes lz == 0 (q_zero) and lz == pdz - 1 (q_top).
+    constexpr bool LEAN = OP == OP_RESID || OP == OP_JAC;
+    bool tile_cpl = false;
+    int q_top = -1;
+    if constexpr (LEAN && BOX) {
+        tile_cpl = (lx0 == 0 && B.plo[0] > 0) || (lx0 + TX >= pdx && B.plo[0] + pdx < B.gn[0]) ||
+                   (ly0 == 0 && B.plo[1] > 0) || (ly0 + TY >= pdy && B.plo[1] + pdy < B.gn[1]);
+        if (lz1 == pdz && B.plo[2] + pdz < B.gn[2]) q_top = REV ? 1 : nplanes - 2;
+    }
     for (int q0 = -o * ZP; q0 <= nplanes - 2; q0 += NS * ZP, par ^= 1u) {
         constexpr int QR = NS * ZP;  // planes per round
         // measured per op: the CG sweeps take both fast variants; the residual,
@@ -1016,13 +1084,24 @@ __device__ int sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, doub
         constexpr bool FAST_ROUNDS = BOX && OP != OP_APPLY;
         constexpr bool GUARDED_FAST = OP == OP_S1 || OP == OP_S2;
         bool fround = false;
-        if constexpr (FAST_ROUNDS) fround = tile_full && !(q_zero >= q0 && q_zero < q0 + QR);
+        if constexpr (FAST_ROUNDS)
+            fround = tile_full && !(q_zero >= q0 && q_zero < q0 + QR) &&
+                     !(LEAN && (tile_cpl || (q_top >= q0 && q_top < q0 + QR)));
         if (fround && q0 >= 1 && q0 + QR - 1 <= nplanes - 2) {  // interior round: no guards at all
+            if (OP == OP_RESID && pend) {
 #pragma unroll
-            for (int u = 0; u < QR; ++u) {
-                const int un = u + 1;
-                single_step(std::true_type{}, q0 + u, u / ZP, slot(u), (un / ZP) % NS, slot(un), un % ZP == 0,
-                            un == QR ? par ^ 1u : par, u % ZP == ZP - 1);
+                for (int u = 0; u < QR; ++u) {
+                    const int un = u + 1;
+                    single_step(std::true_type{}, IntC<1>{}, q0 + u, u / ZP, slot(u), (un / ZP) % NS, slot(un),
+                                un % ZP == 0, un == QR ? par ^ 1u : par, u % ZP == ZP - 1);
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < QR; ++u) {
+                    const int un = u + 1;
+                    single_step(std::true_type{}, IntC<(OP == OP_RESID ? 0 : -1)>{}, q0 + u, u / ZP, slot(u),
+                                (un / ZP) % NS, slot(un), un % ZP == 0, un == QR ? par ^ 1u : par, u % ZP == ZP - 1);
+                }
             }
         } else if (GUARDED_FAST && fround) {  // first / last round: the uniform plane-range guard only
 #pragma unroll
@@ -1030,7 +1109,7 @@ __device__ int sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, doub
                 const int q = q0 + u;
                 const int un = u + 1;
                 if (q >= 1 && q <= nplanes - 2)
-                    single_step(std::true_type{}, q, u / ZP, slot(u), (un / ZP) % NS, slot(un), un % ZP == 0,
+                    single_step(std::true_type{}, IntC<-1>{}, q, u / ZP, slot(u), (un / ZP) % NS, slot(un), un % ZP == 0,
                                 un == QR ? par ^ 1u : par, u % ZP == ZP - 1);
             }
         } else {
@@ -1039,11 +1118,13 @@ __device__ int sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, doub
                 const int q = q0 + u;
                 const int un = u + 1;
                 if (q >= 1 && q <= nplanes - 2)
-                    single_step(std::false_type{}, q, u / ZP, slot(u), (un / ZP) % NS, slot(un), un % ZP == 0,
+                    single_step(std::false_type{}, IntC<-1>{}, q, u / ZP, slot(u), (un / ZP) % NS, slot(un), un % ZP == 0,
                                 un == QR ? par ^ 1u : par, u % ZP == ZP - 1);
             }
         }
     }
+    // box blocks own every row: the owned-row sum is the all-row sum
+    if (OP == OP_RESID && BOX) acc[2] = acc[1];
     if (tid == 0) BS_STAMP(2);
     if (shared_ring) {
         // release the stages the plane loop did not (the one holding only the

@@ -249,6 +249,40 @@ class BlockEngine:
     def synchronize(self) -> None:
         torch.cuda.current_stream(self.device).synchronize()
 
+    def save_state(self, directory: str) -> None:
+        """Write the outer iterate — every local block's x (pending updates
+        applied) and halo planes — as raw fp64 files: all a synchronous sweep
+        needs to continue (``outer_solve(resume=...)``)."""
+        self.flush()
+        self.synchronize()
+        os.makedirs(directory, exist_ok=True)
+        for i, bb in enumerate(self.blocks):
+            if bb is None:
+                continue
+            gid = self.block_ids[i]
+            bb.x.cpu().numpy().tofile(os.path.join(directory, f"x_{gid}.f64"))
+            for q, g in enumerate(bb.ghost):
+                if g is not None:
+                    g.cpu().numpy().tofile(os.path.join(directory, f"halo_{gid}_{q}.f64"))
+
+    def load_state(self, directory: str) -> None:
+        """Restore what ``save_state`` wrote (same decomposition)."""
+        def read(name, t):
+            a = np.fromfile(os.path.join(directory, name), dtype=np.float64)
+            if a.size != t.numel():
+                raise DeviceError(f"checkpoint {name}: {a.size} values, the block holds {t.numel()}")
+            t.copy_(torch.from_numpy(a))
+
+        for i, bb in enumerate(self.blocks):
+            if bb is None:
+                continue
+            gid = self.block_ids[i]
+            read(f"x_{gid}.f64", bb.x)
+            for q, g in enumerate(bb.ghost):
+                if g is not None:
+                    read(f"halo_{gid}_{q}.f64", g)
+        self.synchronize()
+
     def gather_owned(self, out3: "torch.Tensor", name: str = "x") -> None:
         """Write every block's owned values of ``name`` into a global (nz, ny, nx) tensor."""
         for bb in self.blocks:

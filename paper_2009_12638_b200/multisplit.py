@@ -226,12 +226,18 @@ def _validate_device_path(config: OuterConfig) -> None:
             f"inner: {config.inner.kind!r} is outside the accelerated path (device kinds: jacobi, cg, gmres)")
 
 
-def outer_solve(problem: LinearProblem, config: OuterConfig, probe=None) -> SolveResult:
+def outer_solve(problem: LinearProblem, config: OuterConfig, probe=None, resume=None) -> SolveResult:
     """Run the two-stage solve on the GPU and gather the owned values.
 
     ``probe``: optional measurement hooks of the sync sweep loop (see
-    ``sync_driver.run_sync``); results do not depend on it."""
+    ``sync_driver.run_sync``); results do not depend on it.  ``resume`` =
+    (k, directory): continue a segmented synchronous run (overlap > 0) from
+    the iterate ``BlockEngine.save_state`` wrote after sweep k; the trace of
+    this call then starts at sweep k + 1."""
     _validate_device_path(config)
+    if resume is not None and (config.overlap == 0 or config.mode != "sync"):
+        raise ConfigurationError("resume: segmented runs are implemented for synchronous sweeps over "
+                                 "overlapping decompositions")
     grid = problem.grid
     nx, ny, nz = grid.shape
     decomp = decompose(grid, config.block_grid, config.overlap)
@@ -270,6 +276,8 @@ def outer_solve(problem: LinearProblem, config: OuterConfig, probe=None) -> Solv
         overlap = config.overlap
         eng = BlockEngine(grid.shape, decomp.owned, overlap, dev, history_cap=1)
         eng.load_global("b", b_dev)
+        if resume is not None:
+            eng.load_state(resume[1])
         plan = box_halo_plan(decomp.owned, decomp.block_grid) if overlap == 0 else None
         snapshots = []
 
@@ -283,7 +291,8 @@ def outer_solve(problem: LinearProblem, config: OuterConfig, probe=None) -> Solv
         try:
             trace, per_block, converged, final_true = run_sync(
                 eng, config, dens, bnorm, decomp.num_blocks, list(range(decomp.num_blocks)),
-                lambda: eng.halo_pack(plan), lambda table: table, t_start, on_sweep=capture, probe=probe)
+                lambda: eng.halo_pack(plan), lambda table: table, t_start, on_sweep=capture, probe=probe,
+                resume_k=None if resume is None else resume[0])
             eng.flush()
             sol = torch.empty(nz, ny, nx, dtype=torch.float64, device=dev)
             eng.gather_owned(sol)

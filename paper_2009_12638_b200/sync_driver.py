@@ -61,7 +61,7 @@ def make_inner(eng, spec, config):
 
 
 def run_sync(eng, config, dens, bnorm, nblocks, local_ids, exchange, allreduce_rows, t_start,
-             on_sweep=None, merge=None, eng_index=None, probe=None):
+             on_sweep=None, merge=None, eng_index=None, probe=None, resume_k=None):
     """Run sweeps until the reference's termination rule fires.
 
     ``exchange()`` performs the overlap-0 halo exchange; ``allreduce_rows(a)``
@@ -77,6 +77,13 @@ def run_sync(eng, config, dens, bnorm, nblocks, local_ids, exchange, allreduce_r
     thread that launches them, and whose ``sweep(k, its)`` is called once per
     completed sweep with the global per-block inner iteration counts (and
     ``trace(k, estimate, true_residual, inner_total)``, if it has one).
+
+    Segmented runs (overlap > 0): a probe with ``pause(k) -> bool`` is asked
+    after every sweep that decided to continue; True ends this call there
+    (``probe.paused_at = k``; the outer iterate is the blocks' x and halo
+    planes, ``BlockEngine.save_state``).  ``resume_k`` continues such a run:
+    the engine holds the restored iterate of sweep ``resume_k`` and the next
+    inner solve starts from it, exactly as the uninterrupted loop would.
     """
     spec = config.inner
     overlap = eng.overlap
@@ -88,14 +95,18 @@ def run_sync(eng, config, dens, bnorm, nblocks, local_ids, exchange, allreduce_r
         probe = _NoProbe()
     if hasattr(probe, "attach"):
         probe.attach(eng)
+    k = 0
+    if resume_k is not None:
+        if not overlap:
+            raise ConfigurationError("resume: segmented runs are implemented for overlapping decompositions")
+        k = int(resume_k) + 1
     arm()
-    probe.begin("solve", 0)
+    probe.begin("solve", k)
     solve()  # sweep 0: rhs = b (zero halos), x0 = 0
-    probe.end("solve", 0)
+    probe.end("solve", k)
     rows, per_block = [], []
     converged = False
     final_true = math.nan
-    k = 0
     while True:
         if overlap == 0:
             # one device -> host read per sweep: arm() (k_arm) keeps the solve's
@@ -143,6 +154,9 @@ def run_sync(eng, config, dens, bnorm, nblocks, local_ids, exchange, allreduce_r
         if config.residual_check_mode == "true" and true_res < config.tol:  # 685-686
             converged = True
             eng.cancel()
+            break
+        if overlap and hasattr(probe, "pause") and probe.pause(k):
+            probe.paused_at = k
             break
         if overlap:
             arm()

@@ -394,6 +394,32 @@ def test_outer_sync_gmres_matches_oracle():
     assert np.linalg.norm(res.solution - ro.solution) <= 1e-9 * np.linalg.norm(ro.solution)
 
 
+@pytest.mark.parametrize("kind", ["jacobi", "cg"])
+def test_outer_sync_lean_and_coupled_tiles_against_oracle(kind):
+    """Blocks wide and deep enough (48 x 24 x 40) for full 32 x 8 tiles and unguarded ring rounds: tiles
+    without a coupled face take the lean rounds of the residual / Jacobi sweeps (rhs = b, no face code),
+    tiles on a coupled x / y face and the rounds holding a block's first / last plane the general path.
+    Point-Jacobi inner sweeps are bit-reproducible, so the whole outer iteration is."""
+    shape = (96, 48, 40)
+    b = O.seeded_rhs(shape[0] * shape[1] * shape[2], 5)
+    prob = bs.LinearProblem(bs.StencilOperator(*shape), b, bs.Grid3D(*shape))
+    its = 6 if kind == "jacobi" else 8
+    for bg in ((2, 2, 1), (1, 1, 1)):
+        cfg = bs.OuterConfig(block_grid=bg, inner=bs.InnerSolverSpec(kind, its), tol=1e-30, max_outer=4)
+        res = bs.outer_solve(prob, cfg)
+        ro = O.outer_solve_sync(shape, b, bg, 0, dict(kind=kind, max_iterations=its), tol=1e-30, max_outer=4)
+        assert res.outer_iterations == ro.outer_iterations == 4 and not res.converged
+        assert res.inner_iterations_per_block == ro.per_block_inner
+        for row, ref in zip(res.trace.rows, ro.rows):
+            assert row.estimated_residual == pytest.approx(ref.estimated_residual, rel=1e-9)
+            if ref.true_residual is not None:
+                assert row.true_residual == pytest.approx(ref.true_residual, rel=1e-9)
+        if kind == "jacobi":
+            assert np.array_equal(res.solution, ro.solution)
+        else:
+            assert np.linalg.norm(res.solution - ro.solution) <= 1e-10 * np.linalg.norm(ro.solution)
+
+
 # ------------------------------------------------------------------ async (a9)
 
 
