@@ -200,9 +200,12 @@ __host__ __device__ constexpr int op_zp(int op) {
 #define BS_NSTAGE_APPLY 20  // ring depth (planes) of the standalone SpMV: nothing but the stencil per plane
 #endif
 // The residual and point-Jacobi sweeps run 2 CTAs per SM (BS_MINBLOCKS_HEAVY),
-// so each can afford a deeper ring than the 3-per-SM CG sweeps.
+// so each can afford a deeper ring than the 3-per-SM CG sweeps: the residual
+// sweep at 256^3 takes 90.5 / 83.1 / 80.1 us with 8 / 10 / 12 planes in flight
+// (16 and 20 planes slow the Jacobi sweep down: 83.3 / 93.7 us against 79.3;
+// profiles/r02_ab_lean.log).
 #ifndef BS_NSTAGE_RESID
-#define BS_NSTAGE_RESID BS_NSTAGE_AB
+#define BS_NSTAGE_RESID 12
 #endif
 #ifndef BS_NSTAGE_JAC
 #define BS_NSTAGE_JAC BS_NSTAGE_A

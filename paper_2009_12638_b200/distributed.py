@@ -106,15 +106,21 @@ class HaloExchange:
         lib = _lib.load()
         loc = {g: i for i, g in enumerate(local_ids)}
         mine = {}
-        for d, dr, s in plan.tolist():
-            if owner[d] == self.rank and owner[s] != self.rank:
-                handle = (ctypes.c_ubyte * 64)()
-                off = ctypes.c_uint64(0)
-                _lib.check(lib.bs_ipc_export(ctypes.c_void_p(self.eng.ghost(loc[d], dr).data_ptr()), handle,
-                                             ctypes.byref(off)))
-                mine[(d, dr)] = (bytes(handle), off.value)
+        try:
+            for d, dr, s in plan.tolist():
+                if owner[d] == self.rank and owner[s] != self.rank:
+                    handle = (ctypes.c_ubyte * 64)()
+                    off = ctypes.c_uint64(0)
+                    _lib.check(lib.bs_ipc_export(ctypes.c_void_p(self.eng.ghost(loc[d], dr).data_ptr()), handle,
+                                                 ctypes.byref(off)))
+                    mine[(d, dr)] = (bytes(handle), off.value)
+        except Exception as exc:  # every rank must still reach the collective below
+            mine = {"error": f"rank {self.rank}: {exc}"}
         gathered = [None] * torch.distributed.get_world_size(self.group)
         torch.distributed.all_gather_object(gathered, mine, group=self.group)
+        errors = [part["error"] for part in gathered if "error" in part]
+        if errors:
+            raise RuntimeError("p2p halo transport: exporting halo planes failed: " + "; ".join(errors))
         table = {k: v for part in gathered for k, v in part.items()}
         ops = []
         for kind, peer, li, dr, buf, key in self.ops:
@@ -221,15 +227,36 @@ def outer_solve_distributed(problem: LinearProblem, config: OuterConfig, group=N
         if engine_factory is not None:
             raise ConfigurationError("distributed: overlap > 0 runs on the device engine")
         return _solve_overlap(config, group, grid, decomp, local_ids, owner, rank, world, b3, bnorm, dens)
-    if transport == "auto":
+    auto = transport == "auto"
+    if auto:
         transport = _auto_transport(group)
     factory = engine_factory or _default_factory
     eng = factory(grid.shape, [decomp.owned[g] for g in local_ids], config.overlap, local_ids)
     eng.load_host("b", b3)
-    exchange = HaloExchange(eng, box_halo_plan(decomp.owned, decomp.block_grid), local_ids, owner, rank, group,
-                            transport)
     host_comm = dist.get_backend(group) == "gloo"
     comm_dev = torch.device("cpu") if host_comm else eng.comm_device
+    plan = box_halo_plan(decomp.owned, decomp.block_grid)
+    if auto and transport == "p2p":
+        # "auto" never fails a solve over the transport: if any rank cannot map a
+        # peer's halo planes (every collective of the set-up has completed by
+        # then), all ranks agree to fall back to the batched NCCL exchange
+        exchange, err = None, None
+        try:
+            exchange = HaloExchange(eng, plan, local_ids, owner, rank, group, "p2p")
+        except Exception as exc:
+            err = exc
+        ok = torch.tensor([0 if err is not None else 1], dtype=torch.int32, device=comm_dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if int(ok.item()) == 0:
+            if exchange is not None:
+                exchange.close()
+            if rank == 0:
+                import warnings
+
+                warnings.warn(f"p2p halo transport unavailable ({err or 'failed on another rank'}); using nccl")
+            exchange = HaloExchange(eng, plan, local_ids, owner, rank, group, "nccl")
+    else:
+        exchange = HaloExchange(eng, plan, local_ids, owner, rank, group, transport)
 
     def allreduce_rows(table: np.ndarray) -> np.ndarray:
         t = torch.from_numpy(table).to(comm_dev)
