@@ -1115,6 +1115,22 @@ __device__ int sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, doub
                     single_step(std::true_type{}, IntC<-1>{}, q, u / ZP, slot(u), (un / ZP) % NS, slot(un), un % ZP == 0,
                                 un == QR ? par ^ 1u : par, u % ZP == ZP - 1);
             }
+        } else if (LEAN && BOX && tile_full && !tile_cpl) {
+            // first / last round of an uncoupled full tile of the residual / Jacobi sweeps: only the
+            // planes lz == 0 and a coupled lz == pdz - 1 need the general step, the others are lean
+#pragma unroll
+            for (int u = 0; u < QR; ++u) {
+                const int q = q0 + u;
+                const int un = u + 1;
+                if (q >= 1 && q <= nplanes - 2) {
+                    if (q != q_zero && q != q_top)
+                        single_step(std::true_type{}, IntC<-1>{}, q, u / ZP, slot(u), (un / ZP) % NS, slot(un),
+                                    un % ZP == 0, un == QR ? par ^ 1u : par, u % ZP == ZP - 1);
+                    else
+                        single_step(std::false_type{}, IntC<-1>{}, q, u / ZP, slot(u), (un / ZP) % NS, slot(un),
+                                    un % ZP == 0, un == QR ? par ^ 1u : par, u % ZP == ZP - 1);
+                }
+            }
         } else {
 #pragma unroll
             for (int u = 0; u < QR; ++u) {
@@ -2690,14 +2706,13 @@ __global__ void k_halo_pack(const DBlock *__restrict__ blocks, const DState *sta
         nu = D.pdim[1];
         nv = D.pdim[2];
     }
-    const long long n = (long long)nu * nv;
+    const unsigned n = (unsigned)nu * (unsigned)nv;  // a plane of a block: < 2^31 cells
     const double a = SS.alpha_pend;
     const bool pend = SS.pend != 0;
     const double *p = S.p[SS.pcur];
     const double *xsrc = SS.xin ? S.p[0] : S.x;
-    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < n;
-         c += (long long)gridDim.x * blockDim.x) {
-        const int u = (int)(c % nu), v = (int)(c / nu);
+    for (unsigned c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
+        const int v = (int)(c / (unsigned)nu), u = (int)(c - (unsigned)v * (unsigned)nu);
         int i, j, k;
         switch (dir) {
             case 0: i = D.plo[0] + u; j = D.plo[1] + v; k = D.plo[2] - 1; break;
@@ -2970,6 +2985,7 @@ struct bs_ctx {
     int *dactive = nullptr;
     int *dplan = nullptr;
     int plan_cap = 0;
+    std::vector<int32_t> hplan;  // the plan dplan holds (a sweep loop repeats one plan: no copy per sweep)
     int *hpinned = nullptr;  // [0]: n_active, [1..]: active mask staging
     DState *hstates = nullptr;
     Control *hctl = nullptr;
@@ -4151,8 +4167,14 @@ int bs_halo_pack(bs_ctx *c, int nplan, const int32_t *plan, void *stream) {
         c->dplan = nullptr;
         BS_CU(cudaMalloc(&c->dplan, sizeof(int) * 3 * nplan));
         c->plan_cap = nplan;
+        c->hplan.clear();
     }
-    BS_CU(cudaMemcpyAsync(c->dplan, plan, sizeof(int) * 3 * nplan, cudaMemcpyHostToDevice, st));
+    if (c->hplan.size() != (size_t)(3 * nplan) || memcmp(c->hplan.data(), plan, sizeof(int32_t) * 3 * nplan) != 0) {
+        // the copy stages `plan` before returning (pageable host memory); kernels
+        // already launched with the old plan run before it in stream order
+        BS_CU(cudaMemcpyAsync(c->dplan, plan, sizeof(int) * 3 * nplan, cudaMemcpyHostToDevice, st));
+        c->hplan.assign(plan, plan + 3 * nplan);
+    }
     ++g_launches;
     k_halo_pack<<<dim3(64, nplan), 256, 0, st>>>(c->dblocks, c->dstates, c->dplan);
     BS_CU(cudaGetLastError());

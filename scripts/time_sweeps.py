@@ -1,4 +1,4 @@
-"""CUDA-event times of single sweeps at n^3 (one block): the residual sweep
+"""CUDA-event times of single sweeps at n^3 (or nx ny nz; one block): the residual sweep
 (bs_residual), a point-Jacobi solve of K sweeps, and the GMRES cycle."""
 import sys
 
@@ -9,8 +9,9 @@ import paper_2009_12638_b200 as bs  # noqa: E402
 from paper_2009_12638_b200.linalg import single_block_engine  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 256
-N = n ** 3
-op = bs.StencilOperator(n, n, n)
+shape = (n, int(sys.argv[2]), int(sys.argv[3])) if len(sys.argv) > 3 else (n, n, n)  # nx ny nz
+N = shape[0] * shape[1] * shape[2]
+op = bs.StencilOperator(*shape)
 b = bs.seeded_rhs(N, 0, device="cuda")
 eng = single_block_engine(op, b.device, history_cap=256)
 bb = eng.blocks[0]
