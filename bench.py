@@ -301,7 +301,7 @@ class SweepProbe:
         self.warmup, self.steps = max(1, warmup), steps
         self.barrier = barrier
         self.lib = lib
-        self.pairs = {"solve": [], "exchange": []}
+        self.pairs = {"solve": [], "exchange": [], "resid": []}
         self.open = {}
         self.its = []  # per timed sweep: global per-block counts
         self.t_start = self.t_end = None
@@ -466,6 +466,18 @@ def run_config3(args):
         else:
             halo.update({"achieved_gbs": cross * plane / ex_avg / 1e9, "vs": "NVLink 900 GB/s per direction",
                          "frac": cross * plane / ex_avg / 1e9 / NVLINK_GBS})
+    # where a step goes on this rank: device time of the three phases (CUDA events on the solve's
+    # stream) and the rest — the host round trip per sweep (one report read, the scalar reduction and the
+    # stop decision, with the device idle) plus launch gaps
+    rs = probe.durations_s("resid")
+    step_s = probe.elapsed_s() / len(probe.its)
+    phases = {"inner_solve_ms": 1e3 * kernel_s / len(solve_s_list),
+              "halo_exchange_ms": 1e3 * ex_avg if ex_avg else 0.0,
+              "residual_sweep_ms": 1e3 * sum(rs) / len(rs) if rs else 0.0}
+    rest = 1e3 * step_s - sum(phases.values())
+    breakdown = dict(phases, host_and_gaps_ms=rest, host_and_gaps_share=rest / (1e3 * step_s),
+                     note="per outer sweep on rank 0; residual sweep = re-arm + k_sweep<RESID> (local residual, "
+                          "true residual on owned rows, next rhs / r0)")
     clock = clocks.summary(probe.h0, probe.h1)
     config2 = None
     if world == 1 and not args.no_config2:
@@ -496,7 +508,7 @@ def run_config3(args):
             "solve_rate_gpts": Nb * total_its / solve_s / 1e9,
             "hbm_fraction_solve": Nb * sum(64 * i + 64 for row in res.inner_iterations_per_block for i in row)
             / solve_s / 1e9 / (hbm * world),
-            "roofline": roofline, "halo": halo,
+            "roofline": roofline, "halo": halo, "breakdown": breakdown,
             "cpu_baseline": cpu,
             "e2e": {"value": Nb * total_its / solve_s / 1e9, "unit": UNIT, "h2d_bytes_per_step": N * 8,
                     "d2h_bytes_per_step": N * 8,

@@ -73,7 +73,8 @@ def run_sync(eng, config, dens, bnorm, nblocks, local_ids, exchange, allreduce_r
 
     ``probe`` (measurement only, e.g. ``bench.py``): an object whose
     ``begin(phase, k)`` / ``end(phase, k)`` bracket the inner solve
-    (phase "solve", sweep k) and the halo exchange ("exchange") on the host
+    (phase "solve", sweep k), the halo exchange ("exchange") and the residual
+    sweep with its re-arm ("resid", overlap 0) on the host
     thread that launches them, and whose ``sweep(k, its)`` is called once per
     completed sweep with the global per-block inner iteration counts (and
     ``trace(k, estimate, true_residual, inner_total)``, if it has one).
@@ -114,8 +115,10 @@ def run_sync(eng, config, dens, bnorm, nblocks, local_ids, exchange, allreduce_r
             probe.begin("exchange", k)
             exchange()
             probe.end("exchange", k)
+            probe.begin("resid", k)
             arm()
             eng.sweep_resid()
+            probe.end("resid", k)
             reps = eng.reports()
             its_stop = [(r.last_iterations, r.last_stop_reason) for r in reps]
         else:
