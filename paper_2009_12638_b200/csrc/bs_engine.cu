@@ -1115,22 +1115,6 @@ __device__ int sweep_tile(const SweepCtx &C, int tile, unsigned char *smem, doub
                     single_step(std::true_type{}, IntC<-1>{}, q, u / ZP, slot(u), (un / ZP) % NS, slot(un), un % ZP == 0,
                                 un == QR ? par ^ 1u : par, u % ZP == ZP - 1);
             }
-        } else if (LEAN && BOX && tile_full && !tile_cpl) {
-            // first / last round of an uncoupled full tile of the residual / Jacobi sweeps: only the
-            // planes lz == 0 and a coupled lz == pdz - 1 need the general step, the others are lean
-#pragma unroll
-            for (int u = 0; u < QR; ++u) {
-                const int q = q0 + u;
-                const int un = u + 1;
-                if (q >= 1 && q <= nplanes - 2) {
-                    if (q != q_zero && q != q_top)
-                        single_step(std::true_type{}, IntC<-1>{}, q, u / ZP, slot(u), (un / ZP) % NS, slot(un),
-                                    un % ZP == 0, un == QR ? par ^ 1u : par, u % ZP == ZP - 1);
-                    else
-                        single_step(std::false_type{}, IntC<-1>{}, q, u / ZP, slot(u), (un / ZP) % NS, slot(un),
-                                    un % ZP == 0, un == QR ? par ^ 1u : par, u % ZP == ZP - 1);
-                }
-            }
         } else {
 #pragma unroll
             for (int u = 0; u < QR; ++u) {
