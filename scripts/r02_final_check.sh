@@ -1,12 +1,17 @@
 #!/bin/bash
-# Round-2 final evidence in one GPU call: smoke, every GPU test, the driver's bench command and the reference
-# arm, the ncu launch list of a bounded bench run and --set full captures of the sweeps (scripts/round_bench.sh).
+# Round-2 final evidence: PART=A smoke, every GPU test, the driver's bench command and the reference arm;
+# PART=B the ncu launch list of a bounded bench run and --set full captures of the sweeps (scripts/round_bench.sh).
 cd "${GRAFT_REPO_ROOT:-.}"
 mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > gpurun_out/final_gpu.txt 2>&1
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/final_smoke.log
-timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 900 --durations=10 > gpurun_out/final_pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/final_pytest_gpu.log
-tail -n 3 gpurun_out/final_smoke.log gpurun_out/final_pytest_gpu.log
-TAG=${TAG:-r02v2} bash scripts/round_bench.sh
-tail -c 600 gpurun_out/${TAG:-r02v2}_bench.log; tail -c 300 gpurun_out/${TAG:-r02v2}_ref.log
-ls -la gpurun_out/*.ncu-rep
+TAG=${TAG:-r02v2}
+if [ "${PART:-A}" = "A" ]; then
+  nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > gpurun_out/final_gpu.txt 2>&1
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/final_smoke.log
+  timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 900 --durations=10 > gpurun_out/final_pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/final_pytest_gpu.log
+  tail -n 3 gpurun_out/final_smoke.log gpurun_out/final_pytest_gpu.log
+  TAG=$TAG NO_NCU=1 bash scripts/round_bench.sh
+  tail -c 600 gpurun_out/${TAG}_bench.log; tail -c 300 gpurun_out/${TAG}_ref.log
+else
+  TAG=$TAG NO_BENCH=1 bash scripts/round_bench.sh
+  ls -la gpurun_out/*.ncu-rep; tail -3 gpurun_out/${TAG}_ncu_list.log
+fi
