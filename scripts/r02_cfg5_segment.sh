@@ -9,8 +9,8 @@ df -h /tmp | tail -1 >> gpurun_out/cfg5_seg${SEG}_gpu.txt
 (while true; do nvidia-smi --query-gpu=timestamp,clocks.sm,power.draw,clocks_event_reasons.active --format=csv,noheader >> gpurun_out/cfg5_seg${SEG}_smi.csv; sleep 60; done) &
 SMI=$!
 if [ "$SEG" = "1" ]; then rm -rf /tmp/cfg5_ckpt; R=0; else R=1; fi
-RESUME=$R SEG_BUDGET_S=${SEG_BUDGET_S:-2850} LOG_EVERY=${LOG_EVERY:-25} CKPT_DIR=/tmp/cfg5_ckpt \
-  timeout 3350 python scripts/run_cfg5.py ${CFG5_N:-1024} > gpurun_out/cfg5_seg${SEG}.log 2> gpurun_out/cfg5_seg${SEG}.err
+RESUME=$R SEG_BUDGET_S=${SEG_BUDGET_S:-3250} LOG_EVERY=${LOG_EVERY:-25} CKPT_DIR=/tmp/cfg5_ckpt \
+  timeout 3450 python scripts/run_cfg5.py ${CFG5_N:-1024} > gpurun_out/cfg5_seg${SEG}.log 2> gpurun_out/cfg5_seg${SEG}.err
 echo "rc=$?" >> gpurun_out/cfg5_seg${SEG}.log
 kill $SMI
 ls -la /tmp/cfg5_ckpt | head -40 >> gpurun_out/cfg5_seg${SEG}_gpu.txt
