@@ -4160,7 +4160,9 @@ int bs_halo_pack(bs_ctx *c, int nplan, const int32_t *plan, void *stream) {
         c->hplan.assign(plan, plan + 3 * nplan);
     }
     ++g_launches;
-    k_halo_pack<<<dim3(64, nplan), 256, 0, st>>>(c->dblocks, c->dstates, c->dplan);
+    // 256 CTAs per plane: four cells per thread at 512^2 (the grid-stride loop is a chain of dependent
+    // load -> store rounds, so more threads in flight is what shortens it)
+    k_halo_pack<<<dim3(256, nplan), 256, 0, st>>>(c->dblocks, c->dstates, c->dplan);
     BS_CU(cudaGetLastError());
     return BS_OK;
 }
