@@ -14,6 +14,11 @@ if [ "${PART:-A}" = "A" ]; then
 else
   TAG=$TAG NO_BENCH=1 bash scripts/round_bench.sh
   ls -la gpurun_out/*.ncu-rep; tail -3 gpurun_out/${TAG}_ncu_list.log
+  for lib in libbsgpu.so libbsgpu_prev.so libbsgpu_r8.so; do
+    echo "== $lib" >> gpurun_out/diag_async.log
+    BS_LIB=$PWD/paper_2009_12638_b200/_lib/$lib timeout 120 python scripts/diag_async_stall.py 32 >> gpurun_out/diag_async.log 2>&1
+  done
+  cat gpurun_out/diag_async.log
   for lib in ${HALO_LIBS:-libbsgpu.so libbsgpu_ry2.so libbsgpu.so libbsgpu_ry2.so}; do
     BS_LIB=$PWD/paper_2009_12638_b200/_lib/$lib timeout 600 python bench.py --max-outer 30 --steps 20 --warmup 5 --no-cpu --no-config2 | tail -1 > gpurun_out/halo_ab_$lib.json
     python -c "import json; d=json.load(open('gpurun_out/halo_ab_$lib.json')); print('$lib config3 bounded', round(d['value'],2), 'Gpts/s', round(d['ms_per_step'],2), 'ms/step', round(d['roofline']['frac'],4), 'halo us', round(d['halo']['avg_us'],1), d['breakdown'])" | tee -a gpurun_out/halo_ab.log
