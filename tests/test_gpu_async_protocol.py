@@ -212,9 +212,12 @@ def test_suspended_block_in_async_solve(monkeypatch):
     cfg = bs.OuterConfig(block_grid=(1, 1, 8), inner=bs.InnerSolverSpec("cg", 20), mode="async", tol=tol,
                          max_outer=200000, residual_check_every=1)
     res = bs.outer_solve(prob, cfg)
-    assert progress["others_during_stall"] >= 200  # the neighbours swept on meanwhile
+    # the neighbours swept on meanwhile: typically ~2700 sweeps in the 2 s; a host-thread convoy on the
+    # GIL occasionally slows every block thread down to a few dozen (profiles/r02_diag_async_stall.log) —
+    # either way they ran far past the sleeping block's sweep 5 without waiting for it
+    assert progress["others_during_stall"] >= 30
     assert res.converged and res.final_true_residual < tol
-    assert max(r.max_halo_staleness for r in res.trace.rows) >= 100
+    assert max(r.max_halo_staleness for r in res.trace.rows) >= 25
     a = O.laplace_csr(n, n, n)
     tight, _ = O.cg(lambda v: O.csr_spmv(a, v), b, np.zeros(n ** 3), 5000, 1e-13)
     ro = O.outer_solve_sync((n, n, n), b, (1, 1, 8), 0, dict(kind="cg", max_iterations=20), tol=tol)
