@@ -37,7 +37,6 @@ delayed (comm.py:542-598).
 from __future__ import annotations
 
 import math
-import sys
 import threading
 import time
 
@@ -406,20 +405,11 @@ def outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, spec, lo
         except threading.BrokenBarrierError:
             return True
 
-    # One thread per block, each alternating short Python stretches with GIL-free CUDA calls: with the
-    # interpreter's default 5 ms switch interval a thread coming back from a CUDA call can wait that long
-    # for the GIL, and the block threads occasionally fall into a convoy (measured: 30 ms instead of 0.7 ms
-    # per sweep on small blocks, profiles/r02_diag_async_stall.log).  A short interval keeps hand-overs fast.
-    interval = sys.getswitchinterval()
-    sys.setswitchinterval(min(interval, 2e-4))
-    try:
-        threads = [threading.Thread(target=worker, args=(b,), name=f"block-{b}") for b in local]
-        for t in threads:
-            t.start()
-        for t in threads:
-            t.join()
-    finally:
-        sys.setswitchinterval(interval)
+    threads = [threading.Thread(target=worker, args=(b,), name=f"block-{b}") for b in local]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
     if board.error is not None:
         for eng in engines.values():
             eng.close()
