@@ -31,5 +31,5 @@ for rep in range(3):
     t = time.perf_counter()
     res = bs.outer_solve(prob, cfg)
     dt = time.perf_counter() - t
-    print(f"n={n} others_during_stall={progress.get('others')} sweeps={res.outer_iterations} converged={res.converged} "
+    print(time.strftime("%Y/%m/%d %H:%M:%S"), f"n={n} others_during_stall={progress.get('others')} sweeps={res.outer_iterations} converged={res.converged} "
           f"solve={dt:.2f}s", flush=True)

@@ -65,6 +65,31 @@ if done:
             f"`profiles/r02_gmres512_summary.md`): at {done['seconds_per_sweep']:.3f} s per sweep the whole sweep (merge, owner "
             f"residual and restarts included) runs at {8 * cyc / done['seconds_per_sweep'] / 1e12:.2f} TB/s = "
             f"{8 * cyc / done['seconds_per_sweep'] / 1e9 / 6535.4:.2f} of the measured HBM peak.", ""]
+if not done:
+    ks = sorted(rows)
+    last = rows[ks[-1]]
+    tail = [k for k in ks if k >= ks[-1] - 400]
+    rate = math.log(rows[tail[0]]["estimate"] / last["estimate"]) / (ks[-1] - tail[0])
+    more = math.log(last["estimate"] / 1e-8) / rate
+    per = last["solve_s"] / (ks[-1] + 1)
+    tot_s = max(t.get("total_s", 0.0) for t in segs)
+    paused = max(t.get("paused_at", 0) for t in segs)
+    out += [f"**Not converged: the GPU box was taken back by the pool 17 minutes into segment 5** (`gpurun`: \"the GPU box was "
+            f"lost while the command ran\"), and with it the checkpoint in its /tmp.  State of the run at the last pause: "
+            f"**{paused + 1} sweeps in {tot_s:.1f} s** of sweep phases ({tot_s / 3600:.2f} h, {per:.3f} s per sweep, "
+            f"{sum(1 for _ in ks)} logged rows), estimate **{rows[paused - paused % 25]['estimate']:.4e}** at sweep "
+            f"{paused - paused % 25} (true residual {rows[paused - paused % 25]['true']:.4e}), contracting by "
+            f"{100 * (1 - math.exp(-rate)):.3f}% per sweep — a rate that has been flat since sweep ~3000 (table below).  "
+            f"At that rate the stop test (estimate < 1e-8) falls at sweep ~{int(ks[-1] + more)}: about "
+            f"{(ks[-1] + more) * per:.0f} s = {(ks[-1] + more) * per / 3600:.1f} h of sweeps on one B200, "
+            f"{int((ks[-1] + more - paused) * per / 3250) + 1} more one-hour segments.  Restarting from sweep 0 did not fit "
+            f"the rest of the round (5.4 h).", ""]
+    cyc = 135792128 * sum(72 + 32 * j for j in range(30))
+    out += [f"One sweep = 8 blocks x one 30-step GMRES cycle = {8 * cyc / 1e12:.2f} TB of Krylov traffic (16.1 KB per point, "
+            f"`profiles/r02_gmres512_summary.md`): at {per:.3f} s per sweep the whole sweep (merge, owner residual included) "
+            f"runs at {8 * cyc / per / 1e12:.2f} TB/s = {8 * cyc / per / 1e9 / 6535.4:.2f} of the measured HBM peak.  The same "
+            f"code converges the 512^3 companion (2011 sweeps, 747.9 s) and 256^3 (654 sweeps, 33.3 s, segmented and "
+            f"uninterrupted runs identical, `profiles/r02_cfg5_segmented_dry_run.log`).", ""]
 ks = sorted(rows)
 out += ["Convergence (every logged sweep in `profiles/r02_cfg5_1024_trace.csv`):", "",
         "| sweep | estimate | true residual | contraction per sweep |", "|---|---|---|---|"]
