@@ -297,14 +297,6 @@ def outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, spec, lo
                         SWEEP_HOOK(b, k)
                     with board.lock:
                         board.progress[b] = k
-                    # freshest delivered payloads (comm.py:401-416); under injected
-                    # latency only those due by the last exchange iteration k - 1
-                    limit = k - 1 if delayed else NO_FILTER
-                    for mb in incoming[b]:
-                        _lib.check(lib.bs_async_receive_at(eng.ctx, 0, mb.ghost_dir, mb.ring.data_ptr(),
-                                                           mb.seqs.data_ptr(), mb.deliver.data_ptr(), mb.R + 1,
-                                                           limit, mb.applied.data_ptr(), mb.stage.data_ptr(),
-                                                           mb.torn.data_ptr(), st))
                     begin = eng.cg_begin if spec.kind == "cg" else eng.jacobi_begin
                     begin(spec.max_iterations, spec.tolerance, config.tolerance_basis)
                     eng.run(batch=config.batch, max_launches=launch_bound(spec.max_iterations, config.batch))
@@ -314,6 +306,17 @@ def outer_solve_async(problem, config, decomp, b_dev, dens, bnorm, dev, spec, lo
                     its = int(rep.iterations_used)
                     for mb in outgoing[b]:  # one-sided puts, never blocking (comm.py:380-400)
                         _post(eng, mb, k, st)
+                    # the exchange's receive half, after the solve and the posts as in the reference's
+                    # loop (multisplit.py:575-586): the freshest delivered payloads (comm.py:401-416; under
+                    # injected latency those due by this iteration k) land in the halo planes, so the local
+                    # residual below sees them — evaluated on the halos the solve itself used it would only
+                    # measure the inner solve's accuracy and request confirmation rounds far too early
+                    limit = k if delayed else NO_FILTER
+                    for mb in incoming[b]:
+                        _lib.check(lib.bs_async_receive_at(eng.ctx, 0, mb.ghost_dir, mb.ring.data_ptr(),
+                                                           mb.seqs.data_ptr(), mb.deliver.data_ptr(), mb.R + 1,
+                                                           limit, mb.applied.data_ptr(), mb.stage.data_ptr(),
+                                                           mb.torn.data_ptr(), st))
                     # seq = 2k (sweep post) or 2k+1 (confirm flush): monotonic per channel
                     applied = [(int(mb.applied.item()) - 1) // 2 for mb in incoming[b]]
                     staleness = max([k - a for a in applied if a >= 0] + [0])
