@@ -450,9 +450,10 @@ def test_async_converges_to_the_sync_solution():
 @pytest.mark.parametrize("delay,slots", [(("fixed", 3, 0, 0), 100), (("drop_free_jitter", 0, 1, 4), 100),
                                          (("fixed", 4, 0, 0), 2)])
 def test_async_injected_delay(delay, slots):
-    """DelayModel on real asynchrony (comm.py:51-81, 376-416): payloads are
-    applied no earlier than their delivery iteration, so the observed halo
-    staleness is at least d + 1 sweeps once the pipeline is full; an
+    """DelayModel on real asynchrony (comm.py:51-81, 376-416): a payload posted
+    at sweep j with delay d is applied by the receiver's exchange of an
+    iteration k >= j + d (the exchange follows the solve, multisplit.py:575-586),
+    so the observed halo staleness is at least d sweeps while payloads flow; an
     exhausted R-slot pool skips sends; the solve still converges."""
     n = 16
     b = O.seeded_rhs(n ** 3, 0)
@@ -463,16 +464,17 @@ def test_async_injected_delay(delay, slots):
                          delay=bs.DelayModel(kind, fixed=fixed, low=low, high=high, seed=1))
     res = bs.outer_solve(prob, cfg)
     assert res.converged and res.final_true_residual < 1e-7
-    # staleness = k - (sweep of the applied payload) >= d + 1 while payloads
-    # flow; a confirmation round (triggered by a stale, too-optimistic
-    # estimate) flushes fresh planes and resets it to 0, after which it climbs
-    # back through 1..d.  How many rounds a run takes depends on real thread
-    # timing (measured: 43-60% of rows at >= d + 1 for the 2-slot pool), so
-    # the bound leaves room for that.
+    # staleness = k - (sweep of the applied payload) >= d while payloads flow
+    # (measured: 93-100% of the rows with a 100-slot pool); a confirmation
+    # round flushes fresh planes and resets it to 0, after which it climbs back
+    # through 1..d, and with a pool shallower than the delay most sends are
+    # skipped and confirmation rounds dominate the end of the run — there only
+    # the maximum is asserted.
     dmin = fixed if kind == "fixed" else low
     late = np.array([r.max_halo_staleness for r in res.trace.rows[10:]])
-    assert np.mean(late >= dmin + 1) >= 0.3
-    assert late.max() >= dmin + 1
+    if slots >= dmin + 1:
+        assert np.mean(late >= dmin) >= 0.6
+    assert late.max() >= dmin
     events = dict(res.comm_events)
     if slots < fixed + 1:  # a pool shallower than the delay must skip sends
         assert events["skipped_sends"] > 0
