@@ -96,7 +96,7 @@ out += ["The same configuration at smaller sizes, all converged on one B200 with
         "| 256^3 | 8 x 130^3 | 654 | 156,360 | 6.28e-9 | 33.3 s | 0.051 | `profiles/r02_cfg5_segmented_dry_run.log` |",
         "| 512^3 | 8 x 258^3 | 2011 | 481,268 | 6.32e-9 | 731.1 s | 0.364 | `profiles/r02_cfg5_512_final.log` |",
         "| 640^3 | 8 x 322^3 | 2939 | 703,528 | 6.32e-9 | 2033.0 s | 0.692 | `profiles/r02_cfg5_640.log` |",
-        "| 1024^3 | 8 x 514^3 | 4210 of ~6300-6600 | 1,010,000 so far | 2.6e-7 so far | 12,182 s so far | 2.894 | this file |", ""]
+        "| 1024^3 | 8 x 514^3 | 4210 of ~6300-6600 | ~1.0 M so far | 2.6e-7 so far | 12,182 s so far | 2.894 | this file |", ""]
 ks = sorted(rows)
 out += ["Convergence (every logged sweep in `profiles/r02_cfg5_1024_trace.csv`):", "",
         "| sweep | estimate | true residual | contraction per sweep |", "|---|---|---|---|"]
